@@ -1,0 +1,983 @@
+// kernels.cuh -- SPS phase kernels of libsps.so (sm_100a): data preparation,
+// prior draws (K10), C phase (K2/K3 data tempering, K4 power tempering),
+// S phase (K5 integer resampling + gather), M phase (K6 moments, K7 finalize
+// with Cholesky, K8 propose, K9 accept) and accounting (K11).
+// Citations: PAPER.md line numbers; readings R1..R17 in DESIGN.md.
+#pragma once
+#include "common.cuh"
+
+namespace sps {
+
+enum : int { ERR_NONE = 0, ERR_DATA = 3, ERR_NUMERIC = 4 };
+
+// Device control block: scalars shared between kernels and read back by the host.
+struct Ctl {
+  int h;           // step scale, hundredths (R6)
+  int stop;        // M phase: min RNE >= K after the last step
+  int err;         // sticky error code (ERR_*)
+  int s_star;      // C phase: first crossing observation (1-based), -1 = none in chunk
+  int chol_ridge;  // the last Cholesky needed the ridge retry
+  int pad0;
+  unsigned long long acc;  // accepted proposals, this rank, last step
+  double minrne;   // min monitor RNE after the last step
+  double logml_inc;
+  double dphi;     // power tempering increment of the last C phase
+  double ess;      // ESS at the cycle end (diagnostic)
+  unsigned long long q_lo, q_hi;  // power search bracket on the 2^-48 grid
+  int q_ok_full;   // ESS(1 - phi) >= threshold
+  int pad1;
+};
+
+// ============================================================ data preparation
+// Kernel layout of X: n x ldx.  Binary: row t multiplied by (1 - 2 y_t) (exact
+// sign flip, R17); padding columns zero.  Validates labels and finiteness.
+__global__ void k_prep_X(const double* __restrict__ X, const int32_t* __restrict__ y, int n, int k, int C, int ldx,
+                         double* __restrict__ Xs, Ctl* ctl) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)n * ldx) return;
+  const int t = (int)(idx / ldx), i = (int)(idx % ldx);
+  const int yt = y[t];
+  if (i == 0 && (yt < 0 || yt >= C)) atomicExch(&ctl->err, ERR_DATA);
+  double v = 0.0;
+  if (i < k) {
+    v = X[(int64_t)t * k + i];
+    if (!isfinite(v)) atomicExch(&ctl->err, ERR_DATA);
+    if (C == 2 && yt == 1) v = -v;
+  }
+  Xs[idx] = v;
+}
+
+// Column means xbar of X (default monitors / reported functionals, R12).
+__global__ void k_colmeans(const double* __restrict__ X, int n, int k, double* __restrict__ xbar) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= k) return;
+  double s = 0.0;
+  for (int t = 0; t < n; ++t) s += X[(int64_t)t * k + i];
+  xbar[i] = s / (double)n;
+}
+
+// Default monitor rows (R12): theta_c' xbar for c = 1..C-1, then 1/d each.
+__global__ void k_default_monitors(const double* __restrict__ xbar, int k, int C, double* __restrict__ mon) {
+  const int d = k * (C - 1);
+  for (int idx = threadIdx.x; idx < C * d; idx += blockDim.x) {
+    const int row = idx / d, col = idx % d;
+    double v;
+    if (row < C - 1)
+      v = (col / k == row) ? xbar[col % k] : 0.0;
+    else
+      v = 1.0 / (double)d;
+    mon[idx] = v;
+  }
+}
+
+// In-place Cholesky (lower) of a d x d row-major matrix in shared memory, one
+// block.  Returns false (on all threads) if a pivot is not positive.
+__device__ bool block_cholesky(double* A, int d, int* sflag) {
+  if (threadIdx.x == 0) *sflag = 1;
+  __syncthreads();
+  for (int j = 0; j < d; ++j) {
+    if (threadIdx.x == 0) {
+      const double piv = A[j * d + j];
+      if (!(piv > 0.0) || !isfinite(piv))
+        *sflag = 0;
+      else
+        A[j * d + j] = sqrt(piv);
+    }
+    __syncthreads();
+    if (!*sflag) return false;
+    const double ljj = A[j * d + j];
+    for (int i = j + 1 + threadIdx.x; i < d; i += blockDim.x) A[i * d + j] /= ljj;
+    __syncthreads();
+    const int m = d - j - 1;
+    for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
+      const int i = j + 1 + idx / m, l = j + 1 + idx % m;
+      if (l <= i) A[i * d + l] -= A[i * d + j] * A[l * d + j];
+    }
+    __syncthreads();
+  }
+  for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x)
+    if (idx % d > idx / d) A[idx] = 0.0;
+  __syncthreads();
+  return true;
+}
+
+// Factor the prior covariance (one block; dynamic smem d*d doubles).
+__global__ void k_chol_prior(const double* __restrict__ S, int d, double* __restrict__ L, Ctl* ctl) {
+  extern __shared__ double sA[];
+  __shared__ int flag;
+  for (int i = threadIdx.x; i < d * d; i += blockDim.x) sA[i] = S[i];
+  __syncthreads();
+  const bool ok = block_cholesky(sA, d, &flag);
+  if (!ok) {
+    if (threadIdx.x == 0) ctl->err = ERR_NUMERIC;
+    return;
+  }
+  for (int i = threadIdx.x; i < d * d; i += blockDim.x) L[i] = sA[i];
+}
+
+// g-prior helper (R9): XtX = X'X (k x k), one thread per entry.
+__global__ void k_xtx(const double* __restrict__ X, int n, int k, double* __restrict__ out) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= k * k) return;
+  const int a = idx / k, b = idx % k;
+  double s = 0.0;
+  for (int t = 0; t < n; ++t) s += X[(int64_t)t * k + a] * X[(int64_t)t * k + b];
+  out[idx] = s;
+}
+
+// Sigma = g T (X'X)^-1 by Cholesky solves (one block), expanded to the
+// normalized d x d prior covariance: block (i, j) = (i == j ? 2 : 1) Sigma.
+__global__ void k_g_prior(const double* __restrict__ XtX, int n, int k, int C, double g, double* __restrict__ cov,
+                          Ctl* ctl) {
+  extern __shared__ double sA[];  // k*k factor + k*k inverse
+  __shared__ int flag;
+  double* inv = sA + k * k;
+  for (int i = threadIdx.x; i < k * k; i += blockDim.x) sA[i] = XtX[i];
+  __syncthreads();
+  if (!block_cholesky(sA, k, &flag)) {
+    if (threadIdx.x == 0) ctl->err = ERR_DATA;
+    return;
+  }
+  for (int b = threadIdx.x; b < k; b += blockDim.x) {  // column b of the inverse
+    for (int i = 0; i < k; ++i) {
+      double t = (i == b) ? 1.0 : 0.0;
+      for (int j = 0; j < i; ++j) t -= sA[i * k + j] * inv[j * k + b];
+      inv[i * k + b] = t / sA[i * k + i];
+    }
+    for (int i = k - 1; i >= 0; --i) {
+      double t = inv[i * k + b];
+      for (int j = i + 1; j < k; ++j) t -= sA[j * k + i] * inv[j * k + b];
+      inv[i * k + b] = t / sA[i * k + i];
+    }
+  }
+  __syncthreads();
+  const int d = k * (C - 1);
+  for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) {
+    const int r = idx / d, c = idx % d;
+    const double s = g * (double)n * inv[(r % k) * k + (c % k)];
+    cov[idx] = (r / k == c / k) ? 2.0 * s : s;
+  }
+}
+
+// ============================================================ prior draws / proposals
+// Prior kernel lp = -1/2 |Lprior^-1 (theta - mu)|^2, forward
+// substitution with Lprior in shared memory.
+template <int DMAX>
+__device__ __forceinline__ double prior_quad(const double* th, const double* sLp, const double* mu, int d) {
+  double w[DMAX];
+  double q = 0.0;
+#pragma unroll
+  for (int i = 0; i < DMAX; ++i) {
+    if (i < d) {
+      double t = th[i] - mu[i];
+#pragma unroll
+      for (int j = 0; j < i; ++j) t -= sLp[i * d + j] * w[j];
+      w[i] = t / sLp[i * d + i];
+      q += w[i] * w[i];
+    }
+  }
+  return -0.5 * q;
+}
+
+// K10 (Algorithm 1 step 1): theta = mu + Lprior z, z from the
+// INIT stream of global particle id (R15); lp; L = 0.
+// K8 (Algorithm 2 step 2(c)i): theta* = theta + Lprop z, z from
+// the PROPOSAL stream (id = global particle, step = global M-step index); lp*.
+template <int DMAX, bool INIT>
+__global__ void __launch_bounds__(128) k_draw(const double* __restrict__ base, const double* __restrict__ Lz,
+                                              const double* __restrict__ Lprior, const double* __restrict__ mu, int d,
+                                              int64_t P, int64_t p0, uint64_t seed, uint32_t step, uint32_t pass,
+                                              double* __restrict__ out, double* __restrict__ lp_out,
+                                              Ctl* ctl, const int* __restrict__ stop) {
+  extern __shared__ double sm[];
+  if (stop && *stop) return;
+  double* sL = sm;              // d x d draw factor
+  double* sLp = sm + d * d;     // d x d prior factor
+  double* smu = sm + 2 * d * d; // d
+  for (int i = threadIdx.x; i < d * d; i += blockDim.x) {
+    sL[i] = Lz[i];
+    sLp[i] = Lprior[i];
+  }
+  for (int i = threadIdx.x; i < d; i += blockDim.x) smu[i] = mu[i];
+  __syncthreads();
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  const uint32_t gid = (uint32_t)(p0 + p);
+  double z[DMAX], th[DMAX];
+#pragma unroll
+  for (int i = 0; i < DMAX; i += 2) {
+    if (i < d) {
+      double z0, z1;
+      normal_pair(seed, (uint32_t)(i / 2), gid, step, INIT ? TAG_INIT : TAG_PROPOSAL, pass, &z0, &z1);
+      z[i] = z0;
+      if (i + 1 < DMAX) z[i + 1] = z1;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < DMAX; ++i) {
+    if (i < d) {
+      double s = INIT ? smu[i] : base[p * d + i];
+#pragma unroll
+      for (int j = 0; j <= i; ++j) s = fma(sL[i * d + j], z[j], s);
+      th[i] = s;
+    }
+  }
+  double chk = 0.0;
+#pragma unroll
+  for (int i = 0; i < DMAX; ++i)
+    if (i < d) {
+      out[p * d + i] = th[i];
+      chk += th[i];
+    }
+  if (!isfinite(chk)) atomicExch(&ctl->err, ERR_NUMERIC);
+  lp_out[p] = prior_quad<DMAX>(th, sLp, smu, d);
+}
+
+// K9 accept (R16): L* = sum of chunk partials; delta =
+// temper (L* - L) + (lp* - lp); accept iff plog(u) < delta, u the ACCEPT
+// uniform of (global particle, M-step).  Counts accepts; flags non-finite L*.
+__global__ void __launch_bounds__(256) k_accept(double* __restrict__ theta, double* __restrict__ L,
+                                                double* __restrict__ lp, const double* __restrict__ theta_s,
+                                                const double* __restrict__ part, int nchunks,
+                                                const double* __restrict__ lp_s, int d, int64_t P, int64_t p0,
+                                                double temper, uint64_t seed, uint32_t step, uint32_t pass, Ctl* ctl,
+                                                const int* __restrict__ stop) {
+  __shared__ long long scratch[32];
+  if (stop && *stop) return;
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  long long acc = 0;
+  if (p < P) {
+    double Ls = part[p];
+    for (int c = 1; c < nchunks; ++c) Ls += part[(int64_t)c * P + p];
+    if (!isfinite(Ls)) atomicExch(&ctl->err, ERR_NUMERIC);
+    const double delta = temper * (Ls - L[p]) + (lp_s[p] - lp[p]);
+    const u4 w = stream_block(seed, 0u, (uint32_t)(p0 + p), step, TAG_ACCEPT, pass);
+    if (plog(u01(w.x, w.y)) < delta) {
+      acc = 1;
+      for (int i = 0; i < d; ++i) theta[p * d + i] = theta_s[p * d + i];
+      L[p] = Ls;
+      lp[p] = lp_s[p];
+    }
+  }
+  acc = block_sum(acc, scratch);
+  if (threadIdx.x == 0 && acc) atomicAdd(&ctl->acc, (unsigned long long)acc);
+}
+
+// ============================================================ M phase moments (K6)
+// Grid (nblk, ceil(ntri / MOM_ENT)): block x = `pp` consecutive particles of one
+// group, block y = a range of MOM_ENT lower-triangle entries.  Outputs per
+// block the group-sum partial (d; y == 0 only) and the shifted second-moment
+// partial sum (theta - c)(theta - c)' over its particles, c = shift.
+constexpr int MOM_TILE = 64;
+constexpr int MOM_ENT = 1024;  // 4 entries per thread at 256 threads
+__global__ void __launch_bounds__(256) k_moments_partial(const double* __restrict__ theta, int d, int pp,
+                                                         const double* __restrict__ shift,
+                                                         double* __restrict__ gpart, double* __restrict__ mpart,
+                                                         const int* __restrict__ stop) {
+  extern __shared__ double sm[];
+  if (stop && *stop) return;
+  double* tile = sm;  // MOM_TILE x d, centered
+  const int ntri = d * (d + 1) / 2;
+  const int64_t pstart = (int64_t)blockIdx.x * pp;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  int ei[4], el[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int e = blockIdx.y * MOM_ENT + threadIdx.x + q * blockDim.x;
+    int i = 0;
+    while ((i + 1) * (i + 2) / 2 <= e) ++i;
+    ei[q] = e < ntri ? i : -1;
+    el[q] = e < ntri ? e - i * (i + 1) / 2 : 0;
+  }
+  double gsum = 0.0;
+  const bool do_g = blockIdx.y == 0 && threadIdx.x < d;
+  for (int base = 0; base < pp; base += MOM_TILE) {
+    const int cnt = min(MOM_TILE, pp - base);
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < cnt * d; idx += blockDim.x) {
+      const int r = idx / d, c = idx % d;
+      tile[idx] = theta[(pstart + base + r) * d + c] - shift[c];
+    }
+    __syncthreads();
+    if (do_g)
+      for (int r = 0; r < cnt; ++r) gsum += tile[r * d + threadIdx.x];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (ei[q] >= 0) {
+        const int i = ei[q], l = el[q];
+        double s = acc[q];
+        for (int r = 0; r < cnt; ++r) s = fma(tile[r * d + i], tile[r * d + l], s);
+        acc[q] = s;
+      }
+    }
+  }
+  // group-sum partial is of (theta - c): add back pp * c
+  if (do_g) gpart[(int64_t)blockIdx.x * d + threadIdx.x] = gsum + (double)pp * shift[threadIdx.x];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (ei[q] >= 0) mpart[(int64_t)blockIdx.x * ntri + blockIdx.y * MOM_ENT + threadIdx.x + q * blockDim.x] = acc[q];
+}
+
+// Reduce block partials (block order) into this rank's packed stats slice:
+// [J_local x d group sums | d x d second moment (full, symmetric) | acc | err].
+__global__ void k_moments_reduce(const double* __restrict__ gpart, const double* __restrict__ mpart, int nblk,
+                                 int blk_per_group, int Jl, int d, Ctl* ctl, double* __restrict__ slice,
+                                 const int* __restrict__ stop) {
+  if (stop && *stop) return;
+  const int ntri = d * (d + 1) / 2;
+  const int total = Jl * d + ntri;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+    if (idx < Jl * d) {
+      const int j = idx / d, c = idx % d;
+      double s = 0.0;
+      for (int b = 0; b < blk_per_group; ++b) s += gpart[(int64_t)(j * blk_per_group + b) * d + c];
+      slice[idx] = s;
+    } else {
+      const int e = idx - Jl * d;
+      double s = 0.0;
+      for (int b = 0; b < nblk; ++b) s += mpart[(int64_t)b * ntri + e];
+      int i = 0;
+      while ((i + 1) * (i + 2) / 2 <= e) ++i;
+      const int l = e - i * (i + 1) / 2;
+      slice[Jl * d + i * d + l] = s;
+      slice[Jl * d + l * d + i] = s;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    slice[Jl * d + d * d] = (double)ctl->acc;
+    slice[Jl * d + d * d + 1] = (double)ctl->err;
+  }
+}
+
+struct FinArgs {
+  const double* gath;  // G slices of `slice_len` doubles (rank order)
+  int G, slice_len;
+  int J, Jl, N, d;
+  double* shift;       // in: c used by the moments; out: new c = theta-bar
+  double* Lprop;       // out: chol((h/100) V)
+  double* V;           // out: pooled covariance (d x d)
+  const double* mon;   // monitors (nmon x d)
+  int nmon;
+  int mode;            // 0: moments of resampled particles (no h / RNE); 1: after an M step
+  double K;            // RNE target
+  int h_step, h_min, h_max;
+  double accept_target;
+  Ctl* ctl;
+  const int* stop_in;  // skip if already stopped (speculative launches)
+  double* rne_out;     // nmon RNEs (may be null)
+};
+
+// K7 (Algorithm 2 step 2(c)): theta-bar and pooled V (R11) from
+// the gathered stats; h update from the pooled acceptance (ii, R6); monitor
+// RNEs and the stop flag (iii, R12, R14); Cholesky of (h/100) V with one ridge
+// retry (R13).  One block; every rank computes the identical result.
+__global__ void __launch_bounds__(256) k_finalize(FinArgs f) {
+  extern __shared__ double sm[];
+  __shared__ int flag;
+  __shared__ double red[32];
+  if (f.stop_in && *f.stop_in) return;
+  const int d = f.d;
+  double* sV = sm;             // d x d
+  double* sbar = sm + d * d;   // d
+  double* sA = sbar + d;       // d x d (Cholesky work)
+  double* sg = sA + d * d;     // J (monitor group means)
+  const double P = (double)f.J * (double)f.N;
+  const int gs_len = f.Jl * d;
+  // theta-bar from group sums in group order
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < f.J; ++j) {
+      const int r = j / f.Jl, jl = j % f.Jl;
+      s += f.gath[(int64_t)r * f.slice_len + jl * d + i];
+    }
+    sbar[i] = s / P;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) {
+    const int i = idx / d, l = idx % d;
+    double m = 0.0;
+    for (int r = 0; r < f.G; ++r) m += f.gath[(int64_t)r * f.slice_len + gs_len + idx];
+    const double ci = sbar[i] - f.shift[i], cl = sbar[l] - f.shift[l];
+    sV[idx] = (m - P * ci * cl) / (P - 1.0);
+  }
+  __syncthreads();
+  int h = f.ctl->h;
+  if (f.mode == 1) {
+    if (threadIdx.x == 0) {
+      double acc = 0.0, err = 0.0;
+      for (int r = 0; r < f.G; ++r) {
+        acc += f.gath[(int64_t)r * f.slice_len + gs_len + d * d];
+        err = fmax(err, f.gath[(int64_t)r * f.slice_len + gs_len + d * d + 1]);
+      }
+      if (err > 0.0) f.ctl->err = (int)err;
+      h = (acc > f.accept_target * P) ? min(h + f.h_step, f.h_max) : max(h - f.h_step, f.h_min);
+      f.ctl->h = h;
+    }
+    // RNE of each monitor a: gbar_j = a'S_j / N, gbar = a' theta-bar,
+    // vhat = N/(J-1) sum_j (gbar_j - gbar)^2, var = (P-1)/P a'V a
+    double minrne = INFINITY;
+    for (int m = 0; m < f.nmon; ++m) {
+      const double* a = f.mon + (int64_t)m * d;
+      for (int j = threadIdx.x; j < f.J; j += blockDim.x) {
+        const int r = j / f.Jl, jl = j % f.Jl;
+        const double* S = f.gath + (int64_t)r * f.slice_len + jl * d;
+        double s = 0.0;
+        for (int i = 0; i < d; ++i) s = fma(a[i], S[i], s);
+        sg[j] = s / (double)f.N;
+      }
+      __syncthreads();
+      double gbar_part = 0.0;
+      for (int j = threadIdx.x; j < f.J; j += blockDim.x) gbar_part += sg[j];
+      const double gbar = block_sum(gbar_part, red) / (double)f.J;
+      double dev = 0.0;
+      for (int j = threadIdx.x; j < f.J; j += blockDim.x) dev += (sg[j] - gbar) * (sg[j] - gbar);
+      dev = block_sum(dev, red);
+      double quad = 0.0;
+      for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) quad += a[idx / d] * sV[idx] * a[idx % d];
+      quad = block_sum(quad, red);
+      const double vhat = (double)f.N / (double)(f.J - 1) * dev;
+      const double var = quad * (P - 1.0) / P;
+      const double rne = vhat > 0.0 ? var / vhat : INFINITY;
+      if (f.rne_out && threadIdx.x == 0) f.rne_out[m] = rne;
+      minrne = fmin(minrne, rne);
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      f.ctl->minrne = minrne;
+      f.ctl->stop = minrne >= f.K ? 1 : 0;
+    }
+  }
+  __syncthreads();
+  h = f.ctl->h;
+  const double hd = (double)h / 100.0;
+  for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) {
+    f.V[idx] = sV[idx];
+    sA[idx] = hd * sV[idx];
+  }
+  __syncthreads();
+  bool ok = block_cholesky(sA, d, &flag);
+  if (threadIdx.x == 0) f.ctl->chol_ridge = ok ? 0 : 1;
+  if (!ok) {
+    double tr = 0.0;
+    for (int i = 0; i < d; ++i) tr += sV[i * d + i];
+    const double ridge = 1e-8 * tr / (double)d;
+    for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x)
+      sA[idx] = hd * (sV[idx] + ((idx / d == idx % d) ? ridge : 0.0));
+    __syncthreads();
+    ok = block_cholesky(sA, d, &flag);
+    if (!ok) {
+      if (threadIdx.x == 0) f.ctl->err = ERR_NUMERIC;
+      return;
+    }
+  }
+  for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) f.Lprop[idx] = sA[idx];
+  for (int i = threadIdx.x; i < d; i += blockDim.x) f.shift[i] = sbar[i];
+}
+
+// Reported functional moments (K11) from the gathered
+// stats: mean, sd, NSE = [vhat/(JN)]^1/2 (R2), RNE.  One block.
+__global__ void __launch_bounds__(256) k_functional_stats(const double* __restrict__ gath, int G, int slice_len, int J,
+                                                          int Jl, int N, int d, const double* __restrict__ shift,
+                                                          const double* __restrict__ A, int m,
+                                                          double* __restrict__ out /* m x 4 */) {
+  extern __shared__ double sm[];
+  __shared__ double red[32];
+  double* sbar = sm;
+  double* sg = sm + d;
+  const double P = (double)J * (double)N;
+  const int gs_len = Jl * d;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < J; ++j) s += gath[(int64_t)(j / Jl) * slice_len + (j % Jl) * d + i];
+    sbar[i] = s / P;
+  }
+  __syncthreads();
+  for (int q = 0; q < m; ++q) {
+    const double* a = A + (int64_t)q * d;
+    for (int j = threadIdx.x; j < J; j += blockDim.x) {
+      const double* S = gath + (int64_t)(j / Jl) * slice_len + (j % Jl) * d;
+      double s = 0.0;
+      for (int i = 0; i < d; ++i) s = fma(a[i], S[i], s);
+      sg[j] = s / (double)N;
+    }
+    __syncthreads();
+    double gp = 0.0;
+    for (int j = threadIdx.x; j < J; j += blockDim.x) gp += sg[j];
+    const double gbar = block_sum(gp, red) / (double)J;
+    double dev = 0.0;
+    for (int j = threadIdx.x; j < J; j += blockDim.x) dev += (sg[j] - gbar) * (sg[j] - gbar);
+    dev = block_sum(dev, red);
+    // sum_p (g - gbar)^2 = a' [M - P (bar - c)(bar - c)'] a
+    double quad = 0.0;
+    for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) {
+      const int i = idx / d, l = idx % d;
+      double mm = 0.0;
+      for (int r = 0; r < G; ++r) mm += gath[(int64_t)r * slice_len + gs_len + idx];
+      mm -= P * (sbar[i] - shift[i]) * (sbar[l] - shift[l]);
+      quad += a[i] * mm * a[l];
+    }
+    quad = block_sum(quad, red);
+    if (threadIdx.x == 0) {
+      const double vhat = (double)N / (double)(J - 1) * dev;
+      const double var = quad / P;
+      out[q * 4 + 0] = gbar;
+      out[q * 4 + 1] = sqrt(fmax(var, 0.0));
+      out[q * 4 + 2] = sqrt(vhat / P);
+      out[q * 4 + 3] = vhat > 0.0 ? var / vhat : INFINITY;
+    }
+    __syncthreads();
+  }
+}
+
+// ============================================================ C phase, data tempering (K2/K3)
+// K2: cumulative log weights over observations [s0, s0 + B) for every
+// particle (PAPER.md:281-295 eq. C_phase_compute in log form):
+// lwbuf[b][p] = lw_p(s0 + b + 1).  theta staged transposed in shared memory.
+__global__ void __launch_bounds__(128) k_cphase_scan(const double* __restrict__ Xs, const int32_t* __restrict__ y,
+                                                     int ldx, int k, int C, const double* __restrict__ theta, int d,
+                                                     int64_t P, int s0, int B, double* __restrict__ lw_cur,
+                                                     double* __restrict__ lwbuf) {
+  extern __shared__ double sth[];  // d x blockDim (transposed)
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = p < P;
+  for (int i = 0; i < d; ++i) sth[i * blockDim.x + threadIdx.x] = valid ? theta[p * d + i] : 0.0;
+  __syncthreads();
+  if (!valid) return;
+  double lw = lw_cur[p];
+  for (int b = 0; b < B; ++b) {
+    const int t = s0 + b;
+    const double* x = Xs + (int64_t)t * ldx;
+    double lpt;
+    if (C == 2) {
+      double s = 0.0;
+      for (int i = 0; i < k; ++i) s = fma(sth[i * blockDim.x + threadIdx.x], __ldg(x + i), s);
+      lpt = -(fmax(s, 0.0) + log1p(exp(-fabs(s))));
+    } else {
+      double eta[8];
+      eta[0] = 0.0;
+      double m = 0.0;
+      for (int c = 1; c < C; ++c) {
+        double s = 0.0;
+        for (int i = 0; i < k; ++i) s = fma(sth[((c - 1) * k + i) * blockDim.x + threadIdx.x], __ldg(x + i), s);
+        eta[c] = s;
+        m = fmax(m, s);
+      }
+      int cstar = 0;
+      for (int c = 1; c < C; ++c)
+        if (eta[c] > eta[cstar]) cstar = c;
+      double rest = 0.0;
+      for (int c = 0; c < C; ++c)
+        if (c != cstar) rest += exp(eta[c] - m);
+      lpt = (eta[y[t]] - m) - log1p(rest);
+    }
+    lw += lpt;
+    lwbuf[(int64_t)b * P + p] = lw;
+  }
+  lw_cur[p] = lw;
+}
+
+// Per (tile, b): (m, S1 = sum e^(lw - m), S2 = sum e^(2 (lw - m))) over a tile of particles.
+__global__ void __launch_bounds__(256) k_ess_partials(const double* __restrict__ lwbuf, int64_t P, int tile,
+                                                      double* __restrict__ out /* [B][ntiles][3] */) {
+  __shared__ double red[32];
+  const int b = blockIdx.y, ti = blockIdx.x, ntiles = gridDim.x;
+  const double* v = lwbuf + (int64_t)b * P + (int64_t)ti * tile;
+  const int cnt = (int)min((int64_t)tile, P - (int64_t)ti * tile);
+  double m = -INFINITY;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) m = fmax(m, v[i]);
+  m = block_max(m, red);
+  double s1 = 0.0, s2 = 0.0;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    const double w = exp(v[i] - m);
+    s1 += w;
+    s2 += w * w;
+  }
+  s1 = block_sum(s1, red);
+  s2 = block_sum(s2, red);
+  if (threadIdx.x == 0) {
+    double* o = out + ((int64_t)b * ntiles + ti) * 3;
+    o[0] = m;
+    o[1] = s1;
+    o[2] = s2;
+  }
+}
+
+__device__ __forceinline__ void combine3(double& M, double& S1, double& S2, double m, double s1, double s2) {
+  if (m == -INFINITY) return;
+  if (M == -INFINITY) {
+    M = m;
+    S1 = s1;
+    S2 = s2;
+    return;
+  }
+  if (m > M) {
+    const double e = exp(M - m);
+    S1 = S1 * e + s1;
+    S2 = S2 * e * e + s2;
+    M = m;
+  } else {
+    const double e = exp(m - M);
+    S1 += s1 * e;
+    S2 += s2 * e * e;
+  }
+}
+
+// Combine tiles in order -> this rank's (m, S1, S2) per b.
+__global__ void k_ess_rank(const double* __restrict__ parts, int ntiles, int B, double* __restrict__ slice) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  double M = -INFINITY, S1 = 0.0, S2 = 0.0;
+  for (int t = 0; t < ntiles; ++t) {
+    const double* o = parts + ((int64_t)b * ntiles + t) * 3;
+    combine3(M, S1, S2, o[0], o[1], o[2]);
+  }
+  slice[b * 3 + 0] = M;
+  slice[b * 3 + 1] = S1;
+  slice[b * 3 + 2] = S2;
+}
+
+// K3 (Algorithm 2 step 1; R3, R4): combine ranks in rank order;
+// s* = first s in the chunk with S1^2 < ess_frac P S2, or s == n (ends the cycle).
+__global__ void k_ess_final(const double* __restrict__ gath, int G, int B, int s0, int n, double ess_frac, double P,
+                            Ctl* ctl) {
+  if (threadIdx.x != 0) return;
+  ctl->s_star = -1;
+  for (int b = 0; b < B; ++b) {
+    double M = -INFINITY, S1 = 0.0, S2 = 0.0;
+    for (int r = 0; r < G; ++r) {
+      const double* o = gath + ((int64_t)r * B + b) * 3;
+      combine3(M, S1, S2, o[0], o[1], o[2]);
+    }
+    const int s = s0 + b + 1;
+    if (S1 * S1 < ess_frac * P * S2 || s == n) {
+      ctl->s_star = s;
+      ctl->ess = S1 * S1 / S2;
+      return;
+    }
+  }
+}
+
+// lw_p := lwbuf[b*][p] (the cycle's log weights), L_p += lw_p.
+__global__ void k_take_lw(const double* __restrict__ lwbuf, int bstar, int64_t P, double* __restrict__ lw,
+                          double* __restrict__ L) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  const double v = lwbuf[(int64_t)bstar * P + p];
+  lw[p] = v;
+  L[p] += v;
+}
+
+// ============================================================ C phase, power tempering (K4, R5)
+__global__ void __launch_bounds__(256) k_block_max(const double* __restrict__ v, int64_t P, double* __restrict__ out) {
+  __shared__ double red[32];
+  double m = -INFINITY;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmax(m, v[i]);
+  m = block_max(m, red);
+  if (threadIdx.x == 0) out[blockIdx.x] = m;
+}
+
+__global__ void k_max_reduce(const double* __restrict__ in, int cnt, double* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double m = -INFINITY;
+  for (int i = 0; i < cnt; ++i) m = fmax(m, in[i]);
+  *out = m;
+}
+
+// Candidate increments dphi_i = ((lo + i w) 2^-48) rem, i = 1..ncand (w = (hi-lo)/64),
+// or the single candidate rem when ncand == 0.  Per block partial (S1_i, S2_i).
+__device__ __forceinline__ double cand_dphi(const Ctl* ctl, int i, int ncand, double rem) {
+  if (ncand == 0) return rem;
+  const unsigned long long w = (ctl->q_hi - ctl->q_lo) / 64ull;
+  return ((double)(ctl->q_lo + (unsigned long long)i * w) * 0x1p-48) * rem;
+}
+
+__global__ void __launch_bounds__(256) k_power_partials(const double* __restrict__ L, int64_t P,
+                                                        const double* __restrict__ Lmax, const Ctl* ctl, int ncand,
+                                                        double rem, double* __restrict__ out /* [nblk][64][2] */) {
+  __shared__ double red[32];
+  const double lm = *Lmax;
+  const int nc = ncand == 0 ? 1 : ncand;
+  for (int c = 0; c < nc; ++c) {
+    const double dp = cand_dphi(ctl, c + 1, ncand, rem);
+    double s1 = 0.0, s2 = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+      const double w = exp(dp * (L[i] - lm));
+      s1 += w;
+      s2 += w * w;
+    }
+    s1 = block_sum(s1, red);
+    s2 = block_sum(s2, red);
+    if (threadIdx.x == 0) {
+      out[((int64_t)blockIdx.x * 64 + c) * 2 + 0] = s1;
+      out[((int64_t)blockIdx.x * 64 + c) * 2 + 1] = s2;
+    }
+  }
+}
+
+__global__ void k_power_rank(const double* __restrict__ parts, int nblk, int ncand, double* __restrict__ slice) {
+  const int c = threadIdx.x;
+  const int nc = ncand == 0 ? 1 : ncand;
+  if (c >= nc) return;
+  double s1 = 0.0, s2 = 0.0;
+  for (int b = 0; b < nblk; ++b) {
+    s1 += parts[((int64_t)b * 64 + c) * 2 + 0];
+    s2 += parts[((int64_t)b * 64 + c) * 2 + 1];
+  }
+  slice[c * 2 + 0] = s1;
+  slice[c * 2 + 1] = s2;
+}
+
+// Combine ranks; ok(c) = !(S1^2 < ess_frac P S2).  ncand == 0: test the full
+// remaining increment.  Else narrow [lo, hi) to the last ok candidate's cell.
+__global__ void k_power_decide(const double* __restrict__ gath, int G, int ncand, double ess_frac, double P,
+                               Ctl* ctl) {
+  if (threadIdx.x != 0) return;
+  const int nc = ncand == 0 ? 1 : ncand;
+  int last_ok = 0;
+  for (int c = 0; c < nc; ++c) {
+    double s1 = 0.0, s2 = 0.0;
+    for (int r = 0; r < G; ++r) {
+      s1 += gath[((int64_t)r * 64 + c) * 2 + 0];
+      s2 += gath[((int64_t)r * 64 + c) * 2 + 1];
+    }
+    const bool ok = !(s1 * s1 < ess_frac * P * s2);
+    if (ncand == 0) {
+      ctl->q_ok_full = ok ? 1 : 0;
+      if (ok) ctl->ess = s1 * s1 / s2;
+      return;
+    }
+    if (ok) last_ok = c + 1;
+  }
+  const unsigned long long w = (ctl->q_hi - ctl->q_lo) / 64ull;
+  const unsigned long long lo = ctl->q_lo + (unsigned long long)last_ok * w;
+  ctl->q_lo = lo;
+  ctl->q_hi = lo + w;
+}
+
+__global__ void k_power_apply(const double* __restrict__ L, int64_t P, double dphi, double* __restrict__ lw) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < P) lw[p] = dphi * L[p];
+}
+
+// ============================================================ S phase (K5)
+// Integer resampling core of one group (R7), executed by one block.  q (N
+// integer weights) in `cum` on entry; on exit counts[n] hold the copies of n.
+// a(r) supplies the 52-bit uniform of draw r.
+template <typename DrawFn>
+__device__ void resample_core(int N, uint64_t* cum, int* counts, int scheme, DrawFn a, uint64_t* scratch) {
+  // totals
+  uint64_t Q = 0;
+  {
+    uint64_t part = 0;
+    for (int n = threadIdx.x; n < N; n += blockDim.x) part += cum[n];
+    uint64_t tot;
+    // reuse scan helper for the block total
+    block_scan_u64(part, scratch, &tot);
+    Q = tot;
+  }
+  __shared__ unsigned long long sR;
+  if (scheme == 0) {
+    // residual: c_n = floor(N q_n / Q), r_n = N q_n - c_n Q
+    uint64_t csum_part = 0;
+    for (int n = threadIdx.x; n < N; n += blockDim.x) {
+      const uint64_t nq = (uint64_t)N * cum[n];
+      const uint64_t c = nq / Q;
+      counts[n] = (int)c;
+      csum_part += c;
+      cum[n] = nq - c * Q;
+    }
+    uint64_t csum;
+    block_scan_u64(csum_part, scratch, &csum);
+    if (threadIdx.x == 0) sR = (unsigned long long)N - csum;
+  } else {
+    for (int n = threadIdx.x; n < N; n += blockDim.x) counts[n] = 0;
+  }
+  __syncthreads();
+  // inclusive prefix sums of cum over n (chunks of blockDim, in order)
+  {
+    uint64_t carry = 0;
+    for (int base = 0; base < N; base += blockDim.x) {
+      const int n = base + threadIdx.x;
+      const uint64_t v = n < N ? cum[n] : 0ull;
+      uint64_t tot;
+      const uint64_t inc = block_scan_u64(v, scratch, &tot);
+      if (n < N) cum[n] = carry + inc;
+      carry += tot;
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  const uint64_t R = scheme == 0 ? (uint64_t)sR : (uint64_t)N;
+  const uint64_t RQ = scheme == 0 ? R * Q : Q;
+  for (uint64_t i = threadIdx.x; i < R; i += blockDim.x) {
+    uint64_t pos;
+    if (scheme == 1) {
+      const unsigned __int128 num = ((unsigned __int128)i << 53) + (unsigned __int128)(2ull * a(0) + 1ull);
+      pos = (uint64_t)(((num * (unsigned __int128)Q) / (unsigned __int128)(uint64_t)N) >> 53);
+    } else {
+      const uint64_t x = 2ull * a((uint32_t)i) + 1ull;
+      const uint64_t hi = __umul64hi(x, RQ), lo = x * RQ;
+      pos = (hi << 11) | (lo >> 53);
+    }
+    // first n with cum[n] > pos
+    int lo_i = 0, hi_i = N - 1;
+    while (lo_i < hi_i) {
+      const int mid = (lo_i + hi_i) >> 1;
+      if (cum[mid] > pos)
+        hi_i = mid;
+      else
+        lo_i = mid + 1;
+    }
+    atomicAdd(&counts[lo_i], 1);
+  }
+  __syncthreads();
+}
+
+// Expand counts into the ascending ancestor list (block).
+__device__ void counts_to_ancestors(int N, const int* counts, int* anc, uint64_t* scratch) {
+  uint64_t carry = 0;
+  for (int base = 0; base < N; base += blockDim.x) {
+    const int n = base + threadIdx.x;
+    const uint64_t c = n < N ? (uint64_t)counts[n] : 0ull;
+    uint64_t tot;
+    const uint64_t inc = block_scan_u64(c, scratch, &tot);
+    if (n < N) {
+      const int start = (int)(carry + inc - c);
+      for (int q = 0; q < (int)c; ++q) anc[start + q] = n;
+    }
+    carry += tot;
+    __syncthreads();
+  }
+  __syncthreads();
+}
+
+// K5: one block per local group.  q_n = floor(pexp(lw_n -
+// max) 2^32) (R7, R8), residual/systematic/multinomial draws from the
+// RESAMPLE stream of (global group, cycle), ascending ancestors, gather of
+// theta / L / lp into the destination buffers.  Also the group's log-ML
+// increment m_j + log(sum_n e^(lw - m_j) / N) (R10) and (m_j, s_j) for the pooled one.
+__global__ void __launch_bounds__(1024) k_resample(const double* __restrict__ lw, int N, int d, int scheme,
+                                                   uint64_t seed, uint32_t cycle, uint32_t pass, int g0,
+                                                   const double* __restrict__ th_src, const double* __restrict__ L_src,
+                                                   const double* __restrict__ lp_src, double* __restrict__ th_dst,
+                                                   double* __restrict__ L_dst, double* __restrict__ lp_dst,
+                                                   double* __restrict__ grp_ms /* [Jl][2] */,
+                                                   double* __restrict__ Lj, int* __restrict__ anc_out, Ctl* ctl) {
+  extern __shared__ unsigned char smraw[];
+  uint64_t* cum = reinterpret_cast<uint64_t*>(smraw);
+  int* counts = reinterpret_cast<int*>(cum + N);
+  int* anc = reinterpret_cast<int*>(cum);  // reuses cum once the draws are done (12 N bytes of smem)
+  __shared__ uint64_t scratch[33];
+  __shared__ double red[32];
+  const int j = blockIdx.x;
+  const uint32_t gj = (uint32_t)(g0 + j);
+  const double* w = lw + (int64_t)j * N;
+  double m = -INFINITY;
+  for (int n = threadIdx.x; n < N; n += blockDim.x) m = fmax(m, w[n]);
+  m = block_max(m, red);
+  double s = 0.0;
+  for (int n = threadIdx.x; n < N; n += blockDim.x) {
+    s += exp(w[n] - m);
+    cum[n] = (uint64_t)floor(__dmul_rn(pexp(__dsub_rn(w[n], m)), 4294967296.0));
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) {
+    grp_ms[j * 2 + 0] = m;
+    grp_ms[j * 2 + 1] = s;
+    Lj[j] += m + log(s / (double)N);
+    if (!isfinite(m)) ctl->err = ERR_NUMERIC;
+  }
+  auto draw = [&](uint32_t r) -> uint64_t {
+    const u4 v = stream_block(seed, r >> 1, gj, cycle, TAG_RESAMPLE, pass);
+    return (r & 1u) ? a52(v.z, v.w) : a52(v.x, v.y);
+  };
+  resample_core(N, cum, counts, scheme, draw, scratch);
+  counts_to_ancestors(N, counts, anc, scratch);
+  if (anc_out)
+    for (int n = threadIdx.x; n < N; n += blockDim.x) anc_out[(int64_t)j * N + n] = anc[n];
+  const int64_t base = (int64_t)j * N;
+  for (int idx = threadIdx.x; idx < N * d; idx += blockDim.x) {
+    const int n = idx / d, c = idx % d;
+    th_dst[(base + n) * d + c] = th_src[(base + anc[n]) * d + c];
+  }
+  for (int n = threadIdx.x; n < N; n += blockDim.x) {
+    L_dst[base + n] = L_src[base + anc[n]];
+    lp_dst[base + n] = lp_src[base + anc[n]];
+  }
+}
+
+// Pooled log-ML increment from all groups' (m_j, s_j) in group order (R10).
+__global__ void k_logml_pooled(const double* __restrict__ gath_ms, int J, double P, Ctl* ctl) {
+  if (threadIdx.x != 0) return;
+  double M = -INFINITY;
+  for (int j = 0; j < J; ++j) M = fmax(M, gath_ms[j * 2]);
+  double S = 0.0;
+  for (int j = 0; j < J; ++j) S += gath_ms[j * 2 + 1] * exp(gath_ms[j * 2] - M);
+  ctl->logml_inc = M + log(S / P);
+}
+
+// NSE of log ML across groups (R10) from the gathered per-group L_j.
+__global__ void k_logml_nse(const double* __restrict__ Lj, int J, double* __restrict__ out) {
+  if (threadIdx.x != 0) return;
+  double s = 0.0;
+  for (int j = 0; j < J; ++j) s += Lj[j];
+  const double bar = s / (double)J;
+  double v = 0.0;
+  for (int j = 0; j < J; ++j) v += (Lj[j] - bar) * (Lj[j] - bar);
+  *out = sqrt(v / ((double)J * (double)(J - 1)));
+}
+
+// ============================================================ test-export kernels
+__global__ void k_test_philox(int n, const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const u4 r = philox4x32_10(u4{ctr[4 * i], ctr[4 * i + 1], ctr[4 * i + 2], ctr[4 * i + 3]}, k0, k1);
+  out[4 * i] = r.x;
+  out[4 * i + 1] = r.y;
+  out[4 * i + 2] = r.z;
+  out[4 * i + 3] = r.w;
+}
+
+__global__ void k_test_normals(uint64_t seed, uint32_t id, uint32_t step, uint32_t tag, uint32_t pass, int count,
+                               double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (2 * i >= count) return;
+  double z0, z1;
+  normal_pair(seed, (uint32_t)i, id, step, tag, pass, &z0, &z1);
+  out[2 * i] = z0;
+  if (2 * i + 1 < count) out[2 * i + 1] = z1;
+}
+
+__global__ void k_test_portable(int which, int n, const double* x, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (which == 0) out[i] = plog(x[i]);
+  if (which == 1) out[i] = pexp(x[i]);
+  if (which == 2) psincos2pi(x[i], &out[2 * i], &out[2 * i + 1]);
+}
+
+__global__ void __launch_bounds__(1024) k_test_resample_int(int N, const uint64_t* q, int scheme, const uint64_t* a,
+                                                            int* anc_out) {
+  extern __shared__ unsigned char smraw[];
+  uint64_t* cum = reinterpret_cast<uint64_t*>(smraw);
+  int* counts = reinterpret_cast<int*>(cum + N);
+  int* anc = reinterpret_cast<int*>(cum);
+  __shared__ uint64_t scratch[33];
+  for (int n = threadIdx.x; n < N; n += blockDim.x) cum[n] = q[n];
+  __syncthreads();
+  auto draw = [&](uint32_t r) -> uint64_t { return a[r]; };
+  resample_core(N, cum, counts, scheme, draw, scratch);
+  counts_to_ancestors(N, counts, anc, scratch);
+  for (int n = threadIdx.x; n < N; n += blockDim.x) anc_out[n] = anc[n];
+}
+
+__global__ void k_test_accept(int64_t P, const double* delta, uint64_t seed, uint32_t step, uint32_t pass,
+                              uint8_t* flags) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  const u4 w = stream_block(seed, 0u, (uint32_t)p, step, TAG_ACCEPT, pass);
+  flags[p] = plog(u01(w.x, w.y)) < delta[p] ? 1 : 0;
+}
+
+}  // namespace sps

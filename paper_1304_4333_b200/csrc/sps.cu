@@ -1,0 +1,1119 @@
+// sps.cu -- libsps.so: engine (host orchestration of the SPS phases on one
+// CUDA stream) and the C ABI declared in include/sps.h.
+//
+// Algorithm 2 with the phases of Algorithm 1
+// (PAPER.md:266-326).  Every arithmetic step runs in the kernels of
+// loglik.cuh / kernels.cuh; the host only sequences launches, reads back the
+// control scalars (s*, stop flag, h, log-ML increment) and records the trace.
+// Multi-GPU: group sharding, one NCCL allgather per exchange step (dlopen'ed
+// libnccl.so.2), deterministic rank-order combination so every rank takes
+// identical decisions.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/sps.h"
+#include "common.cuh"
+#include "kernels.cuh"
+#include "loglik.cuh"
+
+using namespace sps;
+
+// ================================================================== NCCL (dlopen)
+namespace {
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool load(std::string* why) {
+    if (h) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* nm : names) {
+      h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) {
+      *why = "dlopen(libnccl.so.2) failed";
+      return false;
+    }
+    GetUniqueId = (decltype(GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    CommInitRank = (decltype(CommInitRank))dlsym(h, "ncclCommInitRank");
+    CommDestroy = (decltype(CommDestroy))dlsym(h, "ncclCommDestroy");
+    AllGather = (decltype(AllGather))dlsym(h, "ncclAllGather");
+    GetErrorString = (decltype(GetErrorString))dlsym(h, "ncclGetErrorString");
+    if (!GetUniqueId || !CommInitRank || !CommDestroy || !AllGather) {
+      *why = "libnccl.so.2 lacks a required symbol";
+      return false;
+    }
+    return true;
+  }
+};
+NcclApi g_nccl;
+}  // namespace
+
+// ================================================================== context
+struct sps_ctx {
+  sps_config cfg{};
+  int n = 0, k = 0, C = 0, d = 0, J = 0, N = 0, G = 1, rank = 0, Jl = 0, g0 = 0;
+  int64_t P = 0, Pl = 0, p0 = 0;
+  int ldx = 0, KT = 0, PPT = 1, nmon = 0, dmax = 0, pp = 0, bpg = 0, nblk_mom = 0, ngy_mom = 0;
+  int max_chunks = 1, Bmax = 8;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  ncclComm_t comm = nullptr;
+  // device buffers
+  double *X = nullptr, *Xs = nullptr, *mu = nullptr, *Lprior = nullptr, *xbar = nullptr, *mon = nullptr;
+  int32_t* y = nullptr;
+  double *theta = nullptr, *theta2 = nullptr, *L = nullptr, *L2 = nullptr, *lp = nullptr, *lp2 = nullptr;
+  double *lw = nullptr, *lw_cur = nullptr, *theta_s = nullptr, *lp_s = nullptr, *part = nullptr;
+  double *gpart = nullptr, *mpart = nullptr, *slice = nullptr, *gath = nullptr;
+  double *shift = nullptr, *Lprop = nullptr, *V = nullptr, *rne = nullptr;
+  double *lwbuf = nullptr, *essparts = nullptr, *essslice = nullptr, *essgath = nullptr;
+  double *grp_ms = nullptr, *grp_ms_gath = nullptr, *Lj = nullptr, *Lj_gath = nullptr, *scal = nullptr;
+  double *pw_parts = nullptr, *pw_slice = nullptr, *pw_gath = nullptr, *mx_parts = nullptr, *mx_slice = nullptr,
+         *mx_gath = nullptr;
+  double *fn_A = nullptr, *fn_out = nullptr;
+  int fn_cap = 0;
+  double* ll_scratch = nullptr;  // sps_loglik chunk partials (grown on demand)
+  size_t ll_scratch_cap = 0;
+  Ctl* ctl = nullptr;
+  Ctl* hctl = nullptr;  // pinned mirror
+  int slice_len = 0;
+  // host state (Algorithm 2)
+  int t = 0;            // observations absorbed
+  double phi = 0.0;     // tempering level (power mode)
+  int ell = 0;          // cycles completed
+  uint32_t mstep = 0;   // global M-step counter (PROPOSAL / ACCEPT streams)
+  bool need_pre_moments = false;
+  bool cphase_done = false;  // a C phase ran since the last M phase
+  bool finished = false;
+  double logml = 0.0, pairs = 0.0;
+  std::vector<int> tr_t, tr_R, tr_h;
+  std::vector<double> tr_phi, tr_inc, tr_rne;
+  // counters (sps_get_counters)
+  int64_t launches = 0, k1_launches = 0, syncs = 0;
+  double k1_pairs = 0.0, k1_ms = 0.0;
+  bool profiling = false;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::string err;
+};
+
+namespace {
+
+sps_status fail(sps_ctx* c, sps_status st, const char* fmt, ...) {
+  if (c) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    c->err = buf;
+  }
+  return st;
+}
+
+#define CU(c, x)                                                                                        \
+  do {                                                                                                  \
+    cudaError_t e_ = (x);                                                                               \
+    if (e_ != cudaSuccess) return fail((c), SPS_E_CUDA, "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), \
+                                       __FILE__, __LINE__);                                             \
+  } while (0)
+#define CHECK_LAUNCH(c)        \
+  do {                         \
+    (c)->launches += 1;        \
+    CU(c, cudaGetLastError()); \
+  } while (0)
+#define TRY(x)                         \
+  do {                                 \
+    sps_status s_ = (x);               \
+    if (s_ != SPS_OK) return s_;       \
+  } while (0)
+
+template <typename T>
+sps_status dalloc(sps_ctx* c, T** p, size_t count) {
+  CU(c, cudaMalloc((void**)p, std::max<size_t>(count, 1) * sizeof(T)));
+  return SPS_OK;
+}
+
+int num_sms() {
+  int dev = 0, v = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  return v;
+}
+
+sps_status gather(sps_ctx* c, const double* send, double* recv, size_t count) {
+  if (c->G == 1) {
+    if (send != recv) CU(c, cudaMemcpyAsync(recv, send, count * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    return SPS_OK;
+  }
+  ncclResult_t r = g_nccl.AllGather(send, recv, count, ncclFloat64, c->comm, c->stream);
+  if (r != ncclSuccess) return fail(c, SPS_E_NCCL, "ncclAllGather: %s", g_nccl.GetErrorString(r));
+  return SPS_OK;
+}
+
+// Read back the control block (synchronizes the stream); maps device errors.
+sps_status read_ctl(sps_ctx* c) {
+  CU(c, cudaMemcpyAsync(c->hctl, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->stream));
+  CU(c, cudaStreamSynchronize(c->stream));
+  c->syncs += 1;
+  if (c->hctl->err == ERR_DATA) return fail(c, SPS_E_DATA, "invalid data (label out of range or non-finite X)");
+  if (c->hctl->err == ERR_NUMERIC)
+    return fail(c, SPS_E_NUMERIC, "numerical failure (non-finite log-likelihood, weight collapse or Cholesky "
+                                  "failure after ridge; cf. PAPER.md:1024-1030)");
+  return SPS_OK;
+}
+
+// ------------------------------------------------------------------ K1 dispatch
+using LLKernel = void (*)(LLArgs);
+
+template <int K, int CM1, int PPT>
+LLKernel ll_ptr() {
+  if constexpr (CM1 == 1)
+    return k_loglik_bin<K, PPT>;
+  else
+    return k_loglik_mnl<K, CM1, PPT>;
+}
+
+// Instantiated shapes: binary k = 1..32 (PPT 2) and {40,48,56,64} (PPT 1);
+// C-1 = 2: k = 1..16 (PPT 2 up to 12); C-1 = 3: k = 1..16; C-1 = 4..7: k in {4, 8}.
+// Other k round up to the next instantiated KT (zero padding in X and theta loads).
+struct LLChoice {
+  LLKernel fn;
+  int KT, PPT;
+};
+
+template <int CM1, int PPT, int... Ks>
+bool pick_exact(int k, LLChoice* out, std::integer_sequence<int, Ks...>) {
+  bool found = false;
+  ((k == Ks + 1 && !found ? (out->fn = ll_ptr<Ks + 1, CM1, PPT>(), out->KT = Ks + 1, out->PPT = PPT, found = true)
+                          : false),
+   ...);
+  return found;
+}
+
+bool choose_ll(int k, int C, LLChoice* o) {
+  const int cm1 = C - 1;
+  if (cm1 == 1) {
+    if (k <= 32) return pick_exact<1, 2>(k, o, std::make_integer_sequence<int, 32>{});
+    if (k <= 40) { *o = {ll_ptr<40, 1, 1>(), 40, 1}; return true; }
+    if (k <= 48) { *o = {ll_ptr<48, 1, 1>(), 48, 1}; return true; }
+    if (k <= 56) { *o = {ll_ptr<56, 1, 1>(), 56, 1}; return true; }
+    if (k <= 64) { *o = {ll_ptr<64, 1, 1>(), 64, 1}; return true; }
+    return false;
+  }
+  if (cm1 == 2) {
+    if (k <= 12) return pick_exact<2, 2>(k, o, std::make_integer_sequence<int, 12>{});
+    if (k <= 16) return pick_exact<2, 1>(k, o, std::make_integer_sequence<int, 16>{});
+    return false;
+  }
+  if (cm1 == 3) {
+    if (k <= 16) return pick_exact<3, 1>(k, o, std::make_integer_sequence<int, 16>{});
+    return false;
+  }
+  if (k > 8) return false;
+  const int KT = k <= 4 ? 4 : 8;
+  switch (cm1) {
+    case 4: *o = KT == 4 ? LLChoice{ll_ptr<4, 4, 1>(), 4, 1} : LLChoice{ll_ptr<8, 4, 1>(), 8, 1}; return true;
+    case 5: *o = KT == 4 ? LLChoice{ll_ptr<4, 5, 1>(), 4, 1} : LLChoice{ll_ptr<8, 5, 1>(), 8, 1}; return true;
+    case 6: *o = KT == 4 ? LLChoice{ll_ptr<4, 6, 1>(), 4, 1} : LLChoice{ll_ptr<8, 6, 1>(), 8, 1}; return true;
+    case 7: *o = KT == 4 ? LLChoice{ll_ptr<4, 7, 1>(), 4, 1} : LLChoice{ll_ptr<8, 7, 1>(), 8, 1}; return true;
+    default: return false;
+  }
+}
+
+// Launch K1 over [t0, t1) for P particles: partial sums per observation chunk
+// into `part` ([nchunks][P]); returns nchunks.  Chunk count is chosen so the
+// grid fills whole waves of (SMs x resident blocks) and the X tile fits smem.
+sps_status launch_loglik(sps_ctx* c, const double* theta, int64_t ldt, int64_t P, int t0, int t1, double* part,
+                         int max_chunks, int* nchunks_out) {
+  LLChoice ch;
+  if (!choose_ll(c->k, c->C, &ch)) return fail(c, SPS_E_CONFIG, "unsupported (k, C) = (%d, %d)", c->k, c->C);
+  const int range = t1 - t0;
+  const int64_t tiles = (P + LL_THREADS * ch.PPT - 1) / (LL_THREADS * ch.PPT);
+  const int ldx = c->ldx;
+  const size_t row_bytes = (size_t)ldx * 8 + (c->C > 2 ? 4 : 0);
+  const int smem_budget = 96 * 1024;
+  const int chunk_cap = std::max(1, (int)((smem_budget - 64 * 8 - 64) / row_bytes));
+  int S_min = std::max(1, (range + chunk_cap - 1) / chunk_cap);
+  static thread_local int occ_cache_key = -1, occ_cache_val = 0;
+  const int key = (int)(reinterpret_cast<uintptr_t>(ch.fn) & 0x7fffffff);
+  int occ = 0;
+  const size_t smem_probe = 64 * 8 + (size_t)std::min(range, chunk_cap) * row_bytes + 16;
+  CU(c, cudaFuncSetAttribute(ch.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_budget + 1024));
+  if (occ_cache_key == key) {
+    occ = occ_cache_val;
+  } else {
+    CU(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ch.fn, LL_THREADS, smem_budget));
+    occ = std::max(occ, 1);
+    occ_cache_key = key;
+    occ_cache_val = occ;
+  }
+  (void)smem_probe;
+  const double slots = (double)num_sms() * occ;
+  int best = S_min;
+  double best_eff = -1.0;
+  const int S_hi = std::min(max_chunks, std::max(S_min, range / 16));
+  for (int S = S_min; S <= std::max(S_min, S_hi); ++S) {
+    const double blocks = (double)tiles * S;
+    const double eff = blocks / (std::ceil(blocks / slots) * slots);
+    if (eff > best_eff + 0.02) {
+      best_eff = eff;
+      best = S;
+    }
+    if (blocks >= 4 * slots) break;
+  }
+  int S = std::min(best, max_chunks);
+  if (range <= 0) S = 1;
+  const int chunk = range > 0 ? (range + S - 1) / S : 0;
+  S = range > 0 ? (range + chunk - 1) / chunk : 1;
+  if (S > max_chunks) return fail(c, SPS_E_CONFIG, "observation range too long for the chunk buffer");
+  const size_t smem = 64 * 8 + (size_t)std::max(chunk, 1) * ldx * 8 + (c->C > 2 ? (size_t)std::max(chunk, 1) * 4 : 0);
+  LLArgs a{c->Xs, c->y, theta, part, ldt, P, t0, t1, chunk};
+  a.k = c->k;
+  if (range <= 0) {
+    CU(c, cudaMemsetAsync(part, 0, (size_t)P * sizeof(double), c->stream));
+  } else {
+    dim3 grid((unsigned)tiles, (unsigned)S);
+    if (c->profiling) CU(c, cudaEventRecord(c->ev0, c->stream));
+    ch.fn<<<grid, LL_THREADS, smem, c->stream>>>(a);
+    CHECK_LAUNCH(c);
+    c->k1_launches += 1;
+    c->k1_pairs += (double)P * range;
+    if (c->profiling) {
+      CU(c, cudaEventRecord(c->ev1, c->stream));
+      CU(c, cudaEventSynchronize(c->ev1));
+      float ms = 0.f;
+      CU(c, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+      c->k1_ms += ms;
+    }
+  }
+  *nchunks_out = S;
+  return SPS_OK;
+}
+
+int dmax_of(int d) { return d <= 16 ? 16 : d <= 32 ? 32 : d <= 64 ? 64 : 128; }
+
+sps_status launch_draw(sps_ctx* c, bool init, const double* base, const double* Lz, uint32_t step, double* out,
+                       double* lp_out) {
+  const int d = c->d;
+  const size_t smem = (size_t)(2 * d * d + d) * sizeof(double);
+  const unsigned grid = (unsigned)((c->Pl + 127) / 128);
+  auto go = [&](auto kern) -> sps_status {
+    CU(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
+    kern<<<grid, 128, smem, c->stream>>>(base, Lz, c->Lprior, c->mu, d, c->Pl, c->p0, c->cfg.seed, step,
+                                         (uint32_t)c->cfg.pass, out, lp_out, c->ctl, nullptr);
+    CHECK_LAUNCH(c);
+    return SPS_OK;
+  };
+  switch (c->dmax) {
+    case 16: return init ? go(k_draw<16, true>) : go(k_draw<16, false>);
+    case 32: return init ? go(k_draw<32, true>) : go(k_draw<32, false>);
+    case 64: return init ? go(k_draw<64, true>) : go(k_draw<64, false>);
+    default: return init ? go(k_draw<128, true>) : go(k_draw<128, false>);
+  }
+}
+
+// Moments of the current particles -> gathered stats (`gath`).
+sps_status moments(sps_ctx* c) {
+  const int d = c->d;
+  dim3 grid((unsigned)c->nblk_mom, (unsigned)c->ngy_mom);
+  const size_t smem = (size_t)MOM_TILE * d * sizeof(double);
+  CU(c, cudaFuncSetAttribute(k_moments_partial, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
+  k_moments_partial<<<grid, 256, smem, c->stream>>>(c->theta, d, c->pp, c->shift, c->gpart, c->mpart, nullptr);
+  CHECK_LAUNCH(c);
+  k_moments_reduce<<<64, 256, 0, c->stream>>>(c->gpart, c->mpart, c->nblk_mom, c->bpg, c->Jl, d, c->ctl, c->slice,
+                                              nullptr);
+  CHECK_LAUNCH(c);
+  return gather(c, c->slice, c->gath, (size_t)c->slice_len);
+}
+
+bool final_cycle(const sps_ctx* c) {
+  return c->cfg.tempering == SPS_POWER_TEMPERING ? (c->phi == 1.0) : (c->t == c->n);
+}
+
+sps_status finalize(sps_ctx* c, int mode) {
+  FinArgs f{};
+  f.gath = c->gath;
+  f.G = c->G;
+  f.slice_len = c->slice_len;
+  f.J = c->J;
+  f.Jl = c->Jl;
+  f.N = c->N;
+  f.d = c->d;
+  f.shift = c->shift;
+  f.Lprop = c->Lprop;
+  f.V = c->V;
+  f.mon = c->mon;
+  f.nmon = c->nmon;
+  f.mode = mode;
+  f.K = final_cycle(c) ? c->cfg.K_final : c->cfg.K_inter;
+  f.h_step = c->cfg.h_step;
+  f.h_min = c->cfg.h_min;
+  f.h_max = c->cfg.h_max;
+  f.accept_target = c->cfg.accept_target;
+  f.ctl = c->ctl;
+  f.stop_in = nullptr;
+  f.rne_out = c->rne;
+  const size_t smem = (size_t)(2 * c->d * c->d + c->d + c->J) * sizeof(double);
+  CU(c, cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
+  k_finalize<<<1, 256, smem, c->stream>>>(f);
+  CHECK_LAUNCH(c);
+  return SPS_OK;
+}
+
+sps_status validate(const sps_config* cfg) {
+  if (!cfg) return SPS_E_CONFIG;
+  if (cfg->n < 1 || cfg->k < 1 || cfg->C < 2 || cfg->C > 8) return SPS_E_CONFIG;
+  if (cfg->J < 2 || cfg->N < 2 || cfg->N > 16384) return SPS_E_CONFIG;
+  if (cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks || cfg->J % cfg->nranks) return SPS_E_CONFIG;
+  if (!(cfg->ess_frac > 0 && cfg->ess_frac < 1) || !(cfg->K_inter > 0) || !(cfg->K_final > 0)) return SPS_E_CONFIG;
+  if (cfg->h_min > cfg->h_init || cfg->h_init > cfg->h_max || cfg->h_min < 1 || cfg->h_step < 0) return SPS_E_CONFIG;
+  if (cfg->max_m_steps < 1 || cfg->max_cycles < 1) return SPS_E_CONFIG;
+  if (cfg->tempering != SPS_DATA_TEMPERING && cfg->tempering != SPS_POWER_TEMPERING) return SPS_E_CONFIG;
+  if (cfg->resampling < 0 || cfg->resampling > 2) return SPS_E_CONFIG;
+  const int64_t P = (int64_t)cfg->J * cfg->N;
+  if (P > (int64_t)1 << 31) return SPS_E_CONFIG;
+  return SPS_OK;
+}
+
+void free_ctx(sps_ctx* c) {
+  if (!c) return;
+  void* ptrs[] = {c->X, c->Xs, c->mu, c->Lprior, c->xbar, c->mon, c->y, c->theta, c->theta2, c->L, c->L2, c->lp,
+                  c->lp2, c->lw, c->lw_cur, c->theta_s, c->lp_s, c->part, c->gpart, c->mpart, c->slice, c->gath,
+                  c->shift, c->Lprop, c->V, c->rne, c->lwbuf, c->essparts, c->essslice, c->essgath, c->grp_ms,
+                  c->grp_ms_gath, c->Lj, c->Lj_gath, c->scal, c->pw_parts, c->pw_slice, c->pw_gath, c->mx_parts,
+                  c->mx_slice, c->mx_gath, c->fn_A, c->fn_out, c->ll_scratch, c->ctl};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (c->hctl) cudaFreeHost(c->hctl);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->comm) g_nccl.CommDestroy(c->comm);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+}
+
+constexpr int ESS_TILE = 2048;
+constexpr int MX_BLOCKS = 256;
+constexpr int PW_BLOCKS = 256;
+
+}  // namespace
+
+// ================================================================== C ABI
+extern "C" {
+
+sps_status sps_config_default(sps_config* cfg) {
+  if (!cfg) return SPS_E_CONFIG;
+  std::memset(cfg, 0, sizeof *cfg);
+  cfg->tempering = SPS_DATA_TEMPERING;
+  cfg->resampling = SPS_RESIDUAL;
+  cfg->ess_frac = 0.5;
+  cfg->K_inter = 0.35;
+  cfg->K_final = 0.9;
+  cfg->h_init = 50;
+  cfg->h_step = 1;
+  cfg->h_min = 10;
+  cfg->h_max = 100;
+  cfg->accept_target = 0.25;
+  cfg->max_m_steps = 1000;
+  cfg->max_cycles = 1 << 20;
+  cfg->nranks = 1;
+  return SPS_OK;
+}
+
+const char* sps_last_error(const sps_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+void sps_destroy(sps_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->cfg.device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  free_ctx(ctx);
+  delete ctx;
+}
+
+sps_status sps_nccl_unique_id(void* id128) {
+  std::string why;
+  if (!id128 || !g_nccl.load(&why)) return SPS_E_NCCL;
+  ncclUniqueId id;
+  if (g_nccl.GetUniqueId(&id) != ncclSuccess) return SPS_E_NCCL;
+  std::memcpy(id128, &id, sizeof id);
+  return SPS_OK;
+}
+
+sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* y, const double* prior_mean,
+                      const double* prior_cov, sps_ctx** out) {
+  if (!out) return SPS_E_CONFIG;
+  *out = nullptr;
+  if (validate(cfg_in) != SPS_OK || !X || !y || !prior_mean || !prior_cov) return SPS_E_CONFIG;
+  sps_ctx* c = new sps_ctx();
+  c->cfg = *cfg_in;
+  c->cfg.monitors = nullptr;
+  c->cfg.nccl_id = nullptr;
+  *out = c;
+  const sps_config& cfg = *cfg_in;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(c, SPS_E_CUDA, "no CUDA device: libsps has no CPU fallback");
+  CU(c, cudaSetDevice(cfg.device));
+  c->n = cfg.n;
+  c->k = cfg.k;
+  c->C = cfg.C;
+  c->d = cfg.k * (cfg.C - 1);
+  c->J = cfg.J;
+  c->N = cfg.N;
+  c->G = cfg.nranks;
+  c->rank = cfg.rank;
+  c->Jl = cfg.J / cfg.nranks;
+  c->g0 = c->rank * c->Jl;
+  c->P = (int64_t)cfg.J * cfg.N;
+  c->Pl = (int64_t)c->Jl * cfg.N;
+  c->p0 = (int64_t)c->g0 * cfg.N;
+  const int d = c->d;
+  if (d > 128) return fail(c, SPS_E_CONFIG, "d = k (C-1) = %d > 128 is not supported", d);
+  LLChoice ch;
+  if (!choose_ll(c->k, c->C, &ch)) return fail(c, SPS_E_CONFIG, "unsupported (k, C) = (%d, %d)", c->k, c->C);
+  c->KT = ch.KT;
+  c->PPT = ch.PPT;
+  c->ldx = ch.KT + (ch.KT & 1);
+  c->dmax = dmax_of(d);
+  c->nmon = cfg.n_monitors > 0 ? cfg.n_monitors : c->C;
+  if (cfg.n_monitors > 0 && !cfg_in->monitors) return fail(c, SPS_E_CONFIG, "n_monitors > 0 but monitors == NULL");
+  // moments layout
+  c->pp = 1;
+  for (int q = std::min(c->N, 256); q >= 1; --q)
+    if (c->N % q == 0) {
+      c->pp = q;
+      break;
+    }
+  c->bpg = c->N / c->pp;
+  c->nblk_mom = (int)(c->Pl / c->pp);
+  const int ntri = d * (d + 1) / 2;
+  c->ngy_mom = (ntri + MOM_ENT - 1) / MOM_ENT;
+  c->slice_len = c->Jl * d + d * d + 2;
+  c->max_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(64, ((int64_t)1 << 26) / std::max<int64_t>(c->Pl, 1)));
+  c->Bmax = (int)std::max<int64_t>(8, std::min<int64_t>(256, ((int64_t)1 << 23) / std::max<int64_t>(c->Pl, 1)));
+
+  if (cfg.stream) {
+    c->stream = (cudaStream_t)cfg.stream;
+  } else {
+    CU(c, cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+  }
+  if (c->G > 1) {
+    std::string why;
+    if (!cfg_in->nccl_id) return fail(c, SPS_E_CONFIG, "nranks > 1 requires nccl_id");
+    if (!g_nccl.load(&why)) return fail(c, SPS_E_NCCL, "%s", why.c_str());
+    ncclUniqueId id;
+    std::memcpy(&id, cfg_in->nccl_id, sizeof id);
+    ncclResult_t r = g_nccl.CommInitRank(&c->comm, c->G, id, c->rank);
+    if (r != ncclSuccess) return fail(c, SPS_E_NCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(r));
+  }
+  const int64_t Pl = c->Pl;
+  TRY(dalloc(c, &c->X, (size_t)c->n * c->k));
+  TRY(dalloc(c, &c->Xs, (size_t)c->n * c->ldx + 2));
+  TRY(dalloc(c, &c->y, (size_t)c->n));
+  TRY(dalloc(c, &c->mu, d));
+  TRY(dalloc(c, &c->Lprior, (size_t)d * d));
+  TRY(dalloc(c, &c->xbar, c->k));
+  TRY(dalloc(c, &c->mon, (size_t)c->nmon * d));
+  for (double** p : {&c->theta, &c->theta2, &c->theta_s}) TRY(dalloc(c, p, (size_t)Pl * d));
+  for (double** p : {&c->L, &c->L2, &c->lp, &c->lp2, &c->lw, &c->lw_cur, &c->lp_s}) TRY(dalloc(c, p, (size_t)Pl));
+  TRY(dalloc(c, &c->part, (size_t)c->max_chunks * Pl));
+  TRY(dalloc(c, &c->gpart, (size_t)c->nblk_mom * d));
+  TRY(dalloc(c, &c->mpart, (size_t)c->nblk_mom * ntri));
+  TRY(dalloc(c, &c->slice, (size_t)c->slice_len));
+  TRY(dalloc(c, &c->gath, (size_t)c->slice_len * c->G));
+  TRY(dalloc(c, &c->shift, d));
+  TRY(dalloc(c, &c->Lprop, (size_t)d * d));
+  TRY(dalloc(c, &c->V, (size_t)d * d));
+  TRY(dalloc(c, &c->rne, (size_t)c->nmon));
+  TRY(dalloc(c, &c->lwbuf, (size_t)c->Bmax * Pl));
+  const int ntiles = (int)((Pl + ESS_TILE - 1) / ESS_TILE);
+  TRY(dalloc(c, &c->essparts, (size_t)c->Bmax * ntiles * 3));
+  TRY(dalloc(c, &c->essslice, (size_t)c->Bmax * 3));
+  TRY(dalloc(c, &c->essgath, (size_t)c->Bmax * 3 * c->G));
+  TRY(dalloc(c, &c->grp_ms, (size_t)c->Jl * 2));
+  TRY(dalloc(c, &c->grp_ms_gath, (size_t)c->J * 2));
+  TRY(dalloc(c, &c->Lj, (size_t)c->Jl));
+  TRY(dalloc(c, &c->Lj_gath, (size_t)c->J));
+  TRY(dalloc(c, &c->scal, 8));
+  TRY(dalloc(c, &c->pw_parts, (size_t)PW_BLOCKS * 64 * 2));
+  TRY(dalloc(c, &c->pw_slice, 64 * 2));
+  TRY(dalloc(c, &c->pw_gath, (size_t)64 * 2 * c->G));
+  TRY(dalloc(c, &c->mx_parts, MX_BLOCKS));
+  TRY(dalloc(c, &c->mx_slice, 1));
+  TRY(dalloc(c, &c->mx_gath, (size_t)c->G));
+  TRY(dalloc(c, &c->ctl, 1));
+  CU(c, cudaMallocHost((void**)&c->hctl, sizeof(Ctl)));
+  std::memset(c->hctl, 0, sizeof(Ctl));
+  c->hctl->h = cfg.h_init;
+  CU(c, cudaMemcpyAsync(c->ctl, c->hctl, sizeof(Ctl), cudaMemcpyHostToDevice, c->stream));
+  CU(c, cudaMemsetAsync(c->Lj, 0, sizeof(double) * c->Jl, c->stream));
+  // inputs (host -> device); synchronous copies so the caller may free on return
+  CU(c, cudaMemcpyAsync(c->X, X, sizeof(double) * c->n * c->k, cudaMemcpyHostToDevice, c->stream));
+  CU(c, cudaMemcpyAsync(c->y, y, sizeof(int32_t) * c->n, cudaMemcpyHostToDevice, c->stream));
+  CU(c, cudaMemcpyAsync(c->mu, prior_mean, sizeof(double) * d, cudaMemcpyHostToDevice, c->stream));
+  CU(c, cudaMemcpyAsync(c->shift, prior_mean, sizeof(double) * d, cudaMemcpyHostToDevice, c->stream));
+  CU(c, cudaMemcpyAsync(c->V, prior_cov, sizeof(double) * d * d, cudaMemcpyHostToDevice, c->stream));
+  if (cfg.n_monitors > 0)
+    CU(c, cudaMemcpyAsync(c->mon, cfg_in->monitors, sizeof(double) * c->nmon * d, cudaMemcpyHostToDevice, c->stream));
+  {
+    const int64_t tot = (int64_t)c->n * c->ldx;
+    k_prep_X<<<(unsigned)((tot + 255) / 256), 256, 0, c->stream>>>(c->X, c->y, c->n, c->k, c->C, c->ldx, c->Xs,
+                                                                     c->ctl);
+    CHECK_LAUNCH(c);
+    CU(c, cudaMemsetAsync(c->Xs + tot, 0, 2 * sizeof(double), c->stream));
+    k_colmeans<<<(c->k + 127) / 128, 128, 0, c->stream>>>(c->X, c->n, c->k, c->xbar);
+    CHECK_LAUNCH(c);
+    if (cfg.n_monitors <= 0) {
+      k_default_monitors<<<1, 256, 0, c->stream>>>(c->xbar, c->k, c->C, c->mon);
+      CHECK_LAUNCH(c);
+    }
+    const size_t smem = sizeof(double) * d * d;
+    CU(c, cudaFuncSetAttribute(k_chol_prior, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
+    k_chol_prior<<<1, 256, smem, c->stream>>>(c->V, d, c->Lprior, c->ctl);
+    CHECK_LAUNCH(c);
+  }
+  {
+    sps_status st = read_ctl(c);
+    if (st == SPS_E_NUMERIC) return fail(c, SPS_E_CONFIG, "prior covariance is not positive definite");
+    if (st != SPS_OK) return st;
+  }
+  CU(c, cudaEventCreate(&c->ev0));
+  CU(c, cudaEventCreate(&c->ev1));
+  return sps_reset(c, cfg.seed, cfg.pass);
+}
+
+sps_status sps_reset(sps_ctx* c, uint64_t seed, int32_t pass) {
+  if (!c) return SPS_E_CONFIG;
+  CU(c, cudaSetDevice(c->cfg.device));
+  c->cfg.seed = seed;
+  c->cfg.pass = pass;
+  c->t = 0;
+  c->phi = 0.0;
+  c->ell = 0;
+  c->mstep = 0;
+  c->need_pre_moments = false;
+  c->cphase_done = false;
+  c->finished = false;
+  c->logml = 0.0;
+  c->pairs = 0.0;
+  c->tr_t.clear();
+  c->tr_R.clear();
+  c->tr_h.clear();
+  c->tr_phi.clear();
+  c->tr_inc.clear();
+  c->tr_rne.clear();
+  c->launches = c->k1_launches = c->syncs = 0;
+  c->k1_pairs = c->k1_ms = 0.0;
+  const int64_t Pl = c->Pl;
+  std::memset(c->hctl, 0, sizeof(Ctl));
+  c->hctl->h = c->cfg.h_init;
+  CU(c, cudaMemcpyAsync(c->ctl, c->hctl, sizeof(Ctl), cudaMemcpyHostToDevice, c->stream));
+  CU(c, cudaMemsetAsync(c->Lj, 0, sizeof(double) * c->Jl, c->stream));
+  CU(c, cudaMemcpyAsync(c->shift, c->mu, sizeof(double) * c->d, cudaMemcpyDeviceToDevice, c->stream));
+  // Algorithm 1 step 1: theta_jn ~iid p(theta)
+  TRY(launch_draw(c, true, nullptr, c->Lprior, 0u, c->theta, c->lp));
+  if (c->cfg.tempering == SPS_POWER_TEMPERING) {
+    int nch = 1;
+    TRY(launch_loglik(c, c->theta, c->d, Pl, 0, c->n, c->part, c->max_chunks, &nch));
+    k_sum_chunks<<<(unsigned)((Pl + 255) / 256), 256, 0, c->stream>>>(c->part, nch, Pl, c->L);
+    CHECK_LAUNCH(c);
+    c->pairs += (double)c->P * c->n;
+  } else {
+    CU(c, cudaMemsetAsync(c->L, 0, sizeof(double) * Pl, c->stream));
+  }
+  TRY(read_ctl(c));
+  return SPS_OK;
+}
+
+sps_status sps_set_profiling(sps_ctx* c, int32_t on) {
+  if (!c) return SPS_E_CONFIG;
+  c->profiling = on != 0;
+  return SPS_OK;
+}
+
+sps_status sps_get_counters(const sps_ctx* c, sps_counters* out) {
+  if (!c || !out) return SPS_E_CONFIG;
+  out->launches = c->launches;
+  out->k1_launches = c->k1_launches;
+  out->k1_pairs = c->k1_pairs;
+  out->k1_ms = c->k1_ms;
+  out->syncs = c->syncs;
+  return SPS_OK;
+}
+
+sps_status sps_shard(const sps_ctx* ctx, int64_t* P_local, int32_t* group0, int32_t* J_local) {
+  if (!ctx) return SPS_E_CONFIG;
+  if (P_local) *P_local = ctx->Pl;
+  if (group0) *group0 = ctx->g0;
+  if (J_local) *J_local = ctx->Jl;
+  return SPS_OK;
+}
+
+sps_status sps_loglik(sps_ctx* c, const double* theta_dev, int64_t P, int32_t ld, int32_t t0, int32_t t1,
+                      double* out_dev) {
+  if (!c) return SPS_E_CONFIG;
+  if (!theta_dev || !out_dev || P < 0 || ld < c->d || t0 < 0 || t1 < t0 || t1 > c->n)
+    return fail(c, SPS_E_CONFIG, "sps_loglik: bad arguments");
+  if (P == 0) return SPS_OK;
+  CU(c, cudaSetDevice(c->cfg.device));
+  // chunk partials: up to 64 chunks per particle, in a scratch buffer grown on demand
+  const int max_chunks = 64;
+  const size_t need = (size_t)max_chunks * (size_t)P;
+  if (need > c->ll_scratch_cap) {
+    if (c->ll_scratch) cudaFree(c->ll_scratch);
+    c->ll_scratch = nullptr;
+    c->ll_scratch_cap = 0;
+    TRY(dalloc(c, &c->ll_scratch, need));
+    c->ll_scratch_cap = need;
+  }
+  int nch = 1;
+  TRY(launch_loglik(c, theta_dev, ld, P, t0, t1, c->ll_scratch, max_chunks, &nch));
+  k_sum_chunks<<<(unsigned)((P + 255) / 256), 256, 0, c->stream>>>(c->ll_scratch, nch, P, out_dev);
+  CHECK_LAUNCH(c);
+  return SPS_OK;
+}
+
+sps_status sps_sync(sps_ctx* c) {
+  if (!c) return SPS_E_CONFIG;
+  CU(c, cudaSetDevice(c->cfg.device));
+  CU(c, cudaStreamSynchronize(c->stream));
+  c->syncs += 1;
+  return SPS_OK;
+}
+
+// One C phase + S phase.
+sps_status sps_cphase(sps_ctx* c, int32_t t_target, double phi_target, int32_t* t_new, double* phi_new,
+                      double* logml_inc) {
+  if (!c) return SPS_E_CONFIG;
+  CU(c, cudaSetDevice(c->cfg.device));
+  if (c->finished || final_cycle(c)) return fail(c, SPS_E_STATE, "sps_cphase: all data already absorbed");
+  if (c->ell >= c->cfg.max_cycles) return fail(c, SPS_E_CONFIG, "max_cycles exceeded");
+  const int64_t Pl = c->Pl;
+  const double P = (double)c->P;
+  const unsigned pgrid = (unsigned)((Pl + 255) / 256);
+  if (c->cfg.tempering == SPS_DATA_TEMPERING) {
+    // ---- absorb observations one at a time ----
+    if (t_target >= 0 && (t_target <= c->t || t_target > c->n))
+      return fail(c, SPS_E_CONFIG, "t_target out of range");
+    CU(c, cudaMemsetAsync(c->lw_cur, 0, sizeof(double) * Pl, c->stream));
+    int s = c->t;
+    int B = 8;
+    const int ntiles = (int)((Pl + ESS_TILE - 1) / ESS_TILE);
+    const size_t scan_smem = sizeof(double) * c->d * 128;
+    CU(c, cudaFuncSetAttribute(k_cphase_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem + 1024));
+    for (;;) {
+      int Be = std::min(std::min(B, c->Bmax), c->n - s);
+      if (t_target >= 0) Be = std::min(Be, t_target - s);
+      k_cphase_scan<<<(unsigned)((Pl + 127) / 128), 128, scan_smem, c->stream>>>(
+          c->Xs, c->y, c->ldx, c->k, c->C, c->theta, c->d, Pl, s, Be, c->lw_cur, c->lwbuf);
+      CHECK_LAUNCH(c);
+      c->pairs += P * Be;
+      int sstar = -1;
+      if (t_target >= 0) {
+        if (s + Be == t_target) sstar = t_target;
+      } else {
+        k_ess_partials<<<dim3((unsigned)ntiles, (unsigned)Be), 256, 0, c->stream>>>(c->lwbuf, Pl, ESS_TILE,
+                                                                                   c->essparts);
+        CHECK_LAUNCH(c);
+        k_ess_rank<<<1, 256, 0, c->stream>>>(c->essparts, ntiles, Be, c->essslice);
+        CHECK_LAUNCH(c);
+        TRY(gather(c, c->essslice, c->essgath, (size_t)Be * 3));
+        k_ess_final<<<1, 32, 0, c->stream>>>(c->essgath, c->G, Be, s, c->n, c->cfg.ess_frac, P, c->ctl);
+        CHECK_LAUNCH(c);
+        TRY(read_ctl(c));
+        sstar = c->hctl->s_star;
+      }
+      if (sstar > 0) {
+        k_take_lw<<<pgrid, 256, 0, c->stream>>>(c->lwbuf, sstar - s - 1, Pl, c->lw, c->L);
+        CHECK_LAUNCH(c);
+        c->t = sstar;
+        break;
+      }
+      s += Be;
+      B *= 2;
+    }
+  } else {
+    // ---- power tempering (R5): Delta phi on the 2^-48 grid of the remaining increment ----
+    const double rem = 1.0 - c->phi;
+    double dphi;
+    if (phi_target >= 0) {
+      if (!(phi_target > c->phi && phi_target <= 1.0)) return fail(c, SPS_E_CONFIG, "phi_target out of range");
+      dphi = phi_target - c->phi;
+    } else {
+      k_block_max<<<MX_BLOCKS, 256, 0, c->stream>>>(c->L, Pl, c->mx_parts);
+      k_max_reduce<<<1, 32, 0, c->stream>>>(c->mx_parts, MX_BLOCKS, c->mx_slice);
+      CHECK_LAUNCH(c);
+      TRY(gather(c, c->mx_slice, c->mx_gath, 1));
+      k_max_reduce<<<1, 32, 0, c->stream>>>(c->mx_gath, c->G, c->scal);
+      CHECK_LAUNCH(c);
+      auto round = [&](int ncand) -> sps_status {
+        k_power_partials<<<PW_BLOCKS, 256, 0, c->stream>>>(c->L, Pl, c->scal, c->ctl, ncand, rem, c->pw_parts);
+        k_power_rank<<<1, 64, 0, c->stream>>>(c->pw_parts, PW_BLOCKS, ncand, c->pw_slice);
+        CHECK_LAUNCH(c);
+        TRY(gather(c, c->pw_slice, c->pw_gath, 64 * 2));
+        k_power_decide<<<1, 32, 0, c->stream>>>(c->pw_gath, c->G, ncand, c->cfg.ess_frac, P, c->ctl);
+        CHECK_LAUNCH(c);
+        return SPS_OK;
+      };
+      TRY(round(0));
+      TRY(read_ctl(c));
+      if (c->hctl->q_ok_full) {
+        dphi = rem;
+      } else {
+        c->hctl->q_lo = 0;
+        c->hctl->q_hi = 1ull << 48;
+        CU(c, cudaMemcpyAsync(&c->ctl->q_lo, &c->hctl->q_lo, 2 * sizeof(unsigned long long), cudaMemcpyHostToDevice,
+                              c->stream));
+        for (int r = 0; r < 8; ++r) TRY(round(63));
+        TRY(read_ctl(c));
+        unsigned long long q = c->hctl->q_lo;
+        if (q == 0) q = 1;
+        dphi = ((double)q * 0x1p-48) * rem;
+      }
+    }
+    k_power_apply<<<pgrid, 256, 0, c->stream>>>(c->L, Pl, dphi, c->lw);
+    CHECK_LAUNCH(c);
+    c->phi = (dphi == rem) ? 1.0 : c->phi + dphi;
+  }
+  // ---- S phase + log-ML increments (R10) ----
+  c->ell += 1;
+  {
+    const size_t smem = (size_t)c->N * (8 + 4);
+    CU(c, cudaFuncSetAttribute(k_resample, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
+    k_resample<<<c->Jl, 1024, smem, c->stream>>>(c->lw, c->N, c->d, c->cfg.resampling, c->cfg.seed, (uint32_t)c->ell,
+                                                 (uint32_t)c->cfg.pass, c->g0, c->theta, c->L, c->lp, c->theta2,
+                                                 c->L2, c->lp2, c->grp_ms, c->Lj, nullptr, c->ctl);
+    CHECK_LAUNCH(c);
+    std::swap(c->theta, c->theta2);
+    std::swap(c->L, c->L2);
+    std::swap(c->lp, c->lp2);
+    TRY(gather(c, c->grp_ms, c->grp_ms_gath, (size_t)c->Jl * 2));
+    k_logml_pooled<<<1, 32, 0, c->stream>>>(c->grp_ms_gath, c->J, P, c->ctl);
+    CHECK_LAUNCH(c);
+  }
+  TRY(read_ctl(c));
+  const double inc = c->hctl->logml_inc;
+  c->logml += inc;
+  c->need_pre_moments = true;
+  c->cphase_done = true;
+  c->tr_t.push_back(c->t);
+  c->tr_phi.push_back(c->phi);
+  c->tr_inc.push_back(inc);
+  if (t_new) *t_new = c->t;
+  if (phi_new) *phi_new = c->phi;
+  if (logml_inc) *logml_inc = inc;
+  return SPS_OK;
+}
+
+sps_status sps_mphase(sps_ctx* c, int32_t R_fixed, int32_t* R_out, double* min_rne, int32_t* h_out) {
+  if (!c) return SPS_E_CONFIG;
+  CU(c, cudaSetDevice(c->cfg.device));
+  if (!c->cphase_done) return fail(c, SPS_E_STATE, "sps_mphase before sps_cphase");
+  const bool power = c->cfg.tempering == SPS_POWER_TEMPERING;
+  const int t1 = power ? c->n : c->t;
+  const double temper = power ? c->phi : 1.0;
+  const int64_t Pl = c->Pl;
+  if (c->need_pre_moments) {
+    TRY(moments(c));
+    TRY(finalize(c, 0));  // V of the resampled particles, chol(h V)
+    c->need_pre_moments = false;
+  }
+  int r = 0;
+  for (;;) {
+    r += 1;
+    if (R_fixed <= 0 && r > c->cfg.max_m_steps)
+      return fail(c, SPS_E_MIXING, "M phase did not reach RNE >= K in %d steps", c->cfg.max_m_steps);
+    // K8 propose
+    TRY(launch_draw(c, false, c->theta, c->Lprop, c->mstep, c->theta_s, c->lp_s));
+    // K1 proposal log-likelihood over [0, t_l)
+    int nch = 1;
+    TRY(launch_loglik(c, c->theta_s, c->d, Pl, 0, t1, c->part, c->max_chunks, &nch));
+    c->pairs += (double)c->P * t1;
+    // K9 accept
+    CU(c, cudaMemsetAsync(&c->ctl->acc, 0, sizeof(unsigned long long), c->stream));
+    k_accept<<<(unsigned)((Pl + 255) / 256), 256, 0, c->stream>>>(
+        c->theta, c->L, c->lp, c->theta_s, c->part, nch, c->lp_s, c->d, Pl, c->p0, temper, c->cfg.seed, c->mstep,
+        (uint32_t)c->cfg.pass, c->ctl, nullptr);
+    CHECK_LAUNCH(c);
+    c->mstep += 1;
+    // K6 + K7: moments of theta^(l,r) -> h, RNE, stop, next chol(h V)
+    TRY(moments(c));
+    TRY(finalize(c, 1));
+    TRY(read_ctl(c));
+    if (R_fixed > 0 ? r >= R_fixed : c->hctl->stop) break;
+  }
+  c->cphase_done = false;
+  c->tr_R.push_back(r);
+  c->tr_rne.push_back(c->hctl->minrne);
+  c->tr_h.push_back(c->hctl->h);
+  if (final_cycle(c)) c->finished = true;
+  if (R_out) *R_out = r;
+  if (min_rne) *min_rne = c->hctl->minrne;
+  if (h_out) *h_out = c->hctl->h;
+  return SPS_OK;
+}
+
+sps_status sps_logml(sps_ctx* c, double* logml, double* nse) {
+  if (!c) return SPS_E_CONFIG;
+  CU(c, cudaSetDevice(c->cfg.device));
+  if (logml) *logml = c->logml;
+  if (nse) {
+    TRY(gather(c, c->Lj, c->Lj_gath, (size_t)c->Jl));
+    k_logml_nse<<<1, 32, 0, c->stream>>>(c->Lj_gath, c->J, c->scal + 1);
+    CHECK_LAUNCH(c);
+    CU(c, cudaMemcpyAsync(nse, c->scal + 1, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CU(c, cudaStreamSynchronize(c->stream));
+  }
+  return SPS_OK;
+}
+
+sps_status sps_moments(sps_ctx* c, int32_t m, const double* A, double* mean, double* sd, double* nse, double* rne) {
+  if (!c || m < 0 || (m > 0 && !A)) return SPS_E_CONFIG;
+  if (m == 0) return SPS_OK;
+  CU(c, cudaSetDevice(c->cfg.device));
+  if (m > c->fn_cap) {
+    if (c->fn_A) cudaFree(c->fn_A);
+    if (c->fn_out) cudaFree(c->fn_out);
+    c->fn_A = c->fn_out = nullptr;
+    TRY(dalloc(c, &c->fn_A, (size_t)m * c->d));
+    TRY(dalloc(c, &c->fn_out, (size_t)m * 4));
+    c->fn_cap = m;
+  }
+  CU(c, cudaMemcpyAsync(c->fn_A, A, sizeof(double) * m * c->d, cudaMemcpyHostToDevice, c->stream));
+  TRY(moments(c));
+  const size_t smem = sizeof(double) * (c->d + c->J);
+  k_functional_stats<<<1, 256, smem, c->stream>>>(c->gath, c->G, c->slice_len, c->J, c->Jl, c->N, c->d, c->shift,
+                                                  c->fn_A, m, c->fn_out);
+  CHECK_LAUNCH(c);
+  std::vector<double> h((size_t)m * 4);
+  CU(c, cudaMemcpyAsync(h.data(), c->fn_out, sizeof(double) * m * 4, cudaMemcpyDeviceToHost, c->stream));
+  CU(c, cudaStreamSynchronize(c->stream));
+  for (int q = 0; q < m; ++q) {
+    if (mean) mean[q] = h[q * 4 + 0];
+    if (sd) sd[q] = h[q * 4 + 1];
+    if (nse) nse[q] = h[q * 4 + 2];
+    if (rne) rne[q] = h[q * 4 + 3];
+  }
+  return SPS_OK;
+}
+
+sps_status sps_run(sps_ctx* c, sps_report* rep) {
+  if (!c || !rep) return SPS_E_CONFIG;
+  sps_status st = SPS_OK;
+  while (!c->finished) {
+    st = sps_cphase(c, -1, -1.0, nullptr, nullptr, nullptr);
+    if (st != SPS_OK) break;
+    st = sps_mphase(c, 0, nullptr, nullptr, nullptr);
+    if (st != SPS_OK) break;
+  }
+  rep->status = st;
+  rep->L = c->ell;
+  rep->total_m_steps = 0;
+  for (int r : c->tr_R) rep->total_m_steps += r;
+  rep->h_final = c->hctl->h;
+  rep->pairs = c->pairs;
+  const int L = (int)c->tr_t.size();
+  for (int l = 0; l < std::min(L, rep->cap_cycles); ++l) {
+    if (rep->t_cycle) rep->t_cycle[l] = c->tr_t[l];
+    if (rep->phi_cycle) rep->phi_cycle[l] = c->tr_phi[l];
+    if (rep->logml_inc) rep->logml_inc[l] = c->tr_inc[l];
+    if (l < (int)c->tr_R.size()) {
+      if (rep->R_cycle) rep->R_cycle[l] = c->tr_R[l];
+      if (rep->min_rne) rep->min_rne[l] = c->tr_rne[l];
+      if (rep->h_cycle) rep->h_cycle[l] = c->tr_h[l];
+    }
+  }
+  if (st != SPS_OK) return st;
+  TRY(sps_logml(c, &rep->logml, &rep->logml_nse));
+  if (rep->n_report > 0) {
+    std::vector<double> A;
+    const double* fns = rep->report_fns;
+    if (!fns) {  // theta_c' xbar, c = 1..C-1
+      std::vector<double> mon((size_t)c->C * c->d);
+      std::vector<double> xbar(c->k);
+      CU(c, cudaMemcpyAsync(xbar.data(), c->xbar, sizeof(double) * c->k, cudaMemcpyDeviceToHost, c->stream));
+      CU(c, cudaStreamSynchronize(c->stream));
+      A.assign((size_t)rep->n_report * c->d, 0.0);
+      for (int r = 0; r < std::min(rep->n_report, c->C - 1); ++r)
+        for (int i = 0; i < c->k; ++i) A[(size_t)r * c->d + r * c->k + i] = xbar[i];
+      fns = A.data();
+    }
+    TRY(sps_moments(c, rep->n_report, fns, rep->mean, rep->sd, rep->nse, rep->rne));
+  }
+  return SPS_OK;
+}
+
+sps_status sps_get_particles(sps_ctx* c, double* theta_host, double* L_host, double* lp_host) {
+  if (!c) return SPS_E_CONFIG;
+  CU(c, cudaSetDevice(c->cfg.device));
+  if (theta_host)
+    CU(c, cudaMemcpyAsync(theta_host, c->theta, sizeof(double) * c->Pl * c->d, cudaMemcpyDeviceToHost, c->stream));
+  if (L_host) CU(c, cudaMemcpyAsync(L_host, c->L, sizeof(double) * c->Pl, cudaMemcpyDeviceToHost, c->stream));
+  if (lp_host) CU(c, cudaMemcpyAsync(lp_host, c->lp, sizeof(double) * c->Pl, cudaMemcpyDeviceToHost, c->stream));
+  CU(c, cudaStreamSynchronize(c->stream));
+  return SPS_OK;
+}
+
+sps_status sps_g_prior(const double* X, int32_t n, int32_t k, int32_t C, double g, int32_t device, double* cov_out) {
+  if (!X || !cov_out || n < 1 || k < 1 || C < 2 || k > 128) return SPS_E_CONFIG;
+  if (cudaSetDevice(device) != cudaSuccess) return SPS_E_CUDA;
+  const int d = k * (C - 1);
+  double *dX = nullptr, *dXtX = nullptr, *dcov = nullptr;
+  Ctl* dctl = nullptr;
+  Ctl h{};
+  sps_status st = SPS_OK;
+  if (cudaMalloc(&dX, sizeof(double) * n * k) || cudaMalloc(&dXtX, sizeof(double) * k * k) ||
+      cudaMalloc(&dcov, sizeof(double) * d * d) || cudaMalloc(&dctl, sizeof(Ctl)))
+    st = SPS_E_CUDA;
+  if (st == SPS_OK) {
+    cudaMemcpy(dX, X, sizeof(double) * n * k, cudaMemcpyHostToDevice);
+    cudaMemset(dctl, 0, sizeof(Ctl));
+    k_xtx<<<(k * k + 127) / 128, 128>>>(dX, n, k, dXtX);
+    const size_t smem = sizeof(double) * 2 * k * k;
+    cudaFuncSetAttribute(k_g_prior, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024);
+    k_g_prior<<<1, 128, smem>>>(dXtX, n, k, C, g, dcov, dctl);
+    if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) st = SPS_E_CUDA;
+  }
+  if (st == SPS_OK) {
+    cudaMemcpy(&h, dctl, sizeof(Ctl), cudaMemcpyDeviceToHost);
+    if (h.err) st = SPS_E_DATA;
+    else cudaMemcpy(cov_out, dcov, sizeof(double) * d * d, cudaMemcpyDeviceToHost);
+  }
+  cudaFree(dX);
+  cudaFree(dXtX);
+  cudaFree(dcov);
+  cudaFree(dctl);
+  return st;
+}
+
+// ---------------------------------------------------------------- test exports
+#define TCU(x)                                  \
+  do {                                          \
+    if ((x) != cudaSuccess) return SPS_E_CUDA;  \
+  } while (0)
+
+sps_status sps_test_philox(int32_t n, const uint32_t* ctr, const uint32_t* key, uint32_t* out) {
+  if (n <= 0) return SPS_E_CONFIG;
+  uint32_t *dc = nullptr, *dout = nullptr;
+  TCU(cudaMalloc(&dc, 16 * n));
+  TCU(cudaMalloc(&dout, 16 * n));
+  TCU(cudaMemcpy(dc, ctr, 16 * n, cudaMemcpyHostToDevice));
+  k_test_philox<<<(n + 127) / 128, 128>>>(n, dc, key[0], key[1], dout);
+  TCU(cudaGetLastError());
+  TCU(cudaMemcpy(out, dout, 16 * n, cudaMemcpyDeviceToHost));
+  cudaFree(dc);
+  cudaFree(dout);
+  return SPS_OK;
+}
+
+sps_status sps_test_normals(uint64_t seed, uint32_t id, uint32_t step, uint32_t tag, uint32_t pass, int32_t count,
+                            double* out) {
+  if (count <= 0) return SPS_E_CONFIG;
+  double* d = nullptr;
+  TCU(cudaMalloc(&d, sizeof(double) * count));
+  k_test_normals<<<(count / 2 + 128) / 128, 128>>>(seed, id, step, tag, pass, count, d);
+  TCU(cudaGetLastError());
+  TCU(cudaMemcpy(out, d, sizeof(double) * count, cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  return SPS_OK;
+}
+
+sps_status sps_test_portable(int32_t which, int32_t n, const double* x, double* out) {
+  if (n <= 0 || which < 0 || which > 2) return SPS_E_CONFIG;
+  const int on = which == 2 ? 2 * n : n;
+  double *dx = nullptr, *dout = nullptr;
+  TCU(cudaMalloc(&dx, sizeof(double) * n));
+  TCU(cudaMalloc(&dout, sizeof(double) * on));
+  TCU(cudaMemcpy(dx, x, sizeof(double) * n, cudaMemcpyHostToDevice));
+  k_test_portable<<<(n + 127) / 128, 128>>>(which, n, dx, dout);
+  TCU(cudaGetLastError());
+  TCU(cudaMemcpy(out, dout, sizeof(double) * on, cudaMemcpyDeviceToHost));
+  cudaFree(dx);
+  cudaFree(dout);
+  return SPS_OK;
+}
+
+sps_status sps_test_resample_int(int32_t N, const uint64_t* q, int32_t scheme, const uint64_t* a, int32_t* anc) {
+  if (N < 1 || N > 16384 || scheme < 0 || scheme > 2) return SPS_E_CONFIG;
+  uint64_t *dq = nullptr, *da = nullptr;
+  int32_t* danc = nullptr;
+  TCU(cudaMalloc(&dq, 8 * N));
+  TCU(cudaMalloc(&da, 8 * N));
+  TCU(cudaMalloc(&danc, 4 * N));
+  TCU(cudaMemcpy(dq, q, 8 * N, cudaMemcpyHostToDevice));
+  TCU(cudaMemcpy(da, a, 8 * N, cudaMemcpyHostToDevice));
+  const size_t smem = (size_t)N * 12;
+  TCU(cudaFuncSetAttribute(k_test_resample_int, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
+  k_test_resample_int<<<1, 1024, smem>>>(N, dq, scheme, da, danc);
+  TCU(cudaGetLastError());
+  TCU(cudaMemcpy(anc, danc, 4 * N, cudaMemcpyDeviceToHost));
+  cudaFree(dq);
+  cudaFree(da);
+  cudaFree(danc);
+  return SPS_OK;
+}
+
+sps_status sps_test_resample_group(int32_t N, const double* lw, int32_t scheme, uint64_t seed, uint32_t group,
+                                   uint32_t cycle, uint32_t pass, int32_t* anc) {
+  if (N < 1 || N > 16384 || scheme < 0 || scheme > 2) return SPS_E_CONFIG;
+  double *dlw = nullptr, *dth = nullptr, *dth2 = nullptr, *dL = nullptr, *dL2 = nullptr, *dms = nullptr,
+         *dLj = nullptr;
+  int32_t* danc = nullptr;
+  Ctl* dctl = nullptr;
+  TCU(cudaMalloc(&dlw, 8 * N));
+  TCU(cudaMalloc(&dth, 8 * N));
+  TCU(cudaMalloc(&dth2, 8 * N));
+  TCU(cudaMalloc(&dL, 8 * N));
+  TCU(cudaMalloc(&dL2, 8 * N));
+  TCU(cudaMalloc(&dms, 16));
+  TCU(cudaMalloc(&dLj, 8));
+  TCU(cudaMalloc(&danc, 4 * N));
+  TCU(cudaMalloc(&dctl, sizeof(Ctl)));
+  TCU(cudaMemset(dctl, 0, sizeof(Ctl)));
+  TCU(cudaMemset(dLj, 0, 8));
+  TCU(cudaMemset(dth, 0, 8 * N));
+  TCU(cudaMemset(dL, 0, 8 * N));
+  TCU(cudaMemcpy(dlw, lw, 8 * N, cudaMemcpyHostToDevice));
+  const size_t smem = (size_t)N * 12;
+  TCU(cudaFuncSetAttribute(k_resample, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
+  // the kernel's group index is blockIdx.x + g0: launch one block with g0 = group
+  k_resample<<<1, 1024, smem>>>(dlw, N, 1, scheme, seed, cycle, pass, (int)group, dth, dL, dL, dth2, dL2, dL2, dms,
+                                dLj, danc, dctl);
+  TCU(cudaGetLastError());
+  TCU(cudaMemcpy(anc, danc, 4 * N, cudaMemcpyDeviceToHost));
+  for (void* p : {(void*)dlw, (void*)dth, (void*)dth2, (void*)dL, (void*)dL2, (void*)dms, (void*)dLj, (void*)danc,
+                  (void*)dctl})
+    cudaFree(p);
+  return SPS_OK;
+}
+
+sps_status sps_test_accept(int64_t P, const double* delta, uint64_t seed, uint32_t step, uint32_t pass,
+                           uint8_t* flags) {
+  if (P <= 0) return SPS_E_CONFIG;
+  double* dd = nullptr;
+  uint8_t* df = nullptr;
+  TCU(cudaMalloc(&dd, 8 * P));
+  TCU(cudaMalloc(&df, P));
+  TCU(cudaMemcpy(dd, delta, 8 * P, cudaMemcpyHostToDevice));
+  k_test_accept<<<(unsigned)((P + 255) / 256), 256>>>(P, dd, seed, step, pass, df);
+  TCU(cudaGetLastError());
+  TCU(cudaMemcpy(flags, df, P, cudaMemcpyDeviceToHost));
+  cudaFree(dd);
+  cudaFree(df);
+  return SPS_OK;
+}
+
+}  // extern "C"
