@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""bench.py -- SPS runs to posterior (Algorithm 2) on the
+configs[1] workload of BASELINE.json: German-credit-shaped synthetic binary
+logit, n = 1000, k = 25, J = 64 groups x N = 1024 particles per GPU, g = 1/16.
+
+One "step" = one complete adaptive SPS run (all SURVEY §8(a) rows: prior
+draws, C phases, resampling, M phases with the fused fp64 log-likelihood,
+accounting) through the C ABI on data resident in HBM.  `value` = particle x
+observation log-likelihood terms evaluated per second, whole job (all ranks).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1: launched by torch.distributed.run, one rank per GPU, group sharding
+(weak scaling: 64 groups x 1024 particles per GPU, J = 64 N in total).
+--impl reference: the CPU oracle (oracle/, the tier's reference arm) on a
+bounded sample of the same workload, on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+WORKLOAD = dict(name="cfg2", n=1000, k=25, C=2, J_per_gpu=64, N=1024, g=1.0 / 16)
+WORKLOAD_DESC = ("configs[1]: German-credit-shaped synthetic binary logit, n=1000, k=25 (1 + 3 continuous + 21 "
+                 "binary covariates, ~30% positives), J=64 groups x N=1024 particles per GPU, Zellner g=1/16, "
+                 "data tempering (paper default), residual resampling, full Algorithm 2 to posterior")
+ORACLE_SAMPLE = dict(J=16, N=256)
+# FP64 pipe peak measured on this pool's B200s (profiles/r01_fp64_peaks.json: DMMA 37.07 TF,
+# 64 FMA/clk/SM at 1.96 GHz; DFMA shares the same pipe).  MEASURED_PEAKS.json carries no FP64 figure.
+FP64_PEAK_TFLOPS = 37.07
+# FP64-pipe instructions per pair in K1's binary epilogue (1 DADD relu-sum,
+# 10 exp, 1 DADD, 1.5 DMUL), counted from the SASS of k_loglik_bin.
+EPILOGUE_DP_OPS_BINARY = 13.5
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(self.gpu)], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sms, maxs, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sms.append(float(f[1]))
+                maxs.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        if not sms:
+            return None
+        return {"sm_mhz": statistics.median(sms), "sm_max_mhz": max(maxs), "reasons": sorted(reasons),
+                "samples": len(sms)}
+
+
+# ------------------------------------------------------------------ oracle (CPU) arm
+def oracle_sample(X, y, cov, seed):
+    import oracle
+
+    t0 = time.perf_counter()
+    r = oracle.run(X, y, 2, ORACLE_SAMPLE["J"], ORACLE_SAMPLE["N"], seed=seed, prior_mean=np.zeros(X.shape[1]),
+                   prior_cov=cov, n_threads=os.cpu_count())
+    dt = time.perf_counter() - t0
+    assert r["status"] == 0, r["status"]
+    return r["pairs"], dt
+
+
+def oracle_cov(X):
+    import oracle
+
+    return oracle.g_prior(X, 2, WORKLOAD["g"])
+
+
+def sample_desc():
+    return (f"oracle/ full Algorithm 2 run on the cfg2 data (n=1000, k=25, g=1/16) with J={ORACLE_SAMPLE['J']} x "
+            f"N={ORACLE_SAMPLE['N']} particles (a bounded sample of the J=64 x N=1024 workload), OpenMP over "
+            f"particles on {os.cpu_count()} host threads; pairs/s over the whole run")
+
+
+def run_reference(args, rank, world):
+    import sps_synth
+
+    if rank != 0:
+        return
+    X, y = sps_synth.config_data("cfg2")
+    cov = oracle_cov(X)
+    for w in range(args.warmup):
+        oracle_sample(X, y, cov, seed=100 + w)
+    pairs = secs = 0.0
+    for s in range(args.steps):
+        p, dt = oracle_sample(X, y, cov, seed=1 + s)
+        pairs += p
+        secs += dt
+    v = pairs / secs
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "pairs/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD_DESC, "sample": sample_desc()},
+            "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": os.cpu_count(), "kind": "oracle",
+                             "sample": sample_desc()},
+            "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_1304_4333_b200 as sps
+    import sps_synth
+
+    assert args.warmup >= 3 or os.environ.get("BENCH_ALLOW_SHORT"), "the contract needs >= 3 warm-up steps"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        ids = [sps.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(ids, src=0)
+        nccl_id = ids[0]
+    else:
+        nccl_id = None
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    X, y = sps_synth.config_data("cfg2")
+    n, k = X.shape
+    cov = sps.g_prior(X, 2, WORKLOAD["g"], device=local)
+    J = WORKLOAD["J_per_gpu"] * world
+    N = WORKLOAD["N"]
+    stream = torch.cuda.Stream(device=dev)
+    ctx = sps.Sps(X, y, np.zeros(k), cov, J=J, N=N, seed=1, rank=rank, nranks=world, nccl_id=nccl_id,
+                  device=local, stream=stream.cuda_stream)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+
+    for w in range(args.warmup):
+        ctx.reset(seed=10_000 + w)
+        ctx.run()
+
+    clocks = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    times, pairs, launches = [], 0.0, 0
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    last = None
+    for s in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(float(s))  # L2 flush before every timed step (outside the step's events)
+        ev0.record(stream)
+        ctx.reset(seed=1 + s)
+        last = ctx.run()
+        ev1.record(stream)
+        stream.synchronize()
+        times.append(ev0.elapsed_time(ev1))
+        pairs += last["pairs"]
+        launches += ctx.counters()["launches"]
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    tot_ms = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot_ms, op=dist.ReduceOp.MAX)
+    tot_ms = float(tot_ms.item())
+    value = pairs / (tot_ms / 1e3)
+
+    # ---- roofline of the dominant kernel (K1) measured inside a real run, events on the ctx stream
+    ctx.set_profiling(True)
+    ctx.reset(seed=999)
+    prof_run = ctx.run()
+    cnt = ctx.counters()
+    ctx.set_profiling(False)
+    k1_avg_ms = cnt["k1_ms"] / max(cnt["k1_launches"], 1)
+    pairs_per_launch = cnt["k1_pairs"] / max(cnt["k1_launches"], 1)
+    ops_per_pair = 2 * k * (WORKLOAD["C"] - 1) + EPILOGUE_DP_OPS_BINARY
+    achieved = pairs_per_launch * ops_per_pair / (k1_avg_ms * 1e-3) / 1e12
+    pipe_tflops = pairs_per_launch * 2 * (k * (WORKLOAD["C"] - 1) + EPILOGUE_DP_OPS_BINARY) / (k1_avg_ms * 1e-3) / 1e12
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", "r01_k1_ncu.json")
+    if os.path.exists(tr_path):
+        traffic = json.load(open(tr_path)).get("dram_bytes_per_launch")
+    k1_share = cnt["k1_ms"] / max(sum(times) / max(len(times), 1), 1e-9)
+
+    # ---- full-data K1 evaluation (P x n pairs in one launch): the M phase's largest case
+    th = torch.randn(ctx.P_local, ctx.d, dtype=torch.float64, device=dev) * 0.3
+    out = torch.empty(ctx.P_local, dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+    for _ in range(3):
+        ctx.loglik(th.data_ptr(), ctx.P_local, ctx.d, 0, n, out.data_ptr())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 20
+    e0.record(stream)
+    for _ in range(reps):
+        ctx.loglik(th.data_ptr(), ctx.P_local, ctx.d, 0, n, out.data_ptr())
+    e1.record(stream)
+    stream.synchronize()
+    full_ms = e0.elapsed_time(e1) / reps
+    full_pairs_s = ctx.P_local * n / (full_ms * 1e-3)
+
+    # ---- end to end through the public API with host buffers (create from host arrays, run, report to host)
+    e2e = None
+    if not args.no_e2e:
+        Xp = torch.from_numpy(X).pin_memory().numpy()
+        yp = torch.from_numpy(y).pin_memory().numpy()
+        h2d = Xp.nbytes + yp.nbytes + 8 * k + 8 * k * k
+        barrier()
+        torch.cuda.synchronize()
+        wall = 0.0
+        e2e_pairs = 0.0
+        d2h = 0
+        for s in range(args.steps):
+            t0 = time.perf_counter()
+            c2 = sps.Sps(Xp, yp, np.zeros(k), cov, J=J, N=N, seed=1 + s, rank=rank, nranks=world,
+                         nccl_id=None if world == 1 else nccl_id, device=local)
+            r2 = c2.run()
+            c2.close()
+            wall += time.perf_counter() - t0
+            e2e_pairs += r2["pairs"]
+            L2 = r2["L"]
+            d2h = 4 * 6 * L2 + 8 * 6 + 32  # per-cycle trace + moments + logml
+        wt = torch.tensor([wall], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(wt, op=dist.ReduceOp.MAX)
+        e2e = {"value": e2e_pairs / float(wt.item()), "unit": "pairs/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h)}
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        p, dt = oracle_sample(X, y, oracle_cov(X), seed=7)
+        cpu = {"value": p / dt, "unit": "pairs/s", "cores": os.cpu_count(), "kind": "oracle",
+               "sample": sample_desc(), "seconds": dt}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD_DESC, "n": n, "k": k, "C": 2, "J": J, "N": N,
+                       "global_particles": J * N, "parallelism": f"group-sharded x{world}" if world > 1 else "1 GPU",
+                       "l2": "flushed (256 MiB device write) before every timed step",
+                       "wall_s_to_posterior": tot_ms / args.steps / 1e3},
+            "clocks": clk,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "roofline": {"bound": "alu", "kernel": "k_loglik_bin<25,2> (K1, fused fp64 loglik)",
+                         "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                         "ops_per_pair": ops_per_pair, "k1_avg_ms": k1_avg_ms,
+                         "pairs_per_launch": pairs_per_launch, "k1_launches_per_run": cnt["k1_launches"],
+                         "k1_share_of_step": k1_share,
+                         "fp64_pipe_frac": pipe_tflops / FP64_PEAK_TFLOPS,
+                         "peak_source": "measured FP64 pipe (profiles/r01_fp64_peaks.json)",
+                         "full_data_eval": {"ms": full_ms, "pairs_per_s": full_pairs_s,
+                                            "frac": full_pairs_s * ops_per_pair / 1e12 / FP64_PEAK_TFLOPS}},
+            "cpu_baseline": cpu,
+            "run": {"logml": last["logml"], "logml_nse": last["logml_nse"], "cycles": last["L"],
+                    "m_steps": last["total_m_steps"], "mean": list(last["mean"]), "nse": list(last["nse"]),
+                    "pairs_per_run": last["pairs"], "syncs_per_run": cnt["syncs"]},
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,35 @@
+"""One cfg2 SPS run (after one warm-up run) for ncu launch lists / captures.
+
+    python tools/profile_run.py [--runs R] [--loglik-only]
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import paper_1304_4333_b200 as sps  # noqa: E402
+import sps_synth  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--runs", type=int, default=1)
+ap.add_argument("--loglik-only", action="store_true")
+a = ap.parse_args()
+X, y = sps_synth.config_data("cfg2")
+cov = sps.g_prior(X, 2, 1.0 / 16)
+ctx = sps.Sps(X, y, np.zeros(25), cov, J=64, N=1024, seed=1)
+if a.loglik_only:
+    import torch
+
+    th = torch.randn(65536, 25, dtype=torch.float64, device="cuda") * 0.3
+    for _ in range(5):
+        ctx.loglik_tensor(th)
+else:
+    ctx.run()  # warm-up
+    for r in range(a.runs):
+        ctx.reset(seed=2 + r)
+        rep = ctx.run()
+        print("run", r, "cycles", rep["L"], "msteps", rep["total_m_steps"], "logml", rep["logml"])
+ctx.close()
