@@ -243,6 +243,7 @@ def main():
     if os.path.exists(tr_path):
         traffic = json.load(open(tr_path)).get("dram_bytes_per_launch")
     k1_share = cnt["k1_ms"] / max(sum(times) / max(len(times), 1), 1e-9)
+    breakdown = {k: {"ms": round(v, 3), "n": cnt["cat_n"][k]} for k, v in cnt["cat_ms"].items() if cnt["cat_n"][k]}
 
     # ---- full-data K1 evaluation (P x n pairs in one launch): the M phase's largest case
     th = torch.randn(ctx.P_local, ctx.d, dtype=torch.float64, device=dev) * 0.3
@@ -319,7 +320,8 @@ def main():
             "cpu_baseline": cpu,
             "run": {"logml": last["logml"], "logml_nse": last["logml_nse"], "cycles": last["L"],
                     "m_steps": last["total_m_steps"], "mean": list(last["mean"]), "nse": list(last["nse"]),
-                    "pairs_per_run": last["pairs"], "syncs_per_run": cnt["syncs"]},
+                    "pairs_per_run": last["pairs"], "syncs_per_run": cnt["syncs"],
+                    "profiled_breakdown_ms": breakdown},
         }
         print(json.dumps(line), flush=True)
     ctx.close()

@@ -166,6 +166,11 @@ typedef struct sps_counters {
   double k1_pairs;      /* particle x observation pairs evaluated by K1 launches         */
   double k1_ms;         /* summed CUDA-event duration of K1 launches (profiling on)      */
   int64_t syncs;        /* host synchronizations                                         */
+  /* profiling: per-category event time (ms) and count; categories: 0 K1 loglik, 1 propose,
+   * 2 accept+moments, 3 moments reduce, 4 gather, 5 finalize, 6 control copy, 7 C phase,
+   * 8 resample, 9 other */
+  double cat_ms[16];
+  int64_t cat_n[16];
 } sps_counters;
 
 /* Profiling: when on, every K1 launch is bracketed by CUDA events on the

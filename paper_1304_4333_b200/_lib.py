@@ -73,7 +73,8 @@ EXPORTED = [
 
 class Counters(C.Structure):
     _fields_ = [("launches", C.c_int64), ("k1_launches", C.c_int64), ("k1_pairs", C.c_double),
-                ("k1_ms", C.c_double), ("syncs", C.c_int64)]
+                ("k1_ms", C.c_double), ("syncs", C.c_int64), ("cat_ms", C.c_double * 16),
+                ("cat_n", C.c_int64 * 16)]
 
 
 class Config(C.Structure):

@@ -153,8 +153,11 @@ class Sps:
     def counters(self):
         c = Counters()
         _check(lib().sps_get_counters(self.ctx, C.byref(c)), self.ctx)
+        cats = ["k1", "propose", "accept_moments", "moments_reduce", "gather", "finalize", "ctl_copy", "cphase",
+                "resample", "other", "c10", "c11", "c12", "c13", "host_mstep_launch", "host_mstep_wait"]
         return dict(launches=c.launches, k1_launches=c.k1_launches, k1_pairs=c.k1_pairs, k1_ms=c.k1_ms,
-                    syncs=c.syncs)
+                    syncs=c.syncs, cat_ms={k: c.cat_ms[i] for i, k in enumerate(cats)},
+                    cat_n={k: c.cat_n[i] for i, k in enumerate(cats)})
 
     def logml(self):
         v, nse = C.c_double(), C.c_double()

@@ -147,6 +147,17 @@ __device__ __forceinline__ void normal_pair(uint64_t seed, uint32_t i, uint32_t 
   *z1 = __dmul_rn(r, s);
 }
 
+// ----------------------------------------------------------------- async copies
+// cp.async (LDGSTS) of 8 bytes global -> shared; all issued copies of a thread
+// are waited by cp_async_wait_all (one latency round for a whole staging phase).
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
 // ----------------------------------------------------------------- reductions
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {

@@ -17,7 +17,7 @@ struct Ctl {
   int err;         // sticky error code (ERR_*)
   int s_star;      // C phase: first crossing observation (1-based), -1 = none in chunk
   int chol_ridge;  // the last Cholesky needed the ridge retry
-  int pad0;
+  int steps_done;  // M steps executed since the phase began (speculative launches skip)
   unsigned long long acc;  // accepted proposals, this rank, last step
   double minrne;   // min monitor RNE after the last step
   double logml_inc;
@@ -85,8 +85,8 @@ __device__ bool block_cholesky(double* A, int d, int* sflag) {
     }
     __syncthreads();
     if (!*sflag) return false;
-    const double ljj = A[j * d + j];
-    for (int i = j + 1 + threadIdx.x; i < d; i += blockDim.x) A[i * d + j] /= ljj;
+    const double rjj = 1.0 / A[j * d + j];
+    for (int i = j + 1 + threadIdx.x; i < d; i += blockDim.x) A[i * d + j] *= rjj;
     __syncthreads();
     const int m = d - j - 1;
     for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
@@ -159,196 +159,6 @@ __global__ void k_g_prior(const double* __restrict__ XtX, int n, int k, int C, d
   }
 }
 
-// ============================================================ prior draws / proposals
-// Prior kernel lp = -1/2 |Lprior^-1 (theta - mu)|^2, forward
-// substitution with Lprior in shared memory.
-template <int DMAX>
-__device__ __forceinline__ double prior_quad(const double* th, const double* sLp, const double* mu, int d) {
-  double w[DMAX];
-  double q = 0.0;
-#pragma unroll
-  for (int i = 0; i < DMAX; ++i) {
-    if (i < d) {
-      double t = th[i] - mu[i];
-#pragma unroll
-      for (int j = 0; j < i; ++j) t -= sLp[i * d + j] * w[j];
-      w[i] = t / sLp[i * d + i];
-      q += w[i] * w[i];
-    }
-  }
-  return -0.5 * q;
-}
-
-// K10 (Algorithm 1 step 1): theta = mu + Lprior z, z from the
-// INIT stream of global particle id (R15); lp; L = 0.
-// K8 (Algorithm 2 step 2(c)i): theta* = theta + Lprop z, z from
-// the PROPOSAL stream (id = global particle, step = global M-step index); lp*.
-template <int DMAX, bool INIT>
-__global__ void __launch_bounds__(128) k_draw(const double* __restrict__ base, const double* __restrict__ Lz,
-                                              const double* __restrict__ Lprior, const double* __restrict__ mu, int d,
-                                              int64_t P, int64_t p0, uint64_t seed, uint32_t step, uint32_t pass,
-                                              double* __restrict__ out, double* __restrict__ lp_out,
-                                              Ctl* ctl, const int* __restrict__ stop) {
-  extern __shared__ double sm[];
-  if (stop && *stop) return;
-  double* sL = sm;              // d x d draw factor
-  double* sLp = sm + d * d;     // d x d prior factor
-  double* smu = sm + 2 * d * d; // d
-  for (int i = threadIdx.x; i < d * d; i += blockDim.x) {
-    sL[i] = Lz[i];
-    sLp[i] = Lprior[i];
-  }
-  for (int i = threadIdx.x; i < d; i += blockDim.x) smu[i] = mu[i];
-  __syncthreads();
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= P) return;
-  const uint32_t gid = (uint32_t)(p0 + p);
-  double z[DMAX], th[DMAX];
-#pragma unroll
-  for (int i = 0; i < DMAX; i += 2) {
-    if (i < d) {
-      double z0, z1;
-      normal_pair(seed, (uint32_t)(i / 2), gid, step, INIT ? TAG_INIT : TAG_PROPOSAL, pass, &z0, &z1);
-      z[i] = z0;
-      if (i + 1 < DMAX) z[i + 1] = z1;
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < DMAX; ++i) {
-    if (i < d) {
-      double s = INIT ? smu[i] : base[p * d + i];
-#pragma unroll
-      for (int j = 0; j <= i; ++j) s = fma(sL[i * d + j], z[j], s);
-      th[i] = s;
-    }
-  }
-  double chk = 0.0;
-#pragma unroll
-  for (int i = 0; i < DMAX; ++i)
-    if (i < d) {
-      out[p * d + i] = th[i];
-      chk += th[i];
-    }
-  if (!isfinite(chk)) atomicExch(&ctl->err, ERR_NUMERIC);
-  lp_out[p] = prior_quad<DMAX>(th, sLp, smu, d);
-}
-
-// K9 accept (R16): L* = sum of chunk partials; delta =
-// temper (L* - L) + (lp* - lp); accept iff plog(u) < delta, u the ACCEPT
-// uniform of (global particle, M-step).  Counts accepts; flags non-finite L*.
-__global__ void __launch_bounds__(256) k_accept(double* __restrict__ theta, double* __restrict__ L,
-                                                double* __restrict__ lp, const double* __restrict__ theta_s,
-                                                const double* __restrict__ part, int nchunks,
-                                                const double* __restrict__ lp_s, int d, int64_t P, int64_t p0,
-                                                double temper, uint64_t seed, uint32_t step, uint32_t pass, Ctl* ctl,
-                                                const int* __restrict__ stop) {
-  __shared__ long long scratch[32];
-  if (stop && *stop) return;
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  long long acc = 0;
-  if (p < P) {
-    double Ls = part[p];
-    for (int c = 1; c < nchunks; ++c) Ls += part[(int64_t)c * P + p];
-    if (!isfinite(Ls)) atomicExch(&ctl->err, ERR_NUMERIC);
-    const double delta = temper * (Ls - L[p]) + (lp_s[p] - lp[p]);
-    const u4 w = stream_block(seed, 0u, (uint32_t)(p0 + p), step, TAG_ACCEPT, pass);
-    if (plog(u01(w.x, w.y)) < delta) {
-      acc = 1;
-      for (int i = 0; i < d; ++i) theta[p * d + i] = theta_s[p * d + i];
-      L[p] = Ls;
-      lp[p] = lp_s[p];
-    }
-  }
-  acc = block_sum(acc, scratch);
-  if (threadIdx.x == 0 && acc) atomicAdd(&ctl->acc, (unsigned long long)acc);
-}
-
-// ============================================================ M phase moments (K6)
-// Grid (nblk, ceil(ntri / MOM_ENT)): block x = `pp` consecutive particles of one
-// group, block y = a range of MOM_ENT lower-triangle entries.  Outputs per
-// block the group-sum partial (d; y == 0 only) and the shifted second-moment
-// partial sum (theta - c)(theta - c)' over its particles, c = shift.
-constexpr int MOM_TILE = 64;
-constexpr int MOM_ENT = 1024;  // 4 entries per thread at 256 threads
-__global__ void __launch_bounds__(256) k_moments_partial(const double* __restrict__ theta, int d, int pp,
-                                                         const double* __restrict__ shift,
-                                                         double* __restrict__ gpart, double* __restrict__ mpart,
-                                                         const int* __restrict__ stop) {
-  extern __shared__ double sm[];
-  if (stop && *stop) return;
-  double* tile = sm;  // MOM_TILE x d, centered
-  const int ntri = d * (d + 1) / 2;
-  const int64_t pstart = (int64_t)blockIdx.x * pp;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  int ei[4], el[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int e = blockIdx.y * MOM_ENT + threadIdx.x + q * blockDim.x;
-    int i = 0;
-    while ((i + 1) * (i + 2) / 2 <= e) ++i;
-    ei[q] = e < ntri ? i : -1;
-    el[q] = e < ntri ? e - i * (i + 1) / 2 : 0;
-  }
-  double gsum = 0.0;
-  const bool do_g = blockIdx.y == 0 && threadIdx.x < d;
-  for (int base = 0; base < pp; base += MOM_TILE) {
-    const int cnt = min(MOM_TILE, pp - base);
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < cnt * d; idx += blockDim.x) {
-      const int r = idx / d, c = idx % d;
-      tile[idx] = theta[(pstart + base + r) * d + c] - shift[c];
-    }
-    __syncthreads();
-    if (do_g)
-      for (int r = 0; r < cnt; ++r) gsum += tile[r * d + threadIdx.x];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (ei[q] >= 0) {
-        const int i = ei[q], l = el[q];
-        double s = acc[q];
-        for (int r = 0; r < cnt; ++r) s = fma(tile[r * d + i], tile[r * d + l], s);
-        acc[q] = s;
-      }
-    }
-  }
-  // group-sum partial is of (theta - c): add back pp * c
-  if (do_g) gpart[(int64_t)blockIdx.x * d + threadIdx.x] = gsum + (double)pp * shift[threadIdx.x];
-#pragma unroll
-  for (int q = 0; q < 4; ++q)
-    if (ei[q] >= 0) mpart[(int64_t)blockIdx.x * ntri + blockIdx.y * MOM_ENT + threadIdx.x + q * blockDim.x] = acc[q];
-}
-
-// Reduce block partials (block order) into this rank's packed stats slice:
-// [J_local x d group sums | d x d second moment (full, symmetric) | acc | err].
-__global__ void k_moments_reduce(const double* __restrict__ gpart, const double* __restrict__ mpart, int nblk,
-                                 int blk_per_group, int Jl, int d, Ctl* ctl, double* __restrict__ slice,
-                                 const int* __restrict__ stop) {
-  if (stop && *stop) return;
-  const int ntri = d * (d + 1) / 2;
-  const int total = Jl * d + ntri;
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
-    if (idx < Jl * d) {
-      const int j = idx / d, c = idx % d;
-      double s = 0.0;
-      for (int b = 0; b < blk_per_group; ++b) s += gpart[(int64_t)(j * blk_per_group + b) * d + c];
-      slice[idx] = s;
-    } else {
-      const int e = idx - Jl * d;
-      double s = 0.0;
-      for (int b = 0; b < nblk; ++b) s += mpart[(int64_t)b * ntri + e];
-      int i = 0;
-      while ((i + 1) * (i + 2) / 2 <= e) ++i;
-      const int l = e - i * (i + 1) / 2;
-      slice[Jl * d + i * d + l] = s;
-      slice[Jl * d + l * d + i] = s;
-    }
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    slice[Jl * d + d * d] = (double)ctl->acc;
-    slice[Jl * d + d * d + 1] = (double)ctl->err;
-  }
-}
-
 struct FinArgs {
   const double* gath;  // G slices of `slice_len` doubles (rank order)
   int G, slice_len;
@@ -359,120 +169,15 @@ struct FinArgs {
   const double* mon;   // monitors (nmon x d)
   int nmon;
   int mode;            // 0: moments of resampled particles (no h / RNE); 1: after an M step
-  double K;            // RNE target
+  double K;            // RNE target; <= 0: never stop (fixed number of steps)
   int h_step, h_min, h_max;
   double accept_target;
   Ctl* ctl;
   const int* stop_in;  // skip if already stopped (speculative launches)
   double* rne_out;     // nmon RNEs (may be null)
+  Ctl* host_out;       // mapped pinned host slot for the control block (may be null)
+  long long* trace;    // debug: clock64 at phase boundaries (may be null)
 };
-
-// K7 (Algorithm 2 step 2(c)): theta-bar and pooled V (R11) from
-// the gathered stats; h update from the pooled acceptance (ii, R6); monitor
-// RNEs and the stop flag (iii, R12, R14); Cholesky of (h/100) V with one ridge
-// retry (R13).  One block; every rank computes the identical result.
-__global__ void __launch_bounds__(256) k_finalize(FinArgs f) {
-  extern __shared__ double sm[];
-  __shared__ int flag;
-  __shared__ double red[32];
-  if (f.stop_in && *f.stop_in) return;
-  const int d = f.d;
-  double* sV = sm;             // d x d
-  double* sbar = sm + d * d;   // d
-  double* sA = sbar + d;       // d x d (Cholesky work)
-  double* sg = sA + d * d;     // J (monitor group means)
-  const double P = (double)f.J * (double)f.N;
-  const int gs_len = f.Jl * d;
-  // theta-bar from group sums in group order
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    double s = 0.0;
-    for (int j = 0; j < f.J; ++j) {
-      const int r = j / f.Jl, jl = j % f.Jl;
-      s += f.gath[(int64_t)r * f.slice_len + jl * d + i];
-    }
-    sbar[i] = s / P;
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) {
-    const int i = idx / d, l = idx % d;
-    double m = 0.0;
-    for (int r = 0; r < f.G; ++r) m += f.gath[(int64_t)r * f.slice_len + gs_len + idx];
-    const double ci = sbar[i] - f.shift[i], cl = sbar[l] - f.shift[l];
-    sV[idx] = (m - P * ci * cl) / (P - 1.0);
-  }
-  __syncthreads();
-  int h = f.ctl->h;
-  if (f.mode == 1) {
-    if (threadIdx.x == 0) {
-      double acc = 0.0, err = 0.0;
-      for (int r = 0; r < f.G; ++r) {
-        acc += f.gath[(int64_t)r * f.slice_len + gs_len + d * d];
-        err = fmax(err, f.gath[(int64_t)r * f.slice_len + gs_len + d * d + 1]);
-      }
-      if (err > 0.0) f.ctl->err = (int)err;
-      h = (acc > f.accept_target * P) ? min(h + f.h_step, f.h_max) : max(h - f.h_step, f.h_min);
-      f.ctl->h = h;
-    }
-    // RNE of each monitor a: gbar_j = a'S_j / N, gbar = a' theta-bar,
-    // vhat = N/(J-1) sum_j (gbar_j - gbar)^2, var = (P-1)/P a'V a
-    double minrne = INFINITY;
-    for (int m = 0; m < f.nmon; ++m) {
-      const double* a = f.mon + (int64_t)m * d;
-      for (int j = threadIdx.x; j < f.J; j += blockDim.x) {
-        const int r = j / f.Jl, jl = j % f.Jl;
-        const double* S = f.gath + (int64_t)r * f.slice_len + jl * d;
-        double s = 0.0;
-        for (int i = 0; i < d; ++i) s = fma(a[i], S[i], s);
-        sg[j] = s / (double)f.N;
-      }
-      __syncthreads();
-      double gbar_part = 0.0;
-      for (int j = threadIdx.x; j < f.J; j += blockDim.x) gbar_part += sg[j];
-      const double gbar = block_sum(gbar_part, red) / (double)f.J;
-      double dev = 0.0;
-      for (int j = threadIdx.x; j < f.J; j += blockDim.x) dev += (sg[j] - gbar) * (sg[j] - gbar);
-      dev = block_sum(dev, red);
-      double quad = 0.0;
-      for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) quad += a[idx / d] * sV[idx] * a[idx % d];
-      quad = block_sum(quad, red);
-      const double vhat = (double)f.N / (double)(f.J - 1) * dev;
-      const double var = quad * (P - 1.0) / P;
-      const double rne = vhat > 0.0 ? var / vhat : INFINITY;
-      if (f.rne_out && threadIdx.x == 0) f.rne_out[m] = rne;
-      minrne = fmin(minrne, rne);
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-      f.ctl->minrne = minrne;
-      f.ctl->stop = minrne >= f.K ? 1 : 0;
-    }
-  }
-  __syncthreads();
-  h = f.ctl->h;
-  const double hd = (double)h / 100.0;
-  for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) {
-    f.V[idx] = sV[idx];
-    sA[idx] = hd * sV[idx];
-  }
-  __syncthreads();
-  bool ok = block_cholesky(sA, d, &flag);
-  if (threadIdx.x == 0) f.ctl->chol_ridge = ok ? 0 : 1;
-  if (!ok) {
-    double tr = 0.0;
-    for (int i = 0; i < d; ++i) tr += sV[i * d + i];
-    const double ridge = 1e-8 * tr / (double)d;
-    for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x)
-      sA[idx] = hd * (sV[idx] + ((idx / d == idx % d) ? ridge : 0.0));
-    __syncthreads();
-    ok = block_cholesky(sA, d, &flag);
-    if (!ok) {
-      if (threadIdx.x == 0) f.ctl->err = ERR_NUMERIC;
-      return;
-    }
-  }
-  for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) f.Lprop[idx] = sA[idx];
-  for (int i = threadIdx.x; i < d; i += blockDim.x) f.shift[i] = sbar[i];
-}
 
 // Reported functional moments (K11) from the gathered
 // stats: mean, sd, NSE = [vhat/(JN)]^1/2 (R2), RNE.  One block.

@@ -55,6 +55,7 @@ struct LLArgs {
   int64_t P;
   int32_t t0, t1, chunk;
   int32_t k;           // covariates; theta block stride (K template >= k, zero padded)
+  const int* stop;     // speculative M-step launches: return if set
 };
 
 // max(s, 0) and min(|s|, 708) with integer ops on the ALU pipe (sm_100a has no
@@ -102,6 +103,7 @@ template <int K, int PPT>
 __global__ void __launch_bounds__(LL_THREADS, 2) k_loglik_bin(LLArgs a) {
   constexpr int LDX = ldx_of<K>();
   extern __shared__ __align__(16) double smem[];
+  if (a.stop && *a.stop) return;
   double* sT = smem;
   double* sX = smem + 64;
   const int c0 = a.t0 + blockIdx.y * a.chunk;
@@ -202,6 +204,7 @@ template <int K, int CM1, int PPT>
 __global__ void __launch_bounds__(LL_THREADS, 2) k_loglik_mnl(LLArgs a) {
   constexpr int LDX = ldx_of<K>();
   extern __shared__ __align__(16) double smem[];
+  if (a.stop && *a.stop) return;
   double* sT = smem;
   double* sX = smem + 64;
   const int c0 = a.t0 + blockIdx.y * a.chunk;

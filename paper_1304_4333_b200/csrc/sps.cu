@@ -13,9 +13,11 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -24,6 +26,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "loglik.cuh"
+#include "mstep.cuh"
 
 using namespace sps;
 
@@ -63,6 +66,12 @@ NcclApi g_nccl;
 }  // namespace
 
 // ================================================================== context
+using LLKernel = void (*)(LLArgs);
+struct LLChoice_t {
+  LLKernel fn = nullptr;
+  int KT = 0, PPT = 1;
+};
+
 struct sps_ctx {
   sps_config cfg{};
   int n = 0, k = 0, C = 0, d = 0, J = 0, N = 0, G = 1, rank = 0, Jl = 0, g0 = 0;
@@ -87,6 +96,24 @@ struct sps_ctx {
   int fn_cap = 0;
   double* ll_scratch = nullptr;  // sps_loglik chunk partials (grown on demand)
   size_t ll_scratch_cap = 0;
+  double* Sinv = nullptr;        // prior precision (d x d)
+  double* bpart = nullptr;       // accept+moments block partials
+  int tp = 0, QE = 1, W = 0, nblk = 0;
+  Ctl* hslot = nullptr;          // 2 mapped pinned Ctl slots (pipelined M steps), written by k_finalize2
+  Ctl* dslot = nullptr;          // device view of hslot
+  long long* fin_trace = nullptr;  // debug (SPS_FIN_TRACE): k_finalize2 phase clocks
+  double* Zbuf[2] = {nullptr, nullptr};  // standard normals, one M step ahead (side stream)
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_zready[2] = {nullptr, nullptr}, ev_zfree[2] = {nullptr, nullptr};
+  cudaEvent_t evs[2] = {nullptr, nullptr};
+  LLChoice_t llc{};
+  int ll_regs = 0;
+  struct Plan {
+    int64_t P = -1;
+    int range = -1, max_chunks = -1, S = 1, chunk = 0;
+    size_t smem = 0;
+  } plans[8];
+  int plan_next = 0;
   Ctl* ctl = nullptr;
   Ctl* hctl = nullptr;  // pinned mirror
   int slice_len = 0;
@@ -106,10 +133,20 @@ struct sps_ctx {
   double k1_pairs = 0.0, k1_ms = 0.0;
   bool profiling = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double cat_ms[16] = {0};
+  int64_t cat_n[16] = {0};
+  std::vector<cudaEvent_t> prof_pool;         // event pairs, resolved lazily (no per-launch sync)
+  std::vector<std::pair<int, int>> prof_open; // (event index pair base, category) awaiting resolution
+  int prof_next = 0;
+  int prof_cur = -1;
+  double host_launch_us = 0.0, host_wait_us = 0.0;
   std::string err;
 };
 
 namespace {
+
+enum Cat { CAT_K1 = 0, CAT_PROPOSE, CAT_ACCEPT, CAT_REDUCE, CAT_GATHER, CAT_FINALIZE, CAT_COPY, CAT_CPHASE,
+           CAT_RESAMPLE, CAT_OTHER, NCAT };
 
 sps_status fail(sps_ctx* c, sps_status st, const char* fmt, ...) {
   if (c) {
@@ -134,6 +171,16 @@ sps_status fail(sps_ctx* c, sps_status st, const char* fmt, ...) {
     (c)->launches += 1;        \
     CU(c, cudaGetLastError()); \
   } while (0)
+// Profiling (sps_set_profiling): bracket one enqueued operation with a pair of
+// pooled events on the context stream; pairs are resolved (synchronized) only
+// when the counters are read, so launches stay back to back.
+sps_status prof_begin(sps_ctx* c);
+sps_status prof_end(sps_ctx* c, int cat);
+#define PROF_BEGIN(c) \
+  if ((c)->profiling) TRY(prof_begin(c))
+#define PROF_END(c, cat) \
+  if ((c)->profiling) TRY(prof_end(c, cat))
+
 #define TRY(x)                         \
   do {                                 \
     sps_status s_ = (x);               \
@@ -154,12 +201,47 @@ int num_sms() {
 }
 
 sps_status gather(sps_ctx* c, const double* send, double* recv, size_t count) {
-  if (c->G == 1) {
+  if (c->G == 1) {  // single rank: the gathered buffer aliases the local slice
     if (send != recv) CU(c, cudaMemcpyAsync(recv, send, count * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
     return SPS_OK;
   }
   ncclResult_t r = g_nccl.AllGather(send, recv, count, ncclFloat64, c->comm, c->stream);
   if (r != ncclSuccess) return fail(c, SPS_E_NCCL, "ncclAllGather: %s", g_nccl.GetErrorString(r));
+  return SPS_OK;
+}
+
+sps_status prof_begin(sps_ctx* c) {
+  if ((size_t)c->prof_next + 2 > c->prof_pool.size()) {
+    for (int q = 0; q < 256; ++q) {
+      cudaEvent_t e;
+      CU(c, cudaEventCreate(&e));
+      c->prof_pool.push_back(e);
+    }
+  }
+  c->prof_cur = c->prof_next;
+  c->prof_next += 2;
+  CU(c, cudaEventRecord(c->prof_pool[c->prof_cur], c->stream));
+  return SPS_OK;
+}
+
+sps_status prof_end(sps_ctx* c, int cat) {
+  CU(c, cudaEventRecord(c->prof_pool[c->prof_cur + 1], c->stream));
+  c->prof_open.push_back({c->prof_cur, cat});
+  return SPS_OK;
+}
+
+sps_status prof_resolve(sps_ctx* c) {
+  if (c->prof_open.empty()) return SPS_OK;
+  CU(c, cudaStreamSynchronize(c->stream));
+  for (auto& pr : c->prof_open) {
+    float ms = 0.f;
+    CU(c, cudaEventElapsedTime(&ms, c->prof_pool[pr.first], c->prof_pool[pr.first + 1]));
+    c->cat_ms[pr.second] += ms;
+    c->cat_n[pr.second] += 1;
+    if (pr.second == 0) c->k1_ms += ms;
+  }
+  c->prof_open.clear();
+  c->prof_next = 0;
   return SPS_OK;
 }
 
@@ -176,8 +258,6 @@ sps_status read_ctl(sps_ctx* c) {
 }
 
 // ------------------------------------------------------------------ K1 dispatch
-using LLKernel = void (*)(LLArgs);
-
 template <int K, int CM1, int PPT>
 LLKernel ll_ptr() {
   if constexpr (CM1 == 1)
@@ -189,10 +269,7 @@ LLKernel ll_ptr() {
 // Instantiated shapes: binary k = 1..32 (PPT 2) and {40,48,56,64} (PPT 1);
 // C-1 = 2: k = 1..16 (PPT 2 up to 12); C-1 = 3: k = 1..16; C-1 = 4..7: k in {4, 8}.
 // Other k round up to the next instantiated KT (zero padding in X and theta loads).
-struct LLChoice {
-  LLKernel fn;
-  int KT, PPT;
-};
+using LLChoice = LLChoice_t;
 
 template <int CM1, int PPT, int... Ks>
 bool pick_exact(int k, LLChoice* out, std::integer_sequence<int, Ks...>) {
@@ -234,117 +311,168 @@ bool choose_ll(int k, int C, LLChoice* o) {
 }
 
 // Launch K1 over [t0, t1) for P particles: partial sums per observation chunk
-// into `part` ([nchunks][P]); returns nchunks.  Chunk count is chosen so the
-// grid fills whole waves of (SMs x resident blocks) and the X tile fits smem.
+// into `part` ([nchunks][P]); returns nchunks.  The chunk count S is chosen so
+// the grid (tiles x S) fills whole waves of SMs x resident blocks (occupancy
+// from the kernel's registers and the chunk's shared memory) and the X tile
+// fits in shared memory; plans are cached per (P, range).
 sps_status launch_loglik(sps_ctx* c, const double* theta, int64_t ldt, int64_t P, int t0, int t1, double* part,
-                         int max_chunks, int* nchunks_out) {
-  LLChoice ch;
-  if (!choose_ll(c->k, c->C, &ch)) return fail(c, SPS_E_CONFIG, "unsupported (k, C) = (%d, %d)", c->k, c->C);
+                         int max_chunks, int* nchunks_out, const int* stop = nullptr) {
+  const LLChoice& ch = c->llc;
   const int range = t1 - t0;
-  const int64_t tiles = (P + LL_THREADS * ch.PPT - 1) / (LL_THREADS * ch.PPT);
-  const int ldx = c->ldx;
-  const size_t row_bytes = (size_t)ldx * 8 + (c->C > 2 ? 4 : 0);
-  const int smem_budget = 96 * 1024;
-  const int chunk_cap = std::max(1, (int)((smem_budget - 64 * 8 - 64) / row_bytes));
-  int S_min = std::max(1, (range + chunk_cap - 1) / chunk_cap);
-  static thread_local int occ_cache_key = -1, occ_cache_val = 0;
-  const int key = (int)(reinterpret_cast<uintptr_t>(ch.fn) & 0x7fffffff);
-  int occ = 0;
-  const size_t smem_probe = 64 * 8 + (size_t)std::min(range, chunk_cap) * row_bytes + 16;
-  CU(c, cudaFuncSetAttribute(ch.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_budget + 1024));
-  if (occ_cache_key == key) {
-    occ = occ_cache_val;
-  } else {
-    CU(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ch.fn, LL_THREADS, smem_budget));
-    occ = std::max(occ, 1);
-    occ_cache_key = key;
-    occ_cache_val = occ;
-  }
-  (void)smem_probe;
-  const double slots = (double)num_sms() * occ;
-  int best = S_min;
-  double best_eff = -1.0;
-  const int S_hi = std::min(max_chunks, std::max(S_min, range / 16));
-  for (int S = S_min; S <= std::max(S_min, S_hi); ++S) {
-    const double blocks = (double)tiles * S;
-    const double eff = blocks / (std::ceil(blocks / slots) * slots);
-    if (eff > best_eff + 0.02) {
-      best_eff = eff;
-      best = S;
-    }
-    if (blocks >= 4 * slots) break;
-  }
-  int S = std::min(best, max_chunks);
-  if (range <= 0) S = 1;
-  const int chunk = range > 0 ? (range + S - 1) / S : 0;
-  S = range > 0 ? (range + chunk - 1) / chunk : 1;
-  if (S > max_chunks) return fail(c, SPS_E_CONFIG, "observation range too long for the chunk buffer");
-  const size_t smem = 64 * 8 + (size_t)std::max(chunk, 1) * ldx * 8 + (c->C > 2 ? (size_t)std::max(chunk, 1) * 4 : 0);
-  LLArgs a{c->Xs, c->y, theta, part, ldt, P, t0, t1, chunk};
-  a.k = c->k;
   if (range <= 0) {
     CU(c, cudaMemsetAsync(part, 0, (size_t)P * sizeof(double), c->stream));
-  } else {
-    dim3 grid((unsigned)tiles, (unsigned)S);
-    if (c->profiling) CU(c, cudaEventRecord(c->ev0, c->stream));
-    ch.fn<<<grid, LL_THREADS, smem, c->stream>>>(a);
-    CHECK_LAUNCH(c);
-    c->k1_launches += 1;
-    c->k1_pairs += (double)P * range;
-    if (c->profiling) {
-      CU(c, cudaEventRecord(c->ev1, c->stream));
-      CU(c, cudaEventSynchronize(c->ev1));
-      float ms = 0.f;
-      CU(c, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
-      c->k1_ms += ms;
-    }
+    *nchunks_out = 1;
+    return SPS_OK;
   }
-  *nchunks_out = S;
+  const int64_t tiles = (P + LL_THREADS * ch.PPT - 1) / (LL_THREADS * ch.PPT);
+  const size_t row_bytes = (size_t)c->ldx * 8 + (c->C > 2 ? 4 : 0);
+  sps_ctx::Plan* pl = nullptr;
+  for (auto& q : c->plans)
+    if (q.P == P && q.range == range && q.max_chunks == max_chunks) pl = &q;
+  if (!pl) {
+    pl = &c->plans[c->plan_next];
+    c->plan_next = (c->plan_next + 1) % 8;
+    const int smem_budget = 100 * 1024;
+    const int chunk_cap = std::max(1, (int)((smem_budget - 64 * 8 - 64) / row_bytes));
+    const int S_min = std::max(1, (range + chunk_cap - 1) / chunk_cap);
+    const int S_hi = std::min(max_chunks, std::max(S_min, std::min(S_min + 24, range / 8)));
+    const int warp_regs = ((c->ll_regs * 32 + 255) / 256) * 256;
+    const int by_regs = 65536 / ((LL_THREADS / 32) * warp_regs);
+    int best = S_min;
+    double best_eff = -1.0;
+    for (int S = S_min; S <= S_hi; ++S) {
+      const int chunk = (range + S - 1) / S;
+      const int Se = (range + chunk - 1) / chunk;
+      const size_t smem = 64 * 8 + (size_t)chunk * row_bytes + 16;
+      const int by_smem = (int)(233472 / (smem + 1024));
+      const int occ = std::max(1, std::min(std::min(by_regs, by_smem), 16));
+      const double slots = (double)num_sms() * occ;
+      const double blocks = (double)tiles * Se;
+      const double eff = blocks / (std::ceil(blocks / slots) * slots);
+      if (eff > best_eff + 0.01) {
+        best_eff = eff;
+        best = S;
+      }
+    }
+    int chunk = (range + best - 1) / best;
+    pl->P = P;
+    pl->range = range;
+    pl->max_chunks = max_chunks;
+    pl->chunk = chunk;
+    pl->S = (range + chunk - 1) / chunk;
+    pl->smem = 64 * 8 + (size_t)chunk * c->ldx * 8 + (c->C > 2 ? (size_t)chunk * 4 : 0);
+    if (pl->S > max_chunks) return fail(c, SPS_E_CONFIG, "observation range too long for the chunk buffer");
+  }
+  LLArgs a{c->Xs, c->y, theta, part, ldt, P, t0, t1, pl->chunk};
+  a.k = c->k;
+  a.stop = stop;
+  dim3 grid((unsigned)tiles, (unsigned)pl->S);
+  PROF_BEGIN(c);
+  ch.fn<<<grid, LL_THREADS, pl->smem, c->stream>>>(a);
+  CHECK_LAUNCH(c);
+  c->k1_launches += 1;
+  c->k1_pairs += (double)P * range;
+  PROF_END(c, CAT_K1);
+  *nchunks_out = pl->S;
   return SPS_OK;
 }
 
-int dmax_of(int d) { return d <= 16 ? 16 : d <= 32 ? 32 : d <= 64 ? 64 : 128; }
-
-sps_status launch_draw(sps_ctx* c, bool init, const double* base, const double* Lz, uint32_t step, double* out,
-                       double* lp_out) {
-  const int d = c->d;
-  const size_t smem = (size_t)(2 * d * d + d) * sizeof(double);
-  const unsigned grid = (unsigned)((c->Pl + 127) / 128);
-  auto go = [&](auto kern) -> sps_status {
-    CU(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
-    kern<<<grid, 128, smem, c->stream>>>(base, Lz, c->Lprior, c->mu, d, c->Pl, c->p0, c->cfg.seed, step,
-                                         (uint32_t)c->cfg.pass, out, lp_out, c->ctl, nullptr);
-    CHECK_LAUNCH(c);
-    return SPS_OK;
-  };
-  switch (c->dmax) {
-    case 16: return init ? go(k_draw<16, true>) : go(k_draw<16, false>);
-    case 32: return init ? go(k_draw<32, true>) : go(k_draw<32, false>);
-    case 64: return init ? go(k_draw<64, true>) : go(k_draw<64, false>);
-    default: return init ? go(k_draw<128, true>) : go(k_draw<128, false>);
-  }
+// Standard normals of (step, tag) for every local particle into Zbuf[slot], on
+// the side stream `aux` (waits until Zbuf[slot] is free; signals ev_zready).
+sps_status launch_normals(sps_ctx* c, uint32_t tag, uint32_t step, int slot) {
+  const int np = (c->d + 1) / 2;
+  CU(c, cudaStreamWaitEvent(c->aux, c->ev_zfree[slot], 0));
+  const int64_t tasks = c->Pl * np;
+  k_normals<<<(unsigned)((tasks + 255) / 256), 256, 0, c->aux>>>(c->Pl, c->p0, np, c->cfg.seed, step, tag,
+                                                                 (uint32_t)c->cfg.pass, c->Zbuf[slot]);
+  CHECK_LAUNCH(c);
+  CU(c, cudaEventRecord(c->ev_zready[slot], c->aux));
+  return SPS_OK;
 }
 
-// Moments of the current particles -> gathered stats (`gath`).
-sps_status moments(sps_ctx* c) {
+// K8 / K10: theta = base + Lz z with z = Zbuf[slot], lp = prior kernel.
+sps_status launch_draw(sps_ctx* c, int slot, const double* base, const double* Lz, double* out, double* lp_out,
+                       const int* stop) {
+  const int d = c->d, KP = round_up(d, 4), NP = round_up(d, 8);
+  const size_t base_sm = (size_t)(2 * PR_TILE * KP + PR_TILE * (NP / 8) + KP + PR_TILE * d);
+  const bool stage = (base_sm + 2 * (size_t)NP * KP) * sizeof(double) <= 160 * 1024;
+  const size_t smem = (base_sm + (stage ? 2 * (size_t)NP * KP : 0)) * sizeof(double);
+  DrawArgs a{};
+  a.base = base;
+  a.Lz = Lz;
+  a.Sinv = c->Sinv;
+  a.mu = c->mu;
+  a.Z = c->Zbuf[slot];
+  a.out = out;
+  a.lp_out = lp_out;
+  a.ctl = c->ctl;
+  a.stop = stop;
+  a.P = c->Pl;
+  a.p0 = c->p0;
+  a.d = d;
+  CU(c, cudaStreamWaitEvent(c->stream, c->ev_zready[slot], 0));
+  const unsigned grid = (unsigned)((c->Pl + PR_TILE - 1) / PR_TILE);
+  PROF_BEGIN(c);
+  if (stage)
+    k_propose<true><<<grid, 256, smem, c->stream>>>(a);
+  else
+    k_propose<false><<<grid, 256, smem, c->stream>>>(a);
+  CHECK_LAUNCH(c);
+  PROF_END(c, CAT_PROPOSE);
+  CU(c, cudaEventRecord(c->ev_zfree[slot], c->stream));
+  return SPS_OK;
+}
+
+// K9 + K6 (decide = true) or K6 only, then the deterministic reduction into this
+// rank's stats slice and the gather across ranks -> `gath`.
+sps_status accept_moments(sps_ctx* c, bool decide, int nchunks, double temper, uint32_t step, const int* stop) {
+  AccArgs a{};
+  a.theta = c->theta;
+  a.L = c->L;
+  a.lp = c->lp;
+  a.theta_s = c->theta_s;
+  a.part = c->part;
+  a.lp_s = c->lp_s;
+  a.shift = c->shift;
+  a.bpart = c->bpart;
+  a.ctl = c->ctl;
+  a.stop = stop;
+  a.P = c->Pl;
+  a.p0 = c->p0;
+  a.temper = temper;
+  a.seed = c->cfg.seed;
+  a.nchunks = nchunks;
+  a.d = c->d;
+  a.tp = c->tp;
+  a.decide = decide ? 1 : 0;
+  a.step = step;
+  a.pass = (uint32_t)c->cfg.pass;
+  const size_t smem =
+      ((size_t)round_up(c->tp, 4) * (round_up(c->d, 8) + 4) + 8 * (size_t)c->d) * sizeof(double) + (size_t)c->tp + 16;
+  PROF_BEGIN(c);
+  k_accept_mom<<<c->nblk, 256, smem, c->stream>>>(a);
+  CHECK_LAUNCH(c);
+  PROF_END(c, CAT_ACCEPT);
   const int d = c->d;
-  dim3 grid((unsigned)c->nblk_mom, (unsigned)c->ngy_mom);
-  const size_t smem = (size_t)MOM_TILE * d * sizeof(double);
-  CU(c, cudaFuncSetAttribute(k_moments_partial, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
-  k_moments_partial<<<grid, 256, smem, c->stream>>>(c->theta, d, c->pp, c->shift, c->gpart, c->mpart, nullptr);
+  const int nm = (d * d + 31) / 32, ng = (c->Jl * d + 255) / 256;
+  PROF_BEGIN(c);
+  k_mom_reduce<<<nm + ng + 1, 256, 0, c->stream>>>(c->bpart, c->nblk, c->N / c->tp, c->Jl, d, c->ctl, c->slice, stop);
   CHECK_LAUNCH(c);
-  k_moments_reduce<<<64, 256, 0, c->stream>>>(c->gpart, c->mpart, c->nblk_mom, c->bpg, c->Jl, d, c->ctl, c->slice,
-                                              nullptr);
-  CHECK_LAUNCH(c);
-  return gather(c, c->slice, c->gath, (size_t)c->slice_len);
+  PROF_END(c, CAT_REDUCE);
+  PROF_BEGIN(c);
+  TRY(gather(c, c->slice, c->gath, (size_t)c->slice_len));
+  PROF_END(c, CAT_GATHER);
+  return SPS_OK;
 }
 
 bool final_cycle(const sps_ctx* c) {
   return c->cfg.tempering == SPS_POWER_TEMPERING ? (c->phi == 1.0) : (c->t == c->n);
 }
 
-sps_status finalize(sps_ctx* c, int mode) {
+sps_status finalize(sps_ctx* c, int mode, bool allow_stop, const int* stop, int slot = -1) {
   FinArgs f{};
+  f.host_out = slot >= 0 ? c->dslot + slot : nullptr;
+  f.trace = c->fin_trace;
   f.gath = c->gath;
   f.G = c->G;
   f.slice_len = c->slice_len;
@@ -358,18 +486,34 @@ sps_status finalize(sps_ctx* c, int mode) {
   f.mon = c->mon;
   f.nmon = c->nmon;
   f.mode = mode;
-  f.K = final_cycle(c) ? c->cfg.K_final : c->cfg.K_inter;
+  f.K = allow_stop ? (final_cycle(c) ? c->cfg.K_final : c->cfg.K_inter) : -1.0;
   f.h_step = c->cfg.h_step;
   f.h_min = c->cfg.h_min;
   f.h_max = c->cfg.h_max;
   f.accept_target = c->cfg.accept_target;
   f.ctl = c->ctl;
-  f.stop_in = nullptr;
+  f.stop_in = stop;
   f.rne_out = c->rne;
-  const size_t smem = (size_t)(2 * c->d * c->d + c->d + c->J) * sizeof(double);
-  CU(c, cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
-  k_finalize<<<1, 256, smem, c->stream>>>(f);
+  const size_t smem = (size_t)(3 * c->d * c->d + 2 * c->d + c->nmon * c->J + c->nmon + c->nmon * c->d +
+                                (size_t)c->J * c->d) * sizeof(double);
+  if (smem > 200 * 1024) return fail(c, SPS_E_CONFIG, "J x d too large for the finalize stage (%zu bytes)", smem);
+  PROF_BEGIN(c);
+  k_finalize2<<<1, 256, smem, c->stream>>>(f);
   CHECK_LAUNCH(c);
+  if (c->d <= 32) {  // chol((h/100) V) by one warp, after h is known
+    switch ((c->d + 3) / 4) {
+      case 1: k_chol_warp<4><<<1, 32, 0, c->stream>>>(c->V, c->d, c->ctl, c->Lprop, stop); break;
+      case 2: k_chol_warp<8><<<1, 32, 0, c->stream>>>(c->V, c->d, c->ctl, c->Lprop, stop); break;
+      case 3: k_chol_warp<12><<<1, 32, 0, c->stream>>>(c->V, c->d, c->ctl, c->Lprop, stop); break;
+      case 4: k_chol_warp<16><<<1, 32, 0, c->stream>>>(c->V, c->d, c->ctl, c->Lprop, stop); break;
+      case 5: k_chol_warp<20><<<1, 32, 0, c->stream>>>(c->V, c->d, c->ctl, c->Lprop, stop); break;
+      case 6: k_chol_warp<24><<<1, 32, 0, c->stream>>>(c->V, c->d, c->ctl, c->Lprop, stop); break;
+      case 7: k_chol_warp<28><<<1, 32, 0, c->stream>>>(c->V, c->d, c->ctl, c->Lprop, stop); break;
+      default: k_chol_warp<32><<<1, 32, 0, c->stream>>>(c->V, c->d, c->ctl, c->Lprop, stop); break;
+    }
+    CHECK_LAUNCH(c);
+  }
+  PROF_END(c, CAT_FINALIZE);
   return SPS_OK;
 }
 
@@ -390,14 +534,29 @@ sps_status validate(const sps_config* cfg) {
 
 void free_ctx(sps_ctx* c) {
   if (!c) return;
+  if (c->G == 1) {  // aliases of the local slices
+    c->gath = c->essgath = c->grp_ms_gath = c->Lj_gath = c->pw_gath = c->mx_gath = nullptr;
+  }
+  for (double* z : c->Zbuf)
+    if (z) cudaFree(z);
+  if (c->aux) cudaStreamSynchronize(c->aux);
+  for (int q = 0; q < 2; ++q) {
+    if (c->ev_zready[q]) cudaEventDestroy(c->ev_zready[q]);
+    if (c->ev_zfree[q]) cudaEventDestroy(c->ev_zfree[q]);
+  }
+  if (c->aux) cudaStreamDestroy(c->aux);
   void* ptrs[] = {c->X, c->Xs, c->mu, c->Lprior, c->xbar, c->mon, c->y, c->theta, c->theta2, c->L, c->L2, c->lp,
                   c->lp2, c->lw, c->lw_cur, c->theta_s, c->lp_s, c->part, c->gpart, c->mpart, c->slice, c->gath,
                   c->shift, c->Lprop, c->V, c->rne, c->lwbuf, c->essparts, c->essslice, c->essgath, c->grp_ms,
                   c->grp_ms_gath, c->Lj, c->Lj_gath, c->scal, c->pw_parts, c->pw_slice, c->pw_gath, c->mx_parts,
-                  c->mx_slice, c->mx_gath, c->fn_A, c->fn_out, c->ll_scratch, c->ctl};
+                  c->mx_slice, c->mx_gath, c->fn_A, c->fn_out, c->ll_scratch, c->Sinv, c->bpart, c->ctl};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->hctl) cudaFreeHost(c->hctl);
+  if (c->hslot) cudaFreeHost(c->hslot);
+  for (cudaEvent_t e : c->evs)
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->prof_pool) cudaEventDestroy(e);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->comm) g_nccl.CommDestroy(c->comm);
@@ -485,21 +644,29 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
   if (!choose_ll(c->k, c->C, &ch)) return fail(c, SPS_E_CONFIG, "unsupported (k, C) = (%d, %d)", c->k, c->C);
   c->KT = ch.KT;
   c->PPT = ch.PPT;
+  c->llc = ch;
+  {
+    cudaFuncAttributes fa{};
+    CU(c, cudaFuncGetAttributes(&fa, ch.fn));
+    c->ll_regs = fa.numRegs;
+    CU(c, cudaFuncSetAttribute(ch.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 101 * 1024 + 1024));
+  }
   c->ldx = ch.KT + (ch.KT & 1);
-  c->dmax = dmax_of(d);
   c->nmon = cfg.n_monitors > 0 ? cfg.n_monitors : c->C;
   if (cfg.n_monitors > 0 && !cfg_in->monitors) return fail(c, SPS_E_CONFIG, "n_monitors > 0 but monitors == NULL");
-  // moments layout
-  c->pp = 1;
-  for (int q = std::min(c->N, 256); q >= 1; --q)
-    if (c->N % q == 0) {
-      c->pp = q;
-      break;
-    }
-  c->bpg = c->N / c->pp;
-  c->nblk_mom = (int)(c->Pl / c->pp);
-  const int ntri = d * (d + 1) / 2;
-  c->ngy_mom = (ntri + MOM_ENT - 1) / MOM_ENT;
+  // accept + moments layout: blocks of tp particles inside one group (tp divides N,
+  // tp <= 256, staged tile tp x round_up(d, 8) doubles <= 96 KB)
+  {
+    const int cap = std::max(1, std::min(256, 96 * 1024 / (8 * ((d + 7) / 8 * 8 + 4))));
+    c->tp = 1;
+    for (int q = std::min(c->N, cap); q >= 1; --q)
+      if (c->N % q == 0) {
+        c->tp = q;
+        break;
+      }
+  }
+  c->nblk = (int)(c->Pl / c->tp);
+  c->W = d + d * d + 1;
   c->slice_len = c->Jl * d + d * d + 2;
   c->max_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(64, ((int64_t)1 << 26) / std::max<int64_t>(c->Pl, 1)));
   c->Bmax = (int)std::max<int64_t>(8, std::min<int64_t>(256, ((int64_t)1 << 23) / std::max<int64_t>(c->Pl, 1)));
@@ -530,10 +697,27 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
   for (double** p : {&c->theta, &c->theta2, &c->theta_s}) TRY(dalloc(c, p, (size_t)Pl * d));
   for (double** p : {&c->L, &c->L2, &c->lp, &c->lp2, &c->lw, &c->lw_cur, &c->lp_s}) TRY(dalloc(c, p, (size_t)Pl));
   TRY(dalloc(c, &c->part, (size_t)c->max_chunks * Pl));
-  TRY(dalloc(c, &c->gpart, (size_t)c->nblk_mom * d));
-  TRY(dalloc(c, &c->mpart, (size_t)c->nblk_mom * ntri));
+  TRY(dalloc(c, &c->bpart, (size_t)c->nblk * c->W));
+  TRY(dalloc(c, &c->Sinv, (size_t)d * d));
+  CU(c, cudaHostAlloc((void**)&c->hslot, 2 * sizeof(Ctl), cudaHostAllocMapped));
+  CU(c, cudaHostGetDevicePointer((void**)&c->dslot, c->hslot, 0));
+  if (getenv("SPS_FIN_TRACE")) CU(c, cudaMallocManaged((void**)&c->fin_trace, 8 * sizeof(long long)));
+  CU(c, cudaEventCreateWithFlags(&c->evs[0], cudaEventDisableTiming));
+  CU(c, cudaEventCreateWithFlags(&c->evs[1], cudaEventDisableTiming));
   TRY(dalloc(c, &c->slice, (size_t)c->slice_len));
-  TRY(dalloc(c, &c->gath, (size_t)c->slice_len * c->G));
+  if (c->G > 1) TRY(dalloc(c, &c->gath, (size_t)c->slice_len * c->G));
+  else c->gath = c->slice;
+  {
+    const int np = (d + 1) / 2;
+    TRY(dalloc(c, &c->Zbuf[0], (size_t)Pl * 2 * np));
+    TRY(dalloc(c, &c->Zbuf[1], (size_t)Pl * 2 * np));
+    CU(c, cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+    for (int q = 0; q < 2; ++q) {
+      CU(c, cudaEventCreateWithFlags(&c->ev_zready[q], cudaEventDisableTiming));
+      CU(c, cudaEventCreateWithFlags(&c->ev_zfree[q], cudaEventDisableTiming));
+      CU(c, cudaEventRecord(c->ev_zfree[q], c->stream));
+    }
+  }
   TRY(dalloc(c, &c->shift, d));
   TRY(dalloc(c, &c->Lprop, (size_t)d * d));
   TRY(dalloc(c, &c->V, (size_t)d * d));
@@ -542,18 +726,26 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
   const int ntiles = (int)((Pl + ESS_TILE - 1) / ESS_TILE);
   TRY(dalloc(c, &c->essparts, (size_t)c->Bmax * ntiles * 3));
   TRY(dalloc(c, &c->essslice, (size_t)c->Bmax * 3));
-  TRY(dalloc(c, &c->essgath, (size_t)c->Bmax * 3 * c->G));
   TRY(dalloc(c, &c->grp_ms, (size_t)c->Jl * 2));
-  TRY(dalloc(c, &c->grp_ms_gath, (size_t)c->J * 2));
   TRY(dalloc(c, &c->Lj, (size_t)c->Jl));
-  TRY(dalloc(c, &c->Lj_gath, (size_t)c->J));
+  if (c->G > 1) {
+    TRY(dalloc(c, &c->essgath, (size_t)c->Bmax * 3 * c->G));
+    TRY(dalloc(c, &c->grp_ms_gath, (size_t)c->J * 2));
+    TRY(dalloc(c, &c->Lj_gath, (size_t)c->J));
+  } else {
+    c->essgath = c->essslice;
+    c->grp_ms_gath = c->grp_ms;
+    c->Lj_gath = c->Lj;
+  }
   TRY(dalloc(c, &c->scal, 8));
   TRY(dalloc(c, &c->pw_parts, (size_t)PW_BLOCKS * 64 * 2));
   TRY(dalloc(c, &c->pw_slice, 64 * 2));
-  TRY(dalloc(c, &c->pw_gath, (size_t)64 * 2 * c->G));
+  if (c->G > 1) TRY(dalloc(c, &c->pw_gath, (size_t)64 * 2 * c->G));
+  else c->pw_gath = c->pw_slice;
   TRY(dalloc(c, &c->mx_parts, MX_BLOCKS));
   TRY(dalloc(c, &c->mx_slice, 1));
-  TRY(dalloc(c, &c->mx_gath, (size_t)c->G));
+  if (c->G > 1) TRY(dalloc(c, &c->mx_gath, (size_t)c->G));
+  else c->mx_gath = c->mx_slice;
   TRY(dalloc(c, &c->ctl, 1));
   CU(c, cudaMallocHost((void**)&c->hctl, sizeof(Ctl)));
   std::memset(c->hctl, 0, sizeof(Ctl));
@@ -584,6 +776,18 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
     CU(c, cudaFuncSetAttribute(k_chol_prior, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
     k_chol_prior<<<1, 256, smem, c->stream>>>(c->V, d, c->Lprior, c->ctl);
     CHECK_LAUNCH(c);
+    CU(c, cudaFuncSetAttribute(k_prior_precision, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
+    k_prior_precision<<<1, 128, smem, c->stream>>>(c->Lprior, d, c->Sinv);
+    CHECK_LAUNCH(c);
+    // one-time kernel attributes (dynamic shared memory above 48 KB)
+    const int big = 200 * 1024;
+    CU(c, cudaFuncSetAttribute(k_propose<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_propose<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_finalize2, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_accept_mom, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_functional_stats, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_resample, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_cphase_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
   }
   {
     sps_status st = read_ctl(c);
@@ -617,6 +821,14 @@ sps_status sps_reset(sps_ctx* c, uint64_t seed, int32_t pass) {
   c->tr_rne.clear();
   c->launches = c->k1_launches = c->syncs = 0;
   c->k1_pairs = c->k1_ms = 0.0;
+  c->host_launch_us = c->host_wait_us = 0.0;
+  for (int q = 0; q < 16; ++q) {
+    c->cat_ms[q] = 0.0;
+    c->cat_n[q] = 0;
+  }
+  if (c->stream) CU(c, cudaStreamSynchronize(c->stream));
+  c->prof_open.clear();
+  c->prof_next = 0;
   const int64_t Pl = c->Pl;
   std::memset(c->hctl, 0, sizeof(Ctl));
   c->hctl->h = c->cfg.h_init;
@@ -624,7 +836,8 @@ sps_status sps_reset(sps_ctx* c, uint64_t seed, int32_t pass) {
   CU(c, cudaMemsetAsync(c->Lj, 0, sizeof(double) * c->Jl, c->stream));
   CU(c, cudaMemcpyAsync(c->shift, c->mu, sizeof(double) * c->d, cudaMemcpyDeviceToDevice, c->stream));
   // Algorithm 1 step 1: theta_jn ~iid p(theta)
-  TRY(launch_draw(c, true, nullptr, c->Lprior, 0u, c->theta, c->lp));
+  TRY(launch_normals(c, TAG_INIT, 0u, 0));
+  TRY(launch_draw(c, 0, nullptr, c->Lprior, c->theta, c->lp, nullptr));
   if (c->cfg.tempering == SPS_POWER_TEMPERING) {
     int nch = 1;
     TRY(launch_loglik(c, c->theta, c->d, Pl, 0, c->n, c->part, c->max_chunks, &nch));
@@ -644,13 +857,28 @@ sps_status sps_set_profiling(sps_ctx* c, int32_t on) {
   return SPS_OK;
 }
 
-sps_status sps_get_counters(const sps_ctx* c, sps_counters* out) {
-  if (!c || !out) return SPS_E_CONFIG;
+sps_status sps_get_counters(const sps_ctx* cc, sps_counters* out) {
+  if (!cc || !out) return SPS_E_CONFIG;
+  sps_ctx* c = const_cast<sps_ctx*>(cc);
+  TRY(prof_resolve(c));
+  if (c->fin_trace) {
+    CU(c, cudaStreamSynchronize(c->stream));
+    fprintf(stderr, "fin_trace cycles:");
+    for (int q = 1; q < 7; ++q) fprintf(stderr, " %lld", c->fin_trace[q] - c->fin_trace[q - 1]);
+    fprintf(stderr, "\n");
+  }
   out->launches = c->launches;
   out->k1_launches = c->k1_launches;
   out->k1_pairs = c->k1_pairs;
   out->k1_ms = c->k1_ms;
   out->syncs = c->syncs;
+  out->cat_ms[14] = c->host_launch_us / 1e3;
+  out->cat_ms[15] = c->host_wait_us / 1e3;
+  out->cat_n[14] = out->cat_n[15] = 1;
+  for (int q = 0; q < 14; ++q) {
+    out->cat_ms[q] = c->cat_ms[q];
+    out->cat_n[q] = c->cat_n[q];
+  }
   return SPS_OK;
 }
 
@@ -689,6 +917,7 @@ sps_status sps_loglik(sps_ctx* c, const double* theta_dev, int64_t P, int32_t ld
 sps_status sps_sync(sps_ctx* c) {
   if (!c) return SPS_E_CONFIG;
   CU(c, cudaSetDevice(c->cfg.device));
+  CU(c, cudaStreamSynchronize(c->aux));
   CU(c, cudaStreamSynchronize(c->stream));
   c->syncs += 1;
   return SPS_OK;
@@ -704,6 +933,7 @@ sps_status sps_cphase(sps_ctx* c, int32_t t_target, double phi_target, int32_t* 
   const int64_t Pl = c->Pl;
   const double P = (double)c->P;
   const unsigned pgrid = (unsigned)((Pl + 255) / 256);
+  PROF_BEGIN(c);
   if (c->cfg.tempering == SPS_DATA_TEMPERING) {
     // ---- absorb observations one at a time ----
     if (t_target >= 0 && (t_target <= c->t || t_target > c->n))
@@ -788,8 +1018,10 @@ sps_status sps_cphase(sps_ctx* c, int32_t t_target, double phi_target, int32_t* 
     CHECK_LAUNCH(c);
     c->phi = (dphi == rem) ? 1.0 : c->phi + dphi;
   }
+  PROF_END(c, CAT_CPHASE);
   // ---- S phase + log-ML increments (R10) ----
   c->ell += 1;
+  PROF_BEGIN(c);
   {
     const size_t smem = (size_t)c->N * (8 + 4);
     CU(c, cudaFuncSetAttribute(k_resample, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
@@ -804,6 +1036,7 @@ sps_status sps_cphase(sps_ctx* c, int32_t t_target, double phi_target, int32_t* 
     k_logml_pooled<<<1, 32, 0, c->stream>>>(c->grp_ms_gath, c->J, P, c->ctl);
     CHECK_LAUNCH(c);
   }
+  PROF_END(c, CAT_RESAMPLE);
   TRY(read_ctl(c));
   const double inc = c->hctl->logml_inc;
   c->logml += inc;
@@ -818,51 +1051,80 @@ sps_status sps_cphase(sps_ctx* c, int32_t t_target, double phi_target, int32_t* 
   return SPS_OK;
 }
 
+// One M step (Algorithm 2 step 2(c)), fully enqueued:
+// K8 propose -> K1 loglik of theta* on [0, t_l) -> K9+K6 accept & moments ->
+// stats reduce -> gather -> K7 finalize (h, RNE, stop, chol(h V)) -> D2H of
+// the control block into pinned slot `slot`, event evs[slot].  Every kernel
+// returns at once when the device stop flag is already set, so a step
+// launched speculatively after the stopping step is a no-op.
+static sps_status launch_mstep(sps_ctx* c, uint32_t step, int slot, bool allow_stop) {
+  const bool power = c->cfg.tempering == SPS_POWER_TEMPERING;
+  const int t1 = power ? c->n : c->t;
+  const double temper = power ? c->phi : 1.0;
+  const int* stop = &c->ctl->stop;
+  TRY(launch_draw(c, (int)(step & 1u), c->theta, c->Lprop, c->theta_s, c->lp_s, stop));
+  TRY(launch_normals(c, TAG_PROPOSAL, step + 1u, (int)((step + 1u) & 1u)));  // next step's normals, overlapped
+  int nch = 1;
+  TRY(launch_loglik(c, c->theta_s, c->d, c->Pl, 0, t1, c->part, c->max_chunks, &nch, stop));
+  TRY(accept_moments(c, true, nch, temper, step, stop));
+  TRY(finalize(c, 1, allow_stop, stop, slot));
+  CU(c, cudaEventRecord(c->evs[slot], c->stream));
+  return SPS_OK;
+}
+
 sps_status sps_mphase(sps_ctx* c, int32_t R_fixed, int32_t* R_out, double* min_rne, int32_t* h_out) {
   if (!c) return SPS_E_CONFIG;
   CU(c, cudaSetDevice(c->cfg.device));
   if (!c->cphase_done) return fail(c, SPS_E_STATE, "sps_mphase before sps_cphase");
   const bool power = c->cfg.tempering == SPS_POWER_TEMPERING;
   const int t1 = power ? c->n : c->t;
-  const double temper = power ? c->phi : 1.0;
-  const int64_t Pl = c->Pl;
+  const bool adaptive = R_fixed <= 0;
+  const int Rmax = adaptive ? c->cfg.max_m_steps : R_fixed;
+  // reset stop / step counter; moments + chol(h V) of the resampled particles
+  CU(c, cudaMemsetAsync(&c->ctl->stop, 0, sizeof(int), c->stream));
+  CU(c, cudaMemsetAsync(&c->ctl->steps_done, 0, sizeof(int), c->stream));
   if (c->need_pre_moments) {
-    TRY(moments(c));
-    TRY(finalize(c, 0));  // V of the resampled particles, chol(h V)
+    TRY(accept_moments(c, false, 1, 1.0, 0u, nullptr));
+    TRY(finalize(c, 0, false, nullptr));
     c->need_pre_moments = false;
   }
-  int r = 0;
+  const uint32_t step0 = c->mstep;
+  TRY(launch_normals(c, TAG_PROPOSAL, step0, (int)(step0 & 1u)));
+  TRY(launch_mstep(c, step0, 0, adaptive));
+  int r = 1;
+  Ctl got{};
   for (;;) {
-    r += 1;
-    if (R_fixed <= 0 && r > c->cfg.max_m_steps)
-      return fail(c, SPS_E_MIXING, "M phase did not reach RNE >= K in %d steps", c->cfg.max_m_steps);
-    // K8 propose
-    TRY(launch_draw(c, false, c->theta, c->Lprop, c->mstep, c->theta_s, c->lp_s));
-    // K1 proposal log-likelihood over [0, t_l)
-    int nch = 1;
-    TRY(launch_loglik(c, c->theta_s, c->d, Pl, 0, t1, c->part, c->max_chunks, &nch));
+    // keep one step queued behind the one being checked
+    auto h0 = std::chrono::steady_clock::now();
+    if (r < Rmax) TRY(launch_mstep(c, step0 + (uint32_t)r, r % 2, adaptive));
+    auto h1 = std::chrono::steady_clock::now();
+    CU(c, cudaEventSynchronize(c->evs[(r - 1) % 2]));
+    auto h2 = std::chrono::steady_clock::now();
+    c->host_launch_us += std::chrono::duration<double, std::micro>(h1 - h0).count();
+    c->host_wait_us += std::chrono::duration<double, std::micro>(h2 - h1).count();
+    c->syncs += 1;
+    got = c->hslot[(r - 1) % 2];
     c->pairs += (double)c->P * t1;
-    // K9 accept
-    CU(c, cudaMemsetAsync(&c->ctl->acc, 0, sizeof(unsigned long long), c->stream));
-    k_accept<<<(unsigned)((Pl + 255) / 256), 256, 0, c->stream>>>(
-        c->theta, c->L, c->lp, c->theta_s, c->part, nch, c->lp_s, c->d, Pl, c->p0, temper, c->cfg.seed, c->mstep,
-        (uint32_t)c->cfg.pass, c->ctl, nullptr);
-    CHECK_LAUNCH(c);
-    c->mstep += 1;
-    // K6 + K7: moments of theta^(l,r) -> h, RNE, stop, next chol(h V)
-    TRY(moments(c));
-    TRY(finalize(c, 1));
-    TRY(read_ctl(c));
-    if (R_fixed > 0 ? r >= R_fixed : c->hctl->stop) break;
+    if (got.err == ERR_NUMERIC)
+      return fail(c, SPS_E_NUMERIC, "numerical failure in the M phase (non-finite loglik or Cholesky failure "
+                                    "after ridge; cf. PAPER.md:1024-1030)");
+    if (adaptive ? got.stop != 0 : r >= R_fixed) break;
+    if (r >= Rmax) {
+      CU(c, cudaStreamSynchronize(c->stream));
+      return fail(c, SPS_E_MIXING, "M phase did not reach RNE >= K in %d steps", c->cfg.max_m_steps);
+    }
+    r += 1;
   }
+  c->mstep = step0 + (uint32_t)r;
+  *c->hctl = got;
   c->cphase_done = false;
   c->tr_R.push_back(r);
-  c->tr_rne.push_back(c->hctl->minrne);
-  c->tr_h.push_back(c->hctl->h);
+  c->tr_rne.push_back(got.minrne);
+  c->tr_h.push_back(got.h);
   if (final_cycle(c)) c->finished = true;
   if (R_out) *R_out = r;
-  if (min_rne) *min_rne = c->hctl->minrne;
-  if (h_out) *h_out = c->hctl->h;
+  if (min_rne) *min_rne = got.minrne;
+  if (h_out) *h_out = got.h;
   return SPS_OK;
 }
 
@@ -893,7 +1155,7 @@ sps_status sps_moments(sps_ctx* c, int32_t m, const double* A, double* mean, dou
     c->fn_cap = m;
   }
   CU(c, cudaMemcpyAsync(c->fn_A, A, sizeof(double) * m * c->d, cudaMemcpyHostToDevice, c->stream));
-  TRY(moments(c));
+  TRY(accept_moments(c, false, 1, 1.0, 0u, nullptr));
   const size_t smem = sizeof(double) * (c->d + c->J);
   k_functional_stats<<<1, 256, smem, c->stream>>>(c->gath, c->G, c->slice_len, c->J, c->Jl, c->N, c->d, c->shift,
                                                   c->fn_A, m, c->fn_out);
