@@ -17,8 +17,8 @@ namespace sps {
 constexpr int PR_TILE = 64;  // particles per block (8 DMMA row tiles)
 struct DrawArgs {
   const double* base;  // P x d, or nullptr -> mu
-  const double* Lz;    // d x d lower factor
-  const double* Sinv;  // d x d prior precision
+  const double* Lz;    // lower factor, padded NP x KP (NP = round_up(d, 8), KP = round_up(d, 4))
+  const double* Sinv;  // prior precision, padded NP x KP
   const double* mu;
   const double* Z;  // P x 2 ceil(d/2) standard normals (k_normals)
   double* out;
@@ -33,7 +33,7 @@ struct DrawArgs {
 // particle: Z[p][2 pr + {0,1}] = Box-Muller pair pr (R15).  One thread per
 // (particle, pair).  Independent of the particle state, so the engine runs it
 // one M step ahead on a side stream, overlapped with the latency-bound kernels.
-__global__ void __launch_bounds__(256) k_normals(int64_t P, int64_t p0, int np, uint64_t seed, uint32_t step,
+__global__ void __launch_bounds__(256) k_normals(int64_t P, int64_t p0, int np, int ldz, uint64_t seed, uint32_t step,
                                                  uint32_t tag, uint32_t pass, double* __restrict__ Z) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= P * np) return;
@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(256) k_normals(int64_t P, int64_t p0, int np, 
   const int pr = (int)(t - p * np);
   double z0, z1;
   normal_pair(seed, (uint32_t)pr, (uint32_t)(p0 + p), step, tag, pass, &z0, &z1);
-  reinterpret_cast<double2*>(Z)[t] = make_double2(z0, z1);
+  reinterpret_cast<double2*>(Z + p * ldz)[pr] = make_double2(z0, z1);
 }
 
 // One m8n8k4 fp64 tensor-core MMA (DMMA): {c0,c1} += A(8x4) B(4x8) fragment.
@@ -71,86 +71,185 @@ __global__ void __launch_bounds__(256) k_propose(DrawArgs a) {
   double* smu = qp + PR_TILE * NT;  // KP
   double* sL = smu + KP;            // NP x KP (STAGE)
   double* sS = sL + NP * KP;        // NP x KP (STAGE)
-  const int64_t pb = (int64_t)blockIdx.x * PR_TILE;
-  const int cnt = (int)min((int64_t)PR_TILE, a.P - pb);
-  double* Bs = sS + (STAGE ? NP * KP : 0);  // PR_TILE x d base rows (theta), when base != nullptr
-  // one bulk cp.async round: Z rows, base rows, Lz / Sinv; zero padding by plain stores
+  double* Bs = sS + (STAGE ? NP * KP : 0);  // PR_TILE x d base rows (theta)
+  // mu; Lz and Sinv arrive in the padded DMMA layout (NP x KP, zeros outside d x d) -> bulk copies
   for (int i = threadIdx.x; i < KP; i += blockDim.x) smu[i] = i < d ? a.mu[i] : 0.0;
-  if (STAGE)
-    for (int idx = threadIdx.x; idx < NP * KP; idx += blockDim.x) {
-      const int i = idx / KP, j = idx - i * KP;
-      if (i < d && j < d) {
-        cp_async8(sL + idx, a.Lz + i * d + j);
-        cp_async8(sS + idx, a.Sinv + i * d + j);
-      } else {
-        sL[idx] = 0.0;
-        sS[idx] = 0.0;
-      }
-    }
-  for (int idx = threadIdx.x; idx < PR_TILE * KP; idx += blockDim.x) {
-    const int p = idx / KP, j = idx - p * KP;
-    if (p < cnt && j < d)
-      cp_async8(Zs + idx, a.Z + (pb + p) * d2 + j);
-    else
-      Zs[idx] = 0.0;
-  }
-  if (a.base)
-    for (int idx = threadIdx.x; idx < cnt * d; idx += blockDim.x) cp_async8(Bs + idx, a.base + pb * d + idx);
-  cp_async_wait_all();
-  __syncthreads();
-  auto Lf = [&](int i, int j) -> double {
-    if (STAGE) return sL[i * KP + j];
-    return (i < d && j < d) ? __ldg(a.Lz + i * d + j) : 0.0;
-  };
-  auto Sf = [&](int i, int j) -> double {
-    if (STAGE) return sS[i * KP + j];
-    return (i < d && j < d) ? __ldg(a.Sinv + i * d + j) : 0.0;
-  };
+  auto Lf = [&](int i, int j) -> double { return STAGE ? sL[i * KP + j] : __ldg(a.Lz + i * KP + j); };
+  auto Sf = [&](int i, int j) -> double { return STAGE ? sS[i * KP + j] : __ldg(a.Sinv + i * KP + j); };
   const int MT = PR_TILE / 8, ntiles = MT * NT;
   const int ar = lane >> 2, ac = lane & 3;
-  // theta* = base + Z L'  (C[p][i] = sum_j Z[p][j] L[i][j])
-  for (int t = w; t < ntiles; t += 8) {
-    const int mt = t / NT, nt = t - mt * NT;
-    double c0 = 0.0, c1 = 0.0;
-    for (int k0 = 0; k0 < KP; k0 += 4)
-      dmma884(c0, c1, Zs[(mt * 8 + ar) * KP + k0 + ac], Lf(nt * 8 + ar, k0 + ac));
-    const int p = mt * 8 + ar;
-    const int i0 = nt * 8 + 2 * ac;
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int i = i0 + e;
-      if (i < KP) {
-        double dv = 0.0;
-        if (i < d && p < cnt) {
-          const double v = (a.base ? Bs[p * d + i] : smu[i]) + (e ? c1 : c0);
-          a.out[(pb + p) * d + i] = v;
-          dv = v - smu[i];
-        }
-        Ds[p * KP + i] = dv;
+  __shared__ __align__(8) uint64_t bar;
+  if (threadIdx.x == 0) mbar_init(&bar, 1);
+  __syncthreads();
+  const int64_t ntl = (a.P + PR_TILE - 1) / PR_TILE;
+  unsigned phase = 0;
+  for (int64_t tile = blockIdx.x; tile < ntl; tile += gridDim.x) {
+    const int64_t pb = tile * PR_TILE;
+    const int cnt = (int)min((int64_t)PR_TILE, a.P - pb);
+    __syncthreads();  // previous tile done with Zs / Ds / Bs / qp
+    if (threadIdx.x == 0) {  // TMA bulk copies: Z tile (rows of KP, zero padded in memory), theta tile, Lz, Sinv
+      const unsigned zb = (unsigned)(PR_TILE * KP * 8);
+      const unsigned bb = a.base ? (unsigned)(round_up(cnt * d, 2) * 8) : 0u;
+      const unsigned mb = (STAGE && phase == 0) ? (unsigned)(NP * KP * 8) : 0u;
+      mbar_arrive_expect_tx(&bar, zb + bb + 2 * mb);
+      bulk_g2s(Zs, a.Z + pb * KP, zb, &bar);
+      if (a.base) bulk_g2s(Bs, a.base + pb * d, bb, &bar);
+      if (mb) {
+        bulk_g2s(sL, a.Lz, mb, &bar);
+        bulk_g2s(sS, a.Sinv, mb, &bar);
       }
     }
+    mbar_wait(&bar, phase);
+    phase ^= 1u;
+    __syncthreads();
+    // theta* = base + Z L'  (C[p][i] = sum_j Z[p][j] L[i][j])
+    for (int t = w; t < ntiles; t += 8) {
+      const int mt = t / NT, nt = t - mt * NT;
+      double c0 = 0.0, c1 = 0.0;
+      for (int k0 = 0; k0 < KP; k0 += 4)
+        dmma884(c0, c1, Zs[(mt * 8 + ar) * KP + k0 + ac], Lf(nt * 8 + ar, k0 + ac));
+      const int p = mt * 8 + ar;
+      const int i0 = nt * 8 + 2 * ac;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = i0 + e;
+        if (i < KP) {
+          double dv = 0.0;
+          if (i < d && p < cnt) {
+            const double v = (a.base ? Bs[p * d + i] : smu[i]) + (e ? c1 : c0);
+            a.out[(pb + p) * d + i] = v;
+            dv = v - smu[i];
+          }
+          Ds[p * KP + i] = dv;
+        }
+      }
+    }
+    __syncthreads();
+    // U = Delta Sinv; q_p = sum_i Delta[p][i] U[p][i]
+    for (int t = w; t < ntiles; t += 8) {
+      const int mt = t / NT, nt = t - mt * NT;
+      double c0 = 0.0, c1 = 0.0;
+      for (int k0 = 0; k0 < KP; k0 += 4)
+        dmma884(c0, c1, Ds[(mt * 8 + ar) * KP + k0 + ac], Sf(nt * 8 + ar, k0 + ac));
+      const int p = mt * 8 + ar, i0 = nt * 8 + 2 * ac;
+      double q = 0.0;
+      if (i0 < KP) q = fma(Ds[p * KP + i0], c0, q);
+      if (i0 + 1 < KP) q = fma(Ds[p * KP + i0 + 1], c1, q);
+      q += __shfl_xor_sync(0xffffffffu, q, 1);
+      q += __shfl_xor_sync(0xffffffffu, q, 2);
+      if (ac == 0) qp[p * NT + nt] = q;
+    }
+    __syncthreads();
+    for (int p = threadIdx.x; p < cnt; p += blockDim.x) {
+      double q = 0.0;
+      for (int nt = 0; nt < NT; ++nt) q += qp[p * NT + nt];
+      if (!isfinite(q)) atomicExch(&a.ctl->err, ERR_NUMERIC);
+      a.lp_out[pb + p] = -0.5 * q;
+    }
   }
+}
+
+
+// Register-blocked variant for d <= 32 (KK = round_up(d,4)/4 k-steps, NT =
+// round_up(d,8)/8 column tiles): warp w owns particle rows 8w..8w+7 of the
+// tile; all Lz and Sinv B-fragments live in registers (2 NT KK doubles), so a
+// DMMA costs one shared load of its A fragment (the two-operand smem version
+// is shared-memory-bandwidth bound: 512 B of LDS per 4-cycle DMMA).
+template <int KK>
+__global__ void __launch_bounds__(256, 1) k_propose_rb(DrawArgs a) {
+  constexpr int KP = 4 * KK, NT = (KP + 7) / 8, NP = 8 * NT;
+  extern __shared__ double sm[];
+  if (a.stop && *a.stop) return;
+  const int d = a.d;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, ar = lane >> 2, ac = lane & 3;
+  double* Zs = sm;                  // PR_TILE x KP
+  double* Ds = Zs + PR_TILE * KP;   // PR_TILE x KP (theta* - mu)
+  double* smu = Ds + PR_TILE * KP;  // KP
+  double* sL = smu + KP;            // NP x KP
+  double* sS = sL + NP * KP;        // NP x KP
+  double* Bs = sS + NP * KP;        // PR_TILE x d
+  __shared__ __align__(8) uint64_t bar;
+  if (threadIdx.x == 0) mbar_init(&bar, 1);
+  for (int i = threadIdx.x; i < KP; i += blockDim.x) smu[i] = i < d ? a.mu[i] : 0.0;
   __syncthreads();
-  // U = Delta Sinv; q_p = sum_i Delta[p][i] U[p][i]
-  for (int t = w; t < ntiles; t += 8) {
-    const int mt = t / NT, nt = t - mt * NT;
-    double c0 = 0.0, c1 = 0.0;
-    for (int k0 = 0; k0 < KP; k0 += 4)
-      dmma884(c0, c1, Ds[(mt * 8 + ar) * KP + k0 + ac], Sf(nt * 8 + ar, k0 + ac));
-    const int p = mt * 8 + ar, i0 = nt * 8 + 2 * ac;
+  const int64_t ntl = (a.P + PR_TILE - 1) / PR_TILE;
+  double bL[NT][KK], bS[NT][KK];
+  unsigned phase = 0;
+  for (int64_t tile = blockIdx.x; tile < ntl; tile += gridDim.x) {
+    const int64_t pb = tile * PR_TILE;
+    const int cnt = (int)min((int64_t)PR_TILE, a.P - pb);
+    __syncthreads();  // previous tile's readers of Zs / Bs are done
+    if (threadIdx.x == 0) {
+      const unsigned zb = (unsigned)(PR_TILE * KP * 8);
+      const unsigned bb = a.base ? (unsigned)(round_up(cnt * d, 2) * 8) : 0u;
+      const unsigned mb = phase == 0 ? (unsigned)(NP * KP * 8) : 0u;
+      mbar_arrive_expect_tx(&bar, zb + bb + 2 * mb);
+      bulk_g2s(Zs, a.Z + pb * KP, zb, &bar);
+      if (a.base) bulk_g2s(Bs, a.base + pb * d, bb, &bar);
+      if (mb) {
+        bulk_g2s(sL, a.Lz, mb, &bar);
+        bulk_g2s(sS, a.Sinv, mb, &bar);
+      }
+    }
+    mbar_wait(&bar, phase & 1u);
+    if (phase == 0) {
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int kk = 0; kk < KK; ++kk) {
+          bL[nt][kk] = sL[(nt * 8 + ar) * KP + kk * 4 + ac];
+          bS[nt][kk] = sS[(nt * 8 + ar) * KP + kk * 4 + ac];
+        }
+    }
+    ++phase;
+    const int p = w * 8 + ar;  // this lane's particle row (A / C fragments)
+    double c[NT][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) c[nt][0] = c[nt][1] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < KK; ++kk) {
+      const double av = Zs[p * KP + kk * 4 + ac];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) dmma884(c[nt][0], c[nt][1], av, bL[nt][kk]);
+    }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = nt * 8 + 2 * ac + e;
+        if (i < KP) {
+          double dv = 0.0;
+          if (i < d && p < cnt) {
+            const double v = (a.base ? Bs[p * d + i] : smu[i]) + c[nt][e];
+            a.out[(pb + p) * d + i] = v;
+            dv = v - smu[i];
+          }
+          Ds[p * KP + i] = dv;
+        }
+      }
+    __syncwarp();
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) c[nt][0] = c[nt][1] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < KK; ++kk) {
+      const double av = Ds[p * KP + kk * 4 + ac];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) dmma884(c[nt][0], c[nt][1], av, bS[nt][kk]);
+    }
     double q = 0.0;
-    if (i0 < KP) q = fma(Ds[p * KP + i0], c0, q);
-    if (i0 + 1 < KP) q = fma(Ds[p * KP + i0 + 1], c1, q);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = nt * 8 + 2 * ac + e;
+        if (i < KP) q = fma(Ds[p * KP + i], c[nt][e], q);
+      }
     q += __shfl_xor_sync(0xffffffffu, q, 1);
     q += __shfl_xor_sync(0xffffffffu, q, 2);
-    if (ac == 0) qp[p * NT + nt] = q;
-  }
-  __syncthreads();
-  for (int p = threadIdx.x; p < cnt; p += blockDim.x) {
-    double q = 0.0;
-    for (int nt = 0; nt < NT; ++nt) q += qp[p * NT + nt];
-    if (!isfinite(q)) atomicExch(&a.ctl->err, ERR_NUMERIC);
-    a.lp_out[pb + p] = -0.5 * q;
+    if (ac == 0 && p < cnt) {
+      if (!isfinite(q)) atomicExch(&a.ctl->err, ERR_NUMERIC);
+      a.lp_out[pb + p] = -0.5 * q;
+    }
   }
 }
 
@@ -212,31 +311,47 @@ __global__ void __launch_bounds__(256) k_accept_mom(AccArgs a) {
     acc[q] = ok;
   }
   nacc = block_sum(nacc, red_i);  // includes a __syncthreads: acc[] visible
-  // stage the updated particle rows (accepted -> theta*, else theta) in one cp.async round
+  // stage the updated particle rows (accepted -> theta*, else theta) in one cp.async round;
+  // flat (q, i) loops with incremental row/column (no integer division)
   const int64_t off0 = pbase * d;
-  const int nel = tp * d;
-  for (int idx = threadIdx.x; idx < nel; idx += blockDim.x) {
-    const int q = idx / d, i = idx - q * d;
-    cp_async8(Ts + q * LT + i, (acc[q] ? a.theta_s : a.theta) + off0 + idx);
+  const int sr = 256 / d, sc = 256 - sr * d;
+  {
+    int q = threadIdx.x / d, i = threadIdx.x - q * d;
+    for (; q < tp;) {
+      cp_async8(Ts + q * LT + i, (acc[q] ? a.theta_s : a.theta) + off0 + (int64_t)q * d + i);
+      q += sr;
+      i += sc;
+      if (i >= d) {
+        i -= d;
+        ++q;
+      }
+    }
   }
-  for (int idx = threadIdx.x; idx < TK * LT; idx += blockDim.x) {  // zero padding
-    const int q = idx / LT, i = idx - q * LT;
-    if (q >= tp || i >= d) Ts[idx] = 0.0;
-  }
+  for (int q = w; q < TK; q += 8)  // zero padding columns / rows
+    for (int i = d + lane; i < LT; i += 32) Ts[q * LT + i] = 0.0;
+  for (int q = tp + w; q < TK; q += 8)
+    for (int i = lane; i < d; i += 32) Ts[q * LT + i] = 0.0;
   cp_async_wait_all();
   __syncthreads();
-  // write accepted rows back to theta; center on the shift
-  for (int idx = threadIdx.x; idx < nel; idx += blockDim.x) {
-    const int q = idx / d, i = idx - q * d;
-    const double v = Ts[q * LT + i];
-    if (acc[q]) a.theta[off0 + idx] = v;
-    Ts[q * LT + i] = v - a.shift[i];
+  {  // write accepted rows back to theta; center on the shift
+    int q = threadIdx.x / d, i = threadIdx.x - q * d;
+    for (; q < tp;) {
+      const double v = Ts[q * LT + i];
+      if (acc[q]) a.theta[off0 + (int64_t)q * d + i] = v;
+      Ts[q * LT + i] = v - a.shift[i];
+      q += sr;
+      i += sc;
+      if (i >= d) {
+        i -= d;
+        ++q;
+      }
+    }
   }
   __syncthreads();
   double* out = a.bpart + (int64_t)blockIdx.x * W;
   // group-sum partial: 8 interleaved row sets per coordinate, then fixed-order combine
-  for (int t = threadIdx.x; t < 8 * d; t += blockDim.x) {
-    const int part = t / d, i = t - part * d;
+  for (int i = lane; i < d; i += 32) {
+    const int part = w;
     double g0 = 0.0, g1 = 0.0;
     int q = part;
     for (; q + 8 < tp; q += 16) {
@@ -278,6 +393,140 @@ __global__ void __launch_bounds__(256) k_accept_mom(AccArgs a) {
     }
   }
   __syncthreads();
+  if (threadIdx.x < d) {
+    double g = 0.0;
+    for (int part = 0; part < 8; ++part) g += gsp[part * d + threadIdx.x];
+    out[threadIdx.x] = g + (double)tp * a.shift[threadIdx.x];
+  }
+  if (threadIdx.x == 0) out[W - 1] = (double)nacc;
+}
+
+
+// Register-blocked accept + moments for d <= 32 (NT = round_up(d,8)/8 <= 4):
+// K (particles) split over the 8 warps; for each k-step one shared load per
+// index tile serves as both the A and the B fragment of T'T (they coincide),
+// feeding the NT(NT+1)/2 lower-triangle DMMAs; warp partials are combined in
+// fixed order (deterministic).
+template <int NT>
+__global__ void __launch_bounds__(256) k_accept_mom_rb(AccArgs a) {
+  extern __shared__ double sm[];
+  __shared__ int red_i[32];
+  if (a.stop && *a.stop) return;
+  constexpr int NTRI = NT * (NT + 1) / 2;
+  const int d = a.d, W = d + d * d + 1;
+  constexpr int LT = 8 * NT + 4;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, ar = lane >> 2, ac = lane & 3;
+  const int tp = a.tp, TK = round_up(tp, 32);
+  double* Ts = sm;                                                     // TK x LT
+  double* gsp = sm + TK * LT;                                          // 8 x d
+  unsigned char* acc = reinterpret_cast<unsigned char*>(gsp + 8 * d);  // tp flags
+  const int64_t pbase = (int64_t)blockIdx.x * tp;
+  int nacc = 0;
+  for (int q = threadIdx.x; q < tp; q += blockDim.x) {
+    unsigned char ok = 0;
+    if (a.decide) {
+      const int64_t p = pbase + q;
+      double Ls = a.part[p];
+      for (int c = 1; c < a.nchunks; ++c) Ls += a.part[(int64_t)c * a.P + p];
+      const double Lc = a.L[p], lpc = a.lp[p], lps = a.lp_s[p];
+      if (!isfinite(Ls)) atomicExch(&a.ctl->err, ERR_NUMERIC);
+      const double delta = a.temper * (Ls - Lc) + (lps - lpc);
+      const u4 wv = stream_block(a.seed, 0u, (uint32_t)(a.p0 + p), a.step, TAG_ACCEPT, a.pass);
+      if (plog(u01(wv.x, wv.y)) < delta) {
+        ok = 1;
+        a.L[p] = Ls;
+        a.lp[p] = lps;
+        ++nacc;
+      }
+    }
+    acc[q] = ok;
+  }
+  nacc = block_sum(nacc, red_i);
+  const int64_t off0 = pbase * d;
+  const int sr = 256 / d, sc = 256 - sr * d;
+  {
+    int q = threadIdx.x / d, i = threadIdx.x - q * d;
+    for (; q < tp;) {
+      cp_async8(Ts + q * LT + i, (acc[q] ? a.theta_s : a.theta) + off0 + (int64_t)q * d + i);
+      q += sr;
+      i += sc;
+      if (i >= d) {
+        i -= d;
+        ++q;
+      }
+    }
+  }
+  for (int q = w; q < TK; q += 8)
+    for (int i = (q < tp ? d : 0) + lane; i < LT; i += 32) Ts[q * LT + i] = 0.0;
+  cp_async_wait_all();
+  __syncthreads();
+  {
+    int q = threadIdx.x / d, i = threadIdx.x - q * d;
+    for (; q < tp;) {
+      const double v = Ts[q * LT + i];
+      if (acc[q]) a.theta[off0 + (int64_t)q * d + i] = v;
+      Ts[q * LT + i] = v - a.shift[i];
+      q += sr;
+      i += sc;
+      if (i >= d) {
+        i -= d;
+        ++q;
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = lane; i < d; i += 32) {
+    double g0 = 0.0, g1 = 0.0;
+    int q = w;
+    for (; q + 8 < tp; q += 16) {
+      g0 += Ts[q * LT + i];
+      g1 += Ts[(q + 8) * LT + i];
+    }
+    if (q < tp) g0 += Ts[q * LT + i];
+    gsp[w * d + i] = g0 + g1;
+  }
+  // T'T: warp w takes k-steps k0 = 4 (w + 8 m)
+  double cacc[NTRI][2];
+#pragma unroll
+  for (int t = 0; t < NTRI; ++t) cacc[t][0] = cacc[t][1] = 0.0;
+  for (int k0 = 4 * w; k0 < TK; k0 += 32) {
+    double f[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) f[t] = Ts[(k0 + ac) * LT + t * 8 + ar];
+    int tt = 0;
+#pragma unroll
+    for (int mt = 0; mt < NT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt <= mt; ++nt) {
+        dmma884(cacc[tt][0], cacc[tt][1], f[mt], f[nt]);
+        ++tt;
+      }
+  }
+  __syncthreads();  // Ts free: reuse it for the warp partials
+  double* wp = Ts;  // 8 x NTRI x 64
+#pragma unroll
+  for (int t = 0; t < NTRI; ++t) {
+    wp[(w * NTRI + t) * 64 + lane * 2] = cacc[t][0];
+    wp[(w * NTRI + t) * 64 + lane * 2 + 1] = cacc[t][1];
+  }
+  __syncthreads();
+  double* out = a.bpart + (int64_t)blockIdx.x * W;
+  for (int idx = threadIdx.x; idx < NTRI * 64; idx += blockDim.x) {
+    const int t = idx >> 6, e = idx & 63, ln = e >> 1, ee = e & 1;
+    double v = 0.0;
+    for (int ww = 0; ww < 8; ++ww) v += wp[(ww * NTRI + t) * 64 + e];
+    int mt = 0, rem = t;
+    while (rem > mt) {
+      rem -= mt + 1;
+      ++mt;
+    }
+    const int nt = rem;
+    const int i = mt * 8 + (ln >> 2), l = nt * 8 + 2 * (ln & 3) + ee;
+    if (i < d && l < d) {
+      out[d + i * d + l] = v;
+      if (mt != nt) out[d + l * d + i] = v;
+    }
+  }
   if (threadIdx.x < d) {
     double g = 0.0;
     for (int part = 0; part < 8; ++part) g += gsp[part * d + threadIdx.x];
@@ -357,7 +606,8 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
 }
 
 template <int D>
-__device__ bool warp_cholesky(const double* A, int d, double scale, double ridge, double* Lout, double* colbuf) {
+__device__ bool warp_cholesky(const double* A, int d, double scale, double ridge, double* Lout, double* colbuf,
+                              int ldo) {
   const int lane = threadIdx.x & 31;
   double a[D];
 #pragma unroll
@@ -386,22 +636,10 @@ __device__ bool warp_cholesky(const double* A, int d, double scale, double ridge
   if (lane < d)
 #pragma unroll
     for (int l = 0; l < D; ++l)
-      if (l < d) Lout[lane * d + l] = l <= lane ? a[l] : 0.0;
+      if (l < d) Lout[lane * ldo + l] = l <= lane ? a[l] : 0.0;
   return ok;
 }
 
-__device__ bool warp_cholesky_any(const double* A, int d, double scale, double ridge, double* Lout, double* colbuf) {
-  switch ((d + 3) / 4) {
-    case 1: return warp_cholesky<4>(A, d, scale, ridge, Lout, colbuf);
-    case 2: return warp_cholesky<8>(A, d, scale, ridge, Lout, colbuf);
-    case 3: return warp_cholesky<12>(A, d, scale, ridge, Lout, colbuf);
-    case 4: return warp_cholesky<16>(A, d, scale, ridge, Lout, colbuf);
-    case 5: return warp_cholesky<20>(A, d, scale, ridge, Lout, colbuf);
-    case 6: return warp_cholesky<24>(A, d, scale, ridge, Lout, colbuf);
-    case 7: return warp_cholesky<28>(A, d, scale, ridge, Lout, colbuf);
-    default: return warp_cholesky<32>(A, d, scale, ridge, Lout, colbuf);
-  }
-}
 
 // chol((h/100) V) for d <= 32 by one warp (no divergent enclosing code, so
 // shuffles need no convergence barriers); one ridge retry (R13).
@@ -414,11 +652,12 @@ __global__ void __launch_bounds__(32) k_chol_warp(const double* __restrict__ V, 
   for (int i = threadIdx.x; i < d * d; i += 32) sV[i] = V[i];
   __syncwarp();
   const double hd = (double)ctl->h / 100.0;
-  bool ok = warp_cholesky<D>(sV, d, hd, 0.0, Lout, col);
+  const int ld = round_up(d, 4);  // padded (DMMA) layout of the factor
+  bool ok = warp_cholesky<D>(sV, d, hd, 0.0, Lout, col, ld);
   if (!ok) {
     double tr = 0.0;
     for (int i = 0; i < d; ++i) tr += sV[i * d + i];
-    ok = warp_cholesky<D>(sV, d, hd, 1e-8 * tr / (double)d, Lout, col);
+    ok = warp_cholesky<D>(sV, d, hd, 1e-8 * tr / (double)d, Lout, col, ld);
     if (threadIdx.x == 0) {
       ctl->chol_ridge = 1;
       if (!ok) ctl->err = ERR_NUMERIC;
@@ -575,7 +814,7 @@ __global__ void __launch_bounds__(256) k_finalize2(FinArgs f) {
   for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) f.V[idx] = sV[idx];
   if (f.trace && threadIdx.x == 0) f.trace[5] = clock64();
   if (d > 32)
-    for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) f.Lprop[idx] = sA[idx];
+    for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) f.Lprop[(idx / d) * round_up(d, 4) + idx % d] = sA[idx];
   for (int i = threadIdx.x; i < d; i += blockDim.x) f.shift[i] = sbar[i];
   __syncthreads();
   if (f.host_out && threadIdx.x == 0) *f.host_out = *f.ctl;  // into mapped pinned host memory (visible at kernel end)

@@ -97,6 +97,7 @@ struct sps_ctx {
   double* ll_scratch = nullptr;  // sps_loglik chunk partials (grown on demand)
   size_t ll_scratch_cap = 0;
   double* Sinv = nullptr;        // prior precision (d x d)
+  double *LpriorP = nullptr, *SinvP = nullptr;  // padded copies (NP x KP) for the DMMA proposal kernel
   double* bpart = nullptr;       // accept+moments block partials
   int tp = 0, QE = 1, W = 0, nblk = 0;
   Ctl* hslot = nullptr;          // 2 mapped pinned Ctl slots (pipelined M steps), written by k_finalize2
@@ -381,12 +382,16 @@ sps_status launch_loglik(sps_ctx* c, const double* theta, int64_t ldt, int64_t P
 // the side stream `aux` (waits until Zbuf[slot] is free; signals ev_zready).
 sps_status launch_normals(sps_ctx* c, uint32_t tag, uint32_t step, int slot) {
   const int np = (c->d + 1) / 2;
-  CU(c, cudaStreamWaitEvent(c->aux, c->ev_zfree[slot], 0));
+  static const bool serial = getenv("SPS_SERIAL_NORMALS") != nullptr;  // debug: no overlap, own profile category
+  cudaStream_t st = serial ? c->stream : c->aux;
+  CU(c, cudaStreamWaitEvent(st, c->ev_zfree[slot], 0));
   const int64_t tasks = c->Pl * np;
-  k_normals<<<(unsigned)((tasks + 255) / 256), 256, 0, c->aux>>>(c->Pl, c->p0, np, c->cfg.seed, step, tag,
-                                                                 (uint32_t)c->cfg.pass, c->Zbuf[slot]);
+  if (serial) PROF_BEGIN(c);
+  k_normals<<<(unsigned)((tasks + 255) / 256), 256, 0, st>>>(c->Pl, c->p0, np, round_up(c->d, 4), c->cfg.seed,
+                                                                 step, tag, (uint32_t)c->cfg.pass, c->Zbuf[slot]);
   CHECK_LAUNCH(c);
-  CU(c, cudaEventRecord(c->ev_zready[slot], c->aux));
+  if (serial) PROF_END(c, CAT_OTHER);
+  CU(c, cudaEventRecord(c->ev_zready[slot], st));
   return SPS_OK;
 }
 
@@ -400,7 +405,7 @@ sps_status launch_draw(sps_ctx* c, int slot, const double* base, const double* L
   DrawArgs a{};
   a.base = base;
   a.Lz = Lz;
-  a.Sinv = c->Sinv;
+  a.Sinv = c->SinvP;
   a.mu = c->mu;
   a.Z = c->Zbuf[slot];
   a.out = out;
@@ -411,12 +416,29 @@ sps_status launch_draw(sps_ctx* c, int slot, const double* base, const double* L
   a.p0 = c->p0;
   a.d = d;
   CU(c, cudaStreamWaitEvent(c->stream, c->ev_zready[slot], 0));
-  const unsigned grid = (unsigned)((c->Pl + PR_TILE - 1) / PR_TILE);
+  const int64_t ntl = (c->Pl + PR_TILE - 1) / PR_TILE;
   PROF_BEGIN(c);
-  if (stage)
-    k_propose<true><<<grid, 256, smem, c->stream>>>(a);
-  else
-    k_propose<false><<<grid, 256, smem, c->stream>>>(a);
+  if (d <= 32) {  // register-blocked DMMA proposal
+    const int KK = (d + 3) / 4, KPr = 4 * KK, NPr = 8 * ((KPr + 7) / 8);
+    const size_t sm = (size_t)(2 * PR_TILE * KPr + KPr + 2 * NPr * KPr + PR_TILE * d) * sizeof(double);
+    const unsigned grid = (unsigned)std::min<int64_t>(ntl, (int64_t)num_sms() * 2);
+    switch (KK) {
+      case 1: k_propose_rb<1><<<grid, 256, sm, c->stream>>>(a); break;
+      case 2: k_propose_rb<2><<<grid, 256, sm, c->stream>>>(a); break;
+      case 3: k_propose_rb<3><<<grid, 256, sm, c->stream>>>(a); break;
+      case 4: k_propose_rb<4><<<grid, 256, sm, c->stream>>>(a); break;
+      case 5: k_propose_rb<5><<<grid, 256, sm, c->stream>>>(a); break;
+      case 6: k_propose_rb<6><<<grid, 256, sm, c->stream>>>(a); break;
+      case 7: k_propose_rb<7><<<grid, 256, sm, c->stream>>>(a); break;
+      default: k_propose_rb<8><<<grid, 256, sm, c->stream>>>(a); break;
+    }
+  } else {
+    const unsigned grid = (unsigned)ntl;
+    if (stage)
+      k_propose<true><<<grid, 256, smem, c->stream>>>(a);
+    else
+      k_propose<false><<<grid, 256, smem, c->stream>>>(a);
+  }
   CHECK_LAUNCH(c);
   PROF_END(c, CAT_PROPOSE);
   CU(c, cudaEventRecord(c->ev_zfree[slot], c->stream));
@@ -447,10 +469,22 @@ sps_status accept_moments(sps_ctx* c, bool decide, int nchunks, double temper, u
   a.decide = decide ? 1 : 0;
   a.step = step;
   a.pass = (uint32_t)c->cfg.pass;
-  const size_t smem =
-      ((size_t)round_up(c->tp, 4) * (round_up(c->d, 8) + 4) + 8 * (size_t)c->d) * sizeof(double) + (size_t)c->tp + 16;
   PROF_BEGIN(c);
-  k_accept_mom<<<c->nblk, 256, smem, c->stream>>>(a);
+  if (c->d <= 32) {  // register-blocked T'T on DMMA
+    const int NTr = (c->d + 7) / 8;
+    const size_t sm =
+        ((size_t)round_up(c->tp, 32) * (8 * NTr + 4) + 8 * (size_t)c->d) * sizeof(double) + (size_t)c->tp + 16;
+    switch (NTr) {
+      case 1: k_accept_mom_rb<1><<<c->nblk, 256, sm, c->stream>>>(a); break;
+      case 2: k_accept_mom_rb<2><<<c->nblk, 256, sm, c->stream>>>(a); break;
+      case 3: k_accept_mom_rb<3><<<c->nblk, 256, sm, c->stream>>>(a); break;
+      default: k_accept_mom_rb<4><<<c->nblk, 256, sm, c->stream>>>(a); break;
+    }
+  } else {
+    const size_t smem =
+        ((size_t)round_up(c->tp, 4) * (round_up(c->d, 8) + 4) + 8 * (size_t)c->d) * sizeof(double) + (size_t)c->tp + 16;
+    k_accept_mom<<<c->nblk, 256, smem, c->stream>>>(a);
+  }
   CHECK_LAUNCH(c);
   PROF_END(c, CAT_ACCEPT);
   const int d = c->d;
@@ -549,7 +583,7 @@ void free_ctx(sps_ctx* c) {
                   c->lp2, c->lw, c->lw_cur, c->theta_s, c->lp_s, c->part, c->gpart, c->mpart, c->slice, c->gath,
                   c->shift, c->Lprop, c->V, c->rne, c->lwbuf, c->essparts, c->essslice, c->essgath, c->grp_ms,
                   c->grp_ms_gath, c->Lj, c->Lj_gath, c->scal, c->pw_parts, c->pw_slice, c->pw_gath, c->mx_parts,
-                  c->mx_slice, c->mx_gath, c->fn_A, c->fn_out, c->ll_scratch, c->Sinv, c->bpart, c->ctl};
+                  c->mx_slice, c->mx_gath, c->fn_A, c->fn_out, c->ll_scratch, c->Sinv, c->LpriorP, c->SinvP, c->bpart, c->ctl};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->hctl) cudaFreeHost(c->hctl);
@@ -694,7 +728,7 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
   TRY(dalloc(c, &c->Lprior, (size_t)d * d));
   TRY(dalloc(c, &c->xbar, c->k));
   TRY(dalloc(c, &c->mon, (size_t)c->nmon * d));
-  for (double** p : {&c->theta, &c->theta2, &c->theta_s}) TRY(dalloc(c, p, (size_t)Pl * d));
+  for (double** p : {&c->theta, &c->theta2, &c->theta_s}) TRY(dalloc(c, p, (size_t)Pl * d + 2 * PR_TILE));
   for (double** p : {&c->L, &c->L2, &c->lp, &c->lp2, &c->lw, &c->lw_cur, &c->lp_s}) TRY(dalloc(c, p, (size_t)Pl));
   TRY(dalloc(c, &c->part, (size_t)c->max_chunks * Pl));
   TRY(dalloc(c, &c->bpart, (size_t)c->nblk * c->W));
@@ -708,9 +742,12 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
   if (c->G > 1) TRY(dalloc(c, &c->gath, (size_t)c->slice_len * c->G));
   else c->gath = c->slice;
   {
-    const int np = (d + 1) / 2;
-    TRY(dalloc(c, &c->Zbuf[0], (size_t)Pl * 2 * np));
-    TRY(dalloc(c, &c->Zbuf[1], (size_t)Pl * 2 * np));
+    // normals in rows of round_up(d, 4) (DMMA K padding), whole tiles: zeroed once, padding never written
+    const size_t zn = (size_t)(Pl + PR_TILE) * round_up(d, 4);
+    TRY(dalloc(c, &c->Zbuf[0], zn));
+    TRY(dalloc(c, &c->Zbuf[1], zn));
+    CU(c, cudaMemsetAsync(c->Zbuf[0], 0, zn * sizeof(double), c->stream));
+    CU(c, cudaMemsetAsync(c->Zbuf[1], 0, zn * sizeof(double), c->stream));
     CU(c, cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
     for (int q = 0; q < 2; ++q) {
       CU(c, cudaEventCreateWithFlags(&c->ev_zready[q], cudaEventDisableTiming));
@@ -719,7 +756,15 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
     }
   }
   TRY(dalloc(c, &c->shift, d));
-  TRY(dalloc(c, &c->Lprop, (size_t)d * d));
+  {  // padded DMMA layouts (NP x KP, zeros outside d x d): Lprop, prior factor, prior precision
+    const size_t pn = (size_t)round_up(d, 8) * round_up(d, 4);
+    TRY(dalloc(c, &c->Lprop, pn));
+    TRY(dalloc(c, &c->LpriorP, pn));
+    TRY(dalloc(c, &c->SinvP, pn));
+    CU(c, cudaMemsetAsync(c->Lprop, 0, pn * sizeof(double), c->stream));
+    CU(c, cudaMemsetAsync(c->LpriorP, 0, pn * sizeof(double), c->stream));
+    CU(c, cudaMemsetAsync(c->SinvP, 0, pn * sizeof(double), c->stream));
+  }
   TRY(dalloc(c, &c->V, (size_t)d * d));
   TRY(dalloc(c, &c->rne, (size_t)c->nmon));
   TRY(dalloc(c, &c->lwbuf, (size_t)c->Bmax * Pl));
@@ -779,12 +824,45 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
     CU(c, cudaFuncSetAttribute(k_prior_precision, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
     k_prior_precision<<<1, 128, smem, c->stream>>>(c->Lprior, d, c->Sinv);
     CHECK_LAUNCH(c);
+    const size_t ldp = (size_t)round_up(d, 4) * sizeof(double);
+    CU(c, cudaMemcpy2DAsync(c->LpriorP, ldp, c->Lprior, d * sizeof(double), d * sizeof(double), d,
+                            cudaMemcpyDeviceToDevice, c->stream));
+    CU(c, cudaMemcpy2DAsync(c->SinvP, ldp, c->Sinv, d * sizeof(double), d * sizeof(double), d,
+                            cudaMemcpyDeviceToDevice, c->stream));
     // one-time kernel attributes (dynamic shared memory above 48 KB)
     const int big = 200 * 1024;
+    // every kernel of the M step runs with the same (max shared) carveout, so consecutive
+    // launches never reconfigure the SM's L1/shared split
+    if (getenv("SPS_MAX_CARVEOUT")) {
+      const void* fns[] = {(const void*)c->llc.fn, (const void*)k_propose_rb<1>, (const void*)k_propose_rb<2>,
+                           (const void*)k_propose_rb<3>, (const void*)k_propose_rb<4>, (const void*)k_propose_rb<5>,
+                           (const void*)k_propose_rb<6>, (const void*)k_propose_rb<7>, (const void*)k_propose_rb<8>,
+                           (const void*)k_propose<true>, (const void*)k_propose<false>, (const void*)k_accept_mom,
+                           (const void*)k_accept_mom_rb<1>, (const void*)k_accept_mom_rb<2>,
+                           (const void*)k_accept_mom_rb<3>, (const void*)k_accept_mom_rb<4>, (const void*)k_mom_reduce,
+                           (const void*)k_finalize2, (const void*)k_chol_warp<4>, (const void*)k_chol_warp<8>,
+                           (const void*)k_chol_warp<12>, (const void*)k_chol_warp<16>, (const void*)k_chol_warp<20>,
+                           (const void*)k_chol_warp<24>, (const void*)k_chol_warp<28>, (const void*)k_chol_warp<32>,
+                           (const void*)k_normals};
+      for (const void* fn : fns)
+        CU(c, cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+    }
     CU(c, cudaFuncSetAttribute(k_propose<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(c, cudaFuncSetAttribute(k_propose<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(c, cudaFuncSetAttribute(k_finalize2, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(c, cudaFuncSetAttribute(k_accept_mom, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_accept_mom_rb<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_accept_mom_rb<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_accept_mom_rb<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_accept_mom_rb<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_propose_rb<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_propose_rb<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_propose_rb<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_propose_rb<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_propose_rb<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_propose_rb<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_propose_rb<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_propose_rb<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(c, cudaFuncSetAttribute(k_functional_stats, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(c, cudaFuncSetAttribute(k_resample, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(c, cudaFuncSetAttribute(k_cphase_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
@@ -837,7 +915,7 @@ sps_status sps_reset(sps_ctx* c, uint64_t seed, int32_t pass) {
   CU(c, cudaMemcpyAsync(c->shift, c->mu, sizeof(double) * c->d, cudaMemcpyDeviceToDevice, c->stream));
   // Algorithm 1 step 1: theta_jn ~iid p(theta)
   TRY(launch_normals(c, TAG_INIT, 0u, 0));
-  TRY(launch_draw(c, 0, nullptr, c->Lprior, c->theta, c->lp, nullptr));
+  TRY(launch_draw(c, 0, nullptr, c->LpriorP, c->theta, c->lp, nullptr));
   if (c->cfg.tempering == SPS_POWER_TEMPERING) {
     int nch = 1;
     TRY(launch_loglik(c, c->theta, c->d, Pl, 0, c->n, c->part, c->max_chunks, &nch));
