@@ -40,9 +40,11 @@ ORACLE_SAMPLE = dict(J=16, N=256)
 # FP64 pipe peak measured on this pool's B200s (profiles/r01_fp64_peaks.json: DMMA 37.07 TF,
 # 64 FMA/clk/SM at 1.96 GHz; DFMA shares the same pipe).  MEASURED_PEAKS.json carries no FP64 figure.
 FP64_PEAK_TFLOPS = 37.07
-# FP64-pipe instructions per pair in K1's binary epilogue (1 DADD relu-sum,
-# 10 exp, 1 DADD, 1.5 DMUL), counted from the SASS of k_loglik_bin.
-EPILOGUE_DP_OPS_BINARY = 13.5
+# FP64-pipe operations per pair of K1's binary epilogue (1 DADD relu-sum,
+# 10 table-exp, 1 DADD (1 + e), 1 DMUL product), counted from the SASS of k_loglik_bin_mma.
+EPILOGUE_DP_OPS_BINARY = 13.0
+# K1 contraction: 4 floor(k/4) covariates on DMMA + (k mod 4 <= 2) DFMAs, i.e. k FMAs per pair for
+# k = 25; algorithmic contraction flops per pair = 2 k (C - 1).
 
 
 def parse():
@@ -237,6 +239,7 @@ def main():
     pairs_per_launch = cnt["k1_pairs"] / max(cnt["k1_launches"], 1)
     ops_per_pair = 2 * k * (WORKLOAD["C"] - 1) + EPILOGUE_DP_OPS_BINARY
     achieved = pairs_per_launch * ops_per_pair / (k1_avg_ms * 1e-3) / 1e12
+    # FP64 pipe slots actually issued per pair: k FMA-equivalents (DMMA + remainder DFMA) + epilogue ops
     pipe_tflops = pairs_per_launch * 2 * (k * (WORKLOAD["C"] - 1) + EPILOGUE_DP_OPS_BINARY) / (k1_avg_ms * 1e-3) / 1e12
     traffic = None
     tr_path = os.path.join(ROOT, "profiles", "r01_k1_ncu.json")
@@ -307,7 +310,7 @@ def main():
             "clocks": clk,
             "e2e": e2e,
             "gpu_launches": launches,
-            "roofline": {"bound": "alu", "kernel": "k_loglik_bin<25,2> (K1, fused fp64 loglik)",
+            "roofline": {"bound": "alu", "kernel": "k_loglik_bin_mma<6,1,4> (K1: fp64 DMMA contraction + fused softplus/product epilogue)",
                          "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
                          "ops_per_pair": ops_per_pair, "k1_avg_ms": k1_avg_ms,

@@ -46,6 +46,72 @@ __constant__ double c_exp2tab[64] = {
     0x1.d5818dcfba487p+0, 0x1.da9e603db3285p+0, 0x1.dfc97337b9b5fp+0, 0x1.e502ee78b3ff6p+0,
     0x1.ea4afa2a490dap+0, 0x1.efa1bee615a27p+0, 0x1.f50765b6e4540p+0, 0x1.fa7c1819e90d8p+0};
 
+__constant__ double c_exp2tab256[256] = {
+    0x1.0000000000000p+0, 0x1.00b1afa5abcbfp+0, 0x1.0163da9fb3335p+0, 0x1.02168143b0281p+0,
+    0x1.02c9a3e778061p+0, 0x1.037d42e11bbccp+0, 0x1.04315e86e7f85p+0, 0x1.04e5f72f654b1p+0,
+    0x1.059b0d3158574p+0, 0x1.0650a0e3c1f89p+0, 0x1.0706b29ddf6dep+0, 0x1.07bd42b72a836p+0,
+    0x1.0874518759bc8p+0, 0x1.092bdf66607e0p+0, 0x1.09e3ecac6f383p+0, 0x1.0a9c79b1f3919p+0,
+    0x1.0b5586cf9890fp+0, 0x1.0c0f145e46c85p+0, 0x1.0cc922b7247f7p+0, 0x1.0d83b23395decp+0,
+    0x1.0e3ec32d3d1a2p+0, 0x1.0efa55fdfa9c5p+0, 0x1.0fb66affed31bp+0, 0x1.1073028d7233ep+0,
+    0x1.11301d0125b51p+0, 0x1.11edbab5e2ab6p+0, 0x1.12abdc06c31ccp+0, 0x1.136a814f204abp+0,
+    0x1.1429aaea92de0p+0, 0x1.14e95934f312ep+0, 0x1.15a98c8a58e51p+0, 0x1.166a45471c3c2p+0,
+    0x1.172b83c7d517bp+0, 0x1.17ed48695bbc0p+0, 0x1.18af9388c8deap+0, 0x1.1972658375d2fp+0,
+    0x1.1a35beb6fcb75p+0, 0x1.1af99f8138a1cp+0, 0x1.1bbe084045cd4p+0, 0x1.1c82f95281c6bp+0,
+    0x1.1d4873168b9aap+0, 0x1.1e0e75eb44027p+0, 0x1.1ed5022fcd91dp+0, 0x1.1f9c18438ce4dp+0,
+    0x1.2063b88628cd6p+0, 0x1.212be3578a819p+0, 0x1.21f49917ddc96p+0, 0x1.22bdda27912d1p+0,
+    0x1.2387a6e756238p+0, 0x1.2451ffb82140ap+0, 0x1.251ce4fb2a63fp+0, 0x1.25e85711ece75p+0,
+    0x1.26b4565e27cddp+0, 0x1.2780e341ddf29p+0, 0x1.284dfe1f56381p+0, 0x1.291ba7591bb70p+0,
+    0x1.29e9df51fdee1p+0, 0x1.2ab8a66d10f13p+0, 0x1.2b87fd0dad990p+0, 0x1.2c57e39771b2fp+0,
+    0x1.2d285a6e4030bp+0, 0x1.2df961f641589p+0, 0x1.2ecafa93e2f56p+0, 0x1.2f9d24abd886bp+0,
+    0x1.306fe0a31b715p+0, 0x1.31432edeeb2fdp+0, 0x1.32170fc4cd831p+0, 0x1.32eb83ba8ea32p+0,
+    0x1.33c08b26416ffp+0, 0x1.3496266e3fa2dp+0, 0x1.356c55f929ff1p+0, 0x1.36431a2de883bp+0,
+    0x1.371a7373aa9cbp+0, 0x1.37f26231e754ap+0, 0x1.38cae6d05d866p+0, 0x1.39a401b7140efp+0,
+    0x1.3a7db34e59ff7p+0, 0x1.3b57fbfec6cf4p+0, 0x1.3c32dc313a8e5p+0, 0x1.3d0e544ede173p+0,
+    0x1.3dea64c123422p+0, 0x1.3ec70df1c5175p+0, 0x1.3fa4504ac801cp+0, 0x1.40822c367a024p+0,
+    0x1.4160a21f72e2ap+0, 0x1.423fb2709468ap+0, 0x1.431f5d950a897p+0, 0x1.43ffa3f84b9d4p+0,
+    0x1.44e086061892dp+0, 0x1.45c2042a7d232p+0, 0x1.46a41ed1d0057p+0, 0x1.4786d668b3237p+0,
+    0x1.486a2b5c13cd0p+0, 0x1.494e1e192aed2p+0, 0x1.4a32af0d7d3dep+0, 0x1.4b17dea6db7d7p+0,
+    0x1.4bfdad5362a27p+0, 0x1.4ce41b817c114p+0, 0x1.4dcb299fddd0dp+0, 0x1.4eb2d81d8abffp+0,
+    0x1.4f9b2769d2ca7p+0, 0x1.508417f4531eep+0, 0x1.516daa2cf6642p+0, 0x1.5257de83f4eefp+0,
+    0x1.5342b569d4f82p+0, 0x1.542e2f4f6ad27p+0, 0x1.551a4ca5d920fp+0, 0x1.56070dde910d2p+0,
+    0x1.56f4736b527dap+0, 0x1.57e27dbe2c4cfp+0, 0x1.58d12d497c7fdp+0, 0x1.59c0827ff07ccp+0,
+    0x1.5ab07dd485429p+0, 0x1.5ba11fba87a03p+0, 0x1.5c9268a5946b7p+0, 0x1.5d84590998b93p+0,
+    0x1.5e76f15ad2148p+0, 0x1.5f6a320dceb71p+0, 0x1.605e1b976dc09p+0, 0x1.6152ae6cdf6f4p+0,
+    0x1.6247eb03a5585p+0, 0x1.633dd1d1929fdp+0, 0x1.6434634ccc320p+0, 0x1.652b9febc8fb7p+0,
+    0x1.6623882552225p+0, 0x1.671c1c70833f6p+0, 0x1.68155d44ca973p+0, 0x1.690f4b19e9538p+0,
+    0x1.6a09e667f3bcdp+0, 0x1.6b052fa75173ep+0, 0x1.6c012750bdabfp+0, 0x1.6cfdcddd47645p+0,
+    0x1.6dfb23c651a2fp+0, 0x1.6ef9298593ae5p+0, 0x1.6ff7df9519484p+0, 0x1.70f7466f42e87p+0,
+    0x1.71f75e8ec5f74p+0, 0x1.72f8286ead08ap+0, 0x1.73f9a48a58174p+0, 0x1.74fbd35d7cbfdp+0,
+    0x1.75feb564267c9p+0, 0x1.77024b1ab6e09p+0, 0x1.780694fde5d3fp+0, 0x1.790b938ac1cf6p+0,
+    0x1.7a11473eb0187p+0, 0x1.7b17b0976cfdbp+0, 0x1.7c1ed0130c132p+0, 0x1.7d26a62ff86f0p+0,
+    0x1.7e2f336cf4e62p+0, 0x1.7f3878491c491p+0, 0x1.80427543e1a12p+0, 0x1.814d2add106d9p+0,
+    0x1.82589994cce13p+0, 0x1.8364c1eb941f7p+0, 0x1.8471a4623c7adp+0, 0x1.857f4179f5b21p+0,
+    0x1.868d99b4492edp+0, 0x1.879cad931a436p+0, 0x1.88ac7d98a6699p+0, 0x1.89bd0a478580fp+0,
+    0x1.8ace5422aa0dbp+0, 0x1.8be05bad61778p+0, 0x1.8cf3216b5448cp+0, 0x1.8e06a5e0866d9p+0,
+    0x1.8f1ae99157736p+0, 0x1.902fed0282c8ap+0, 0x1.9145b0b91ffc6p+0, 0x1.925c353aa2fe2p+0,
+    0x1.93737b0cdc5e5p+0, 0x1.948b82b5f98e5p+0, 0x1.95a44cbc8520fp+0, 0x1.96bdd9a7670b3p+0,
+    0x1.97d829fde4e50p+0, 0x1.98f33e47a22a2p+0, 0x1.9a0f170ca07bap+0, 0x1.9b2bb4d53fe0dp+0,
+    0x1.9c49182a3f090p+0, 0x1.9d674194bb8d5p+0, 0x1.9e86319e32323p+0, 0x1.9fa5e8d07f29ep+0,
+    0x1.a0c667b5de565p+0, 0x1.a1e7aed8eb8bbp+0, 0x1.a309bec4a2d33p+0, 0x1.a42c980460ad8p+0,
+    0x1.a5503b23e255dp+0, 0x1.a674a8af46052p+0, 0x1.a799e1330b358p+0, 0x1.a8bfe53c12e59p+0,
+    0x1.a9e6b5579fdbfp+0, 0x1.ab0e521356ebap+0, 0x1.ac36bbfd3f37ap+0, 0x1.ad5ff3a3c2774p+0,
+    0x1.ae89f995ad3adp+0, 0x1.afb4ce622f2ffp+0, 0x1.b0e07298db666p+0, 0x1.b20ce6c9a8952p+0,
+    0x1.b33a2b84f15fbp+0, 0x1.b468415b749b1p+0, 0x1.b59728de5593ap+0, 0x1.b6c6e29f1c52ap+0,
+    0x1.b7f76f2fb5e47p+0, 0x1.b928cf22749e4p+0, 0x1.ba5b030a1064ap+0, 0x1.bb8e0b79a6f1fp+0,
+    0x1.bcc1e904bc1d2p+0, 0x1.bdf69c3f3a207p+0, 0x1.bf2c25bd71e09p+0, 0x1.c06286141b33dp+0,
+    0x1.c199bdd85529cp+0, 0x1.c2d1cd9fa652cp+0, 0x1.c40ab5fffd07ap+0, 0x1.c544778fafb22p+0,
+    0x1.c67f12e57d14bp+0, 0x1.c7ba88988c933p+0, 0x1.c8f6d9406e7b5p+0, 0x1.ca3405751c4dbp+0,
+    0x1.cb720dcef9069p+0, 0x1.ccb0f2e6d1675p+0, 0x1.cdf0b555dc3fap+0, 0x1.cf3155b5bab74p+0,
+    0x1.d072d4a07897cp+0, 0x1.d1b532b08c968p+0, 0x1.d2f87080d89f2p+0, 0x1.d43c8eacaa1d6p+0,
+    0x1.d5818dcfba487p+0, 0x1.d6c76e862e6d3p+0, 0x1.d80e316c98398p+0, 0x1.d955d71ff6075p+0,
+    0x1.da9e603db3285p+0, 0x1.dbe7cd63a8315p+0, 0x1.dd321f301b460p+0, 0x1.de7d5641c0658p+0,
+    0x1.dfc97337b9b5fp+0, 0x1.e11676b197d17p+0, 0x1.e264614f5a129p+0, 0x1.e3b333b16ee12p+0,
+    0x1.e502ee78b3ff6p+0, 0x1.e653924676d76p+0, 0x1.e7a51fbc74c83p+0, 0x1.e8f7977cdb740p+0,
+    0x1.ea4afa2a490dap+0, 0x1.eb9f4867cca6ep+0, 0x1.ecf482d8e67f1p+0, 0x1.ee4aaa2188510p+0,
+    0x1.efa1bee615a27p+0, 0x1.f0f9c1cb6412ap+0, 0x1.f252b376bba97p+0, 0x1.f3ac948dd7274p+0,
+    0x1.f50765b6e4540p+0, 0x1.f6632798844f8p+0, 0x1.f7bfdad9cbe14p+0, 0x1.f91d802243c89p+0,
+    0x1.fa7c1819e90d8p+0, 0x1.fbdba3692d514p+0, 0x1.fd3c22b8f71f1p+0, 0x1.fe9d96b2a23d9p+0};
+
 struct LLArgs {
   const double* X;     // n x ldx (binary: rows sign-flipped by (1 - 2 y_t))
   const int32_t* y;    // n labels (C > 2)
@@ -71,6 +137,15 @@ __device__ __forceinline__ double abs_clamp708(double s) {
   return hi >= 0x40862000 ? 708.0 : __hiloint2double(hi, lo);  // 708 = 0x4086200000000000
 }
 
+// One m8n8k4 fp64 tensor-core MMA (DMMA): {c0,c1} += A(8x4) B(4x8) fragment.
+// Fragments (PTX ISA, mma.m8n8k4 .f64): a = A[lane/4][lane%4],
+// b = B[lane%4][lane/4], c0/c1 = C[lane/4][2 (lane%4) + {0,1}].
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
 // e^-a for 0 <= a <= 708: table-driven, ~1 ulp.  sT = 2^(i/64).
 __device__ __forceinline__ double exp_neg(double a, const double* __restrict__ sT) {
   const double t = fma(a, -0x1.71547652b82fep+6, 0x1.8p52);  // MAGIC - round(a 64/ln2)
@@ -84,6 +159,20 @@ __device__ __forceinline__ double exp_neg(double a, const double* __restrict__ s
   return fma(Ts, q, Ts);
 }
 
+// e^-a for 0 <= a <= 708 with the 2^(i/256) table (sT256 in smem): |r| <= ln2/512,
+// degree-4 polynomial (truncation 4e-17): 9 FP64 ops.
+__device__ __forceinline__ double exp_neg256(double a, const double* __restrict__ sT) {
+  const double t = fma(a, -0x1.71547652b82fep+8, 0x1.8p52);  // MAGIC - round(a 256/ln2)
+  const double kd = t - 0x1.8p52;
+  double r = fma(kd, -0x1.62e42fec00000p-9, -a);
+  r = fma(kd, -0x1.d1cf79abc9e3bp-40, r);
+  const int ki = __double2loint(t);
+  const double T = sT[ki & 255];
+  const double q = r * fma(fma(fma(r, 1.0 / 24.0, 1.0 / 6.0), r, 0.5), r, 1.0);
+  const double Ts = __hiloint2double(__double2hiint(T) + ((ki >> 8) << 20), __double2loint(T));
+  return fma(Ts, q, Ts);
+}
+
 // Split a positive running product into mantissa in [1,2) and exponent count.
 __device__ __forceinline__ void renorm(double& Pp, int& E) {
   const int hi = __double2hiint(Pp);
@@ -92,9 +181,10 @@ __device__ __forceinline__ void renorm(double& Pp, int& E) {
   Pp = __hiloint2double(hi - (e << 20), __double2loint(Pp));
 }
 
+// Row stride of the kernel layout of X: k padded to a multiple of 4 (DMMA k-step).
 template <int K>
 __host__ __device__ constexpr int ldx_of() {
-  return K + (K & 1);
+  return (K + 3) / 4 * 4;
 }
 
 // ---------------------------------------------------------------------------
@@ -143,7 +233,7 @@ __global__ void __launch_bounds__(LL_THREADS, 2) k_loglik_bin(LLArgs a) {
 #pragma unroll
     for (int j = 0; j < PPT; ++j) s0[j] = s1[j] = 0.0;
 #pragma unroll
-    for (int i2 = 0; i2 < LDX / 2; ++i2) {
+    for (int i2 = 0; i2 < (K + 1) / 2; ++i2) {
       const double2 u = x0[i2], v = x1[i2];
 #pragma unroll
       for (int j = 0; j < PPT; ++j) {
@@ -172,7 +262,7 @@ __global__ void __launch_bounds__(LL_THREADS, 2) k_loglik_bin(LLArgs a) {
 #pragma unroll
     for (int j = 0; j < PPT; ++j) s0[j] = 0.0;
 #pragma unroll
-    for (int i2 = 0; i2 < LDX / 2; ++i2) {
+    for (int i2 = 0; i2 < (K + 1) / 2; ++i2) {
       const double2 u = x0[i2];
 #pragma unroll
       for (int j = 0; j < PPT; ++j) {
@@ -248,7 +338,7 @@ __global__ void __launch_bounds__(LL_THREADS, 2) k_loglik_mnl(LLArgs a) {
 #pragma unroll
       for (int c = 0; c < CM1; ++c) eta[j][c] = 0.0;
 #pragma unroll
-    for (int i2 = 0; i2 < LDX / 2; ++i2) {
+    for (int i2 = 0; i2 < (K + 1) / 2; ++i2) {
       const double2 u = x0[i2];
 #pragma unroll
       for (int j = 0; j < PPT; ++j)
@@ -286,6 +376,179 @@ __global__ void __launch_bounds__(LL_THREADS, 2) k_loglik_mnl(LLArgs a) {
       a.part[(int64_t)blockIdx.y * a.P + p] = L;
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// Binary, contraction on DMMA (mma.sync m8n8k4 f64): M = 8 observations, N =
+// 8 particles, K = 4 covariates per instruction.  Warp w owns NTW x 8
+// particles whose theta B-fragments (KKD k-steps) stay in registers; each
+// 8-observation tile costs KKD shared loads (A fragments of X) + KKD*NTW
+// DMMAs, i.e. ~0.2 issue slots per pair for the contraction (the DFMA form
+// needs ~31: 25 DFMA + 6 LDS), leaving the issue bandwidth to the epilogue.
+// k = 4 KKD + REM: the last REM (<= 2) covariates are DFMAs on the C
+// fragment instead of a zero-padded DMMA step (k = 25: 25 FMAs, not 28).
+// Lane l holds C[obs = l/4][particle = 2 (l%4) + e] of every n-tile; two
+// observation tiles are folded into each product update; per-lane running
+// sums are combined over the 8 lanes of a particle column at the end.
+template <int TAB>
+__device__ __forceinline__ double exp_neg_tab(double a, const double* __restrict__ sT) {
+  if constexpr (TAB == 256)
+    return exp_neg256(a, sT);
+  else
+    return exp_neg(a, sT);
+}
+
+// H: 8-observation tiles folded into one product update (1 or 2); TAB: exp table size (64 or 256);
+// KS: independent DMMA accumulator chains over k (1 or 2); MINB: min resident blocks (register budget).
+template <int KKD, int REM, int NTW, int H = 1, int TAB = 64, int KS = 1, int MINB = 1>
+__global__ void __launch_bounds__(128, MINB) k_loglik_bin_mma(LLArgs a) {
+  constexpr int KP = 4 * KKD + (REM ? 4 : 0);  // X row stride (k padded to 4)
+  extern __shared__ __align__(16) double smem[];
+  if (a.stop && *a.stop) return;
+  double* sT = smem;        // TAB
+  double* sX = smem + 256;  // (chunk rounded up to 16) x KP
+  const int c0 = a.t0 + blockIdx.y * a.chunk;
+  const int c1 = min(c0 + a.chunk, a.t1);
+  const int nobs = max(c1 - c0, 0);
+  const int nobs16 = (nobs + 15) & ~15;
+  for (int i = threadIdx.x; i < TAB; i += blockDim.x) sT[i] = TAB == 256 ? c_exp2tab256[i] : c_exp2tab[i];
+  {
+    const double2* src = reinterpret_cast<const double2*>(a.X + (int64_t)c0 * KP);
+    double2* dst = reinterpret_cast<double2*>(sX);
+    const int nv = nobs * KP / 2, nv16 = nobs16 * KP / 2;
+    for (int i = threadIdx.x; i < nv16; i += blockDim.x) dst[i] = i < nv ? __ldg(src + i) : make_double2(0.0, 0.0);
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, ar = lane >> 2, ac = lane & 3;
+  const int64_t pw = ((int64_t)blockIdx.x * 4 + w) * (NTW * 8);  // first particle of this warp
+  double b[NTW][KKD > 0 ? KKD : 1];
+  double tr[NTW][2][REM > 0 ? REM : 1];  // remainder covariates of this lane's 2 particles per n-tile
+#pragma unroll
+  for (int nt = 0; nt < NTW; ++nt) {
+    const int64_t p = pw + nt * 8 + ar;
+    const double* row = a.theta + (p < a.P ? p : 0) * a.ldt;
+#pragma unroll
+    for (int kk = 0; kk < KKD; ++kk) {
+      const int k = kk * 4 + ac;
+      b[nt][kk] = (p < a.P && k < a.k) ? __ldg(row + k) : 0.0;
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int64_t q = pw + nt * 8 + 2 * ac + e;
+      const double* rq = a.theta + (q < a.P ? q : 0) * a.ldt;
+#pragma unroll
+      for (int r = 0; r < REM; ++r) tr[nt][e][r] = q < a.P ? __ldg(rq + 4 * KKD + r) : 0.0;
+    }
+  }
+  __syncthreads();
+  double M[NTW][2], Pp[NTW][2];
+  int E[NTW][2];
+#pragma unroll
+  for (int nt = 0; nt < NTW; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      M[nt][e] = 0.0;
+      Pp[nt][e] = 1.0;
+      E[nt][e] = 0;
+    }
+  int nit = 0;
+  for (int t0 = 0; t0 < nobs; t0 += 8 * H) {
+    double acc[H][NTW][2];
+#pragma unroll
+    for (int h = 0; h < H; ++h)
+#pragma unroll
+      for (int nt = 0; nt < NTW; ++nt) acc[h][nt][0] = acc[h][nt][1] = 0.0;
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const double* xr = sX + (t0 + 8 * h + ar) * KP;
+      if (KS == 2 && KKD >= 2) {
+        double acc2[NTW][2];
+#pragma unroll
+        for (int nt = 0; nt < NTW; ++nt) acc2[nt][0] = acc2[nt][1] = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < KKD; ++kk) {
+          const double av = xr[kk * 4 + ac];
+#pragma unroll
+          for (int nt = 0; nt < NTW; ++nt) {
+            if (kk & 1)
+              dmma884(acc2[nt][0], acc2[nt][1], av, b[nt][kk]);
+            else
+              dmma884(acc[h][nt][0], acc[h][nt][1], av, b[nt][kk]);
+          }
+        }
+#pragma unroll
+        for (int nt = 0; nt < NTW; ++nt) {
+          acc[h][nt][0] += acc2[nt][0];
+          acc[h][nt][1] += acc2[nt][1];
+        }
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < KKD; ++kk) {
+          const double av = xr[kk * 4 + ac];
+#pragma unroll
+          for (int nt = 0; nt < NTW; ++nt) dmma884(acc[h][nt][0], acc[h][nt][1], av, b[nt][kk]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < REM; ++r) {
+        const double xv = xr[4 * KKD + r];
+#pragma unroll
+        for (int nt = 0; nt < NTW; ++nt) {
+          acc[h][nt][0] = fma(xv, tr[nt][0][r], acc[h][nt][0]);
+          acc[h][nt][1] = fma(xv, tr[nt][1][r], acc[h][nt][1]);
+        }
+      }
+    }
+    // padded observations (beyond the chunk) contribute s = -inf: relu 0, e^-|s| = 0
+    if (H == 1) {
+      if (t0 + ar < nobs) {
+#pragma unroll
+        for (int nt = 0; nt < NTW; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            M[nt][e] += relu_bits(acc[0][nt][e]);
+            Pp[nt][e] *= 1.0 + exp_neg_tab<TAB>(abs_clamp708(acc[0][nt][e]), sT);
+          }
+      }
+    } else {
+      const bool v0 = t0 + ar < nobs, v1 = t0 + 8 + ar < nobs;
+#pragma unroll
+      for (int nt = 0; nt < NTW; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const double s0 = v0 ? acc[0][nt][e] : -1e300, s1 = v1 ? acc[H - 1][nt][e] : -1e300;
+          M[nt][e] += relu_bits(s0) + relu_bits(s1);
+          const double e0 = exp_neg_tab<TAB>(abs_clamp708(s0), sT), e1 = exp_neg_tab<TAB>(abs_clamp708(s1), sT);
+          Pp[nt][e] *= (1.0 + e0) * (1.0 + e1);
+        }
+    }
+    if ((++nit & 31) == 0) {
+#pragma unroll
+      for (int nt = 0; nt < NTW; ++nt) {
+        renorm(Pp[nt][0], E[nt][0]);
+        renorm(Pp[nt][1], E[nt][1]);
+      }
+    }
+  }
+  // combine the 8 lanes (ar = 0..7) of each particle column: sums of M and E, product of P
+#pragma unroll
+  for (int nt = 0; nt < NTW; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      renorm(Pp[nt][e], E[nt][e]);
+      double m = M[nt][e], pp = Pp[nt][e];
+      int ex = E[nt][e];
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        m += __shfl_xor_sync(0xffffffffu, m, o);
+        pp *= __shfl_xor_sync(0xffffffffu, pp, o);  // 8 factors in [1,2): < 2^8
+        ex += __shfl_xor_sync(0xffffffffu, ex, o);
+      }
+      const int64_t p = pw + nt * 8 + 2 * ac + e;
+      if (ar == 0 && p < a.P) {
+        renorm(pp, ex);
+        a.part[(int64_t)blockIdx.y * a.P + p] = -(m + (log(pp) + (double)ex * 0x1.62e42fefa39efp-1));
+      }
+    }
 }
 
 // Sum chunk partials in chunk order: out[p] = sum_c part[c][p].

@@ -6,6 +6,7 @@
 #pragma once
 #include "common.cuh"
 #include "kernels.cuh"
+#include "loglik.cuh"
 
 namespace sps {
 
@@ -44,14 +45,6 @@ __global__ void __launch_bounds__(256) k_normals(int64_t P, int64_t p0, int np, 
   reinterpret_cast<double2*>(Z + p * ldz)[pr] = make_double2(z0, z1);
 }
 
-// One m8n8k4 fp64 tensor-core MMA (DMMA): {c0,c1} += A(8x4) B(4x8) fragment.
-// Fragments (PTX ISA, mma.m8n8k4 .f64): a = A[lane/4][lane%4],
-// b = B[lane%4][lane/4], c0/c1 = C[lane/4][2 (lane%4) + {0,1}].
-__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
-}
 
 __host__ __device__ constexpr int round_up(int x, int m) { return (x + m - 1) / m * m; }
 

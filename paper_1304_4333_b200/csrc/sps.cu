@@ -283,6 +283,23 @@ bool pick_exact(int k, LLChoice* out, std::integer_sequence<int, Ks...>) {
 
 bool choose_ll(int k, int C, LLChoice* o) {
   const int cm1 = C - 1;
+  static const bool force_dfma = getenv("SPS_K1_DFMA") != nullptr;
+  if (cm1 == 1 && k <= 32 && !force_dfma) {  // DMMA contraction (+ <= 2 remainder DFMAs), 128 particles per block
+    switch (k) {
+#define MMA_CASE(K_, KKD_, REM_)                                       \
+  case K_:                                                             \
+    *o = {k_loglik_bin_mma<KKD_, REM_, 4>, 4 * KKD_ + (REM_ ? 4 : 0), 1}; \
+    return true;
+      MMA_CASE(1, 0, 1) MMA_CASE(2, 0, 2) MMA_CASE(3, 1, 0) MMA_CASE(4, 1, 0) MMA_CASE(5, 1, 1) MMA_CASE(6, 1, 2)
+      MMA_CASE(7, 2, 0) MMA_CASE(8, 2, 0) MMA_CASE(9, 2, 1) MMA_CASE(10, 2, 2) MMA_CASE(11, 3, 0) MMA_CASE(12, 3, 0)
+      MMA_CASE(13, 3, 1) MMA_CASE(14, 3, 2) MMA_CASE(15, 4, 0) MMA_CASE(16, 4, 0) MMA_CASE(17, 4, 1)
+      MMA_CASE(18, 4, 2) MMA_CASE(19, 5, 0) MMA_CASE(20, 5, 0) MMA_CASE(21, 5, 1) MMA_CASE(22, 5, 2)
+      MMA_CASE(23, 6, 0) MMA_CASE(24, 6, 0) MMA_CASE(25, 6, 1) MMA_CASE(26, 6, 2) MMA_CASE(27, 7, 0)
+      MMA_CASE(28, 7, 0) MMA_CASE(29, 7, 1) MMA_CASE(30, 7, 2) MMA_CASE(31, 8, 0) MMA_CASE(32, 8, 0)
+#undef MMA_CASE
+      default: break;
+    }
+  }
   if (cm1 == 1) {
     if (k <= 32) return pick_exact<1, 2>(k, o, std::make_integer_sequence<int, 32>{});
     if (k <= 40) { *o = {ll_ptr<40, 1, 1>(), 40, 1}; return true; }
@@ -339,19 +356,21 @@ sps_status launch_loglik(sps_ctx* c, const double* theta, int64_t ldt, int64_t P
     const int S_hi = std::min(max_chunks, std::max(S_min, std::min(S_min + 24, range / 8)));
     const int warp_regs = ((c->ll_regs * 32 + 255) / 256) * 256;
     const int by_regs = 65536 / ((LL_THREADS / 32) * warp_regs);
+    // cost ~ waves x (chunk + per-block overhead), overhead ~ 24 observation-equivalents
+    // (theta load, X staging, final logs): fills whole waves without shredding the range
     int best = S_min;
-    double best_eff = -1.0;
+    double best_cost = 1e300;
     for (int S = S_min; S <= S_hi; ++S) {
       const int chunk = (range + S - 1) / S;
       const int Se = (range + chunk - 1) / chunk;
-      const size_t smem = 64 * 8 + (size_t)chunk * row_bytes + 16;
+      const size_t smem = 256 * 8 + (size_t)(chunk + 16) * row_bytes + 16;
       const int by_smem = (int)(233472 / (smem + 1024));
       const int occ = std::max(1, std::min(std::min(by_regs, by_smem), 16));
       const double slots = (double)num_sms() * occ;
-      const double blocks = (double)tiles * Se;
-      const double eff = blocks / (std::ceil(blocks / slots) * slots);
-      if (eff > best_eff + 0.01) {
-        best_eff = eff;
+      const double waves = std::ceil((double)tiles * Se / slots);
+      const double cost = waves * (chunk + 24.0);
+      if (cost < best_cost * 0.995) {
+        best_cost = cost;
         best = S;
       }
     }
@@ -361,7 +380,7 @@ sps_status launch_loglik(sps_ctx* c, const double* theta, int64_t ldt, int64_t P
     pl->max_chunks = max_chunks;
     pl->chunk = chunk;
     pl->S = (range + chunk - 1) / chunk;
-    pl->smem = 64 * 8 + (size_t)chunk * c->ldx * 8 + (c->C > 2 ? (size_t)chunk * 4 : 0);
+    pl->smem = 256 * 8 + (size_t)(chunk + 16) * c->ldx * 8 + (c->C > 2 ? (size_t)chunk * 4 : 0);
     if (pl->S > max_chunks) return fail(c, SPS_E_CONFIG, "observation range too long for the chunk buffer");
   }
   LLArgs a{c->Xs, c->y, theta, part, ldt, P, t0, t1, pl->chunk};
@@ -685,7 +704,7 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
     c->ll_regs = fa.numRegs;
     CU(c, cudaFuncSetAttribute(ch.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 101 * 1024 + 1024));
   }
-  c->ldx = ch.KT + (ch.KT & 1);
+  c->ldx = (ch.KT + 3) / 4 * 4;  // X row stride: k padded to 4 (DMMA k-step; zero columns)
   c->nmon = cfg.n_monitors > 0 ? cfg.n_monitors : c->C;
   if (cfg.n_monitors > 0 && !cfg_in->monitors) return fail(c, SPS_E_CONFIG, "n_monitors > 0 but monitors == NULL");
   // accept + moments layout: blocks of tp particles inside one group (tp divides N,
