@@ -187,6 +187,12 @@ const char* sps_last_error(const sps_ctx* ctx);
 /* 128-byte NCCL unique id for rank 0 to broadcast (via torch.distributed). */
 sps_status sps_nccl_unique_id(void* id128);
 
+/* 128-byte id of an in-process loopback group: passed as cfg.nccl_id instead of an
+ * NCCL id, the ranks are contexts of one process (one host thread per rank, any
+ * device, e.g. all on one GPU) and each exchange step is staged through host
+ * memory at a host barrier.  Exercises the sharded engine without NCCL; slow. */
+sps_status sps_loopback_unique_id(void* id128);
+
 /* Zellner g-prior (PAPER.md:665-668 eq. g-prior_def, exchangeable, normalized
  * by eq. prior_norm): cov (d x d, host) = blocks
  * (2 if i == j else 1) * g T (X'X)^-1.  Computed on the device.  (R9) */

@@ -7,4 +7,4 @@ entry point raises.
 """
 from ._lib import EXPORTED, SO, SpsError, build, lib  # noqa: F401
 from .api import (DATA, MULTINOMIAL, POWER, RESIDUAL, SYSTEMATIC, Sps, config, g_prior,  # noqa: F401
-                  nccl_unique_id)
+                  loopback_unique_id, nccl_unique_id)

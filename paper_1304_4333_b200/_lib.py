@@ -67,7 +67,7 @@ EXPORTED = [
     "sps_config_default", "sps_create", "sps_loglik", "sps_cphase", "sps_mphase", "sps_run", "sps_logml",
     "sps_moments", "sps_get_particles", "sps_shard", "sps_destroy", "sps_last_error", "sps_nccl_unique_id",
     "sps_g_prior", "sps_test_philox", "sps_test_normals", "sps_test_portable", "sps_test_resample_int",
-    "sps_test_resample_group", "sps_test_accept", "sps_reset", "sps_set_profiling", "sps_get_counters", "sps_sync",
+    "sps_test_resample_group", "sps_test_accept", "sps_reset", "sps_set_profiling", "sps_get_counters", "sps_sync", "sps_loopback_unique_id",
 ]
 
 
@@ -121,6 +121,7 @@ def _declare(L):
         "sps_destroy": ([vp], None),
         "sps_last_error": ([vp], C.c_char_p),
         "sps_nccl_unique_id": ([vp], st),
+        "sps_loopback_unique_id": ([vp], st),
         "sps_g_prior": ([dp, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_int32, dp], st),
         "sps_test_philox": ([C.c_int32, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)], st),
         "sps_test_normals": ([C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int32, dp], st),

@@ -185,6 +185,13 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def loopback_unique_id() -> bytes:
+    """Id of an in-process loopback rank group (tests of the sharded engine on one GPU)."""
+    buf = C.create_string_buffer(128)
+    _check(lib().sps_loopback_unique_id(buf), what="sps_loopback_unique_id failed")
+    return buf.raw
+
+
 def g_prior(X, C_, g, device=0):
     X = np.ascontiguousarray(X, dtype=np.float64)
     n, k = X.shape

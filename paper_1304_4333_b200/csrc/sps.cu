@@ -20,6 +20,10 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <condition_variable>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <vector>
 
 #include "../../include/sps.h"
@@ -63,6 +67,37 @@ struct NcclApi {
   }
 };
 NcclApi g_nccl;
+
+// Loopback transport: the ranks of one "group" are contexts of ONE process (one host
+// thread per rank, usually on one GPU).  An allgather stages the slice through host
+// memory and meets the other ranks at a host barrier -- no kernel ever waits on another
+// rank.  Used to test the sharded (G > 1) engine on a single GPU.
+constexpr char kLoopMagic[] = "SPS-LOOPBACK-v1";
+struct Loopback {
+  int G = 0;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  std::vector<char> buf[2];
+  void allgather(int rank, const void* send, size_t bytes, void* recv) {
+    std::unique_lock<std::mutex> lk(m);
+    std::vector<char>& b = buf[gen & 1];
+    if (b.size() < (size_t)G * bytes) b.resize((size_t)G * bytes);
+    std::memcpy(b.data() + (size_t)rank * bytes, send, bytes);
+    const uint64_t my = gen;
+    if (++arrived == G) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != my; });
+    }
+    std::memcpy(recv, buf[my & 1].data(), (size_t)G * bytes);
+  }
+};
+std::mutex g_loop_mu;
+std::map<std::string, std::shared_ptr<Loopback>> g_loops;
 }  // namespace
 
 // ================================================================== context
@@ -81,6 +116,8 @@ struct sps_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   ncclComm_t comm = nullptr;
+  std::shared_ptr<Loopback> loop;      // loopback transport (tests), else NCCL
+  std::vector<char> loop_send, loop_recv;
   // device buffers
   double *X = nullptr, *Xs = nullptr, *mu = nullptr, *Lprior = nullptr, *xbar = nullptr, *mon = nullptr;
   int32_t* y = nullptr;
@@ -204,6 +241,17 @@ int num_sms() {
 sps_status gather(sps_ctx* c, const double* send, double* recv, size_t count) {
   if (c->G == 1) {  // single rank: the gathered buffer aliases the local slice
     if (send != recv) CU(c, cudaMemcpyAsync(recv, send, count * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    return SPS_OK;
+  }
+  if (c->loop) {
+    const size_t bytes = count * sizeof(double);
+    if (c->loop_send.size() < bytes) c->loop_send.resize(bytes);
+    if (c->loop_recv.size() < bytes * c->G) c->loop_recv.resize(bytes * c->G);
+    CU(c, cudaMemcpyAsync(c->loop_send.data(), send, bytes, cudaMemcpyDeviceToHost, c->stream));
+    CU(c, cudaStreamSynchronize(c->stream));
+    c->loop->allgather(c->rank, c->loop_send.data(), bytes, c->loop_recv.data());
+    CU(c, cudaMemcpyAsync(recv, c->loop_recv.data(), bytes * c->G, cudaMemcpyHostToDevice, c->stream));
+    CU(c, cudaStreamSynchronize(c->stream));
     return SPS_OK;
   }
   ncclResult_t r = g_nccl.AllGather(send, recv, count, ncclFloat64, c->comm, c->stream);
@@ -654,6 +702,19 @@ void sps_destroy(sps_ctx* ctx) {
   delete ctx;
 }
 
+sps_status sps_loopback_unique_id(void* id128) {
+  if (!id128) return SPS_E_CONFIG;
+  static std::mutex mu;
+  static uint64_t counter = 0;
+  std::lock_guard<std::mutex> lk(mu);
+  char buf[128] = {0};
+  std::memcpy(buf, kLoopMagic, sizeof kLoopMagic - 1);
+  const uint64_t v = ++counter ^ (uint64_t)std::chrono::steady_clock::now().time_since_epoch().count();
+  std::memcpy(buf + 32, &v, sizeof v);
+  std::memcpy(id128, buf, 128);
+  return SPS_OK;
+}
+
 sps_status sps_nccl_unique_id(void* id128) {
   std::string why;
   if (!id128 || !g_nccl.load(&why)) return SPS_E_NCCL;
@@ -730,7 +791,17 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
     CU(c, cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->own_stream = true;
   }
-  if (c->G > 1) {
+  if (c->G > 1 && cfg_in->nccl_id &&
+      std::memcmp(cfg_in->nccl_id, kLoopMagic, sizeof kLoopMagic - 1) == 0) {  // loopback transport
+    const std::string key((const char*)cfg_in->nccl_id, 128);
+    std::lock_guard<std::mutex> lk(g_loop_mu);
+    auto& lb = g_loops[key];
+    if (!lb) {
+      lb = std::make_shared<Loopback>();
+      lb->G = c->G;
+    }
+    c->loop = lb;
+  } else if (c->G > 1) {
     std::string why;
     if (!cfg_in->nccl_id) return fail(c, SPS_E_CONFIG, "nranks > 1 requires nccl_id");
     if (!g_nccl.load(&why)) return fail(c, SPS_E_NCCL, "%s", why.c_str());
