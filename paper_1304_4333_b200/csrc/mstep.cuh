@@ -34,8 +34,11 @@ struct DrawArgs {
 // particle: Z[p][2 pr + {0,1}] = Box-Muller pair pr (R15).  One thread per
 // (particle, pair).  Independent of the particle state, so the engine runs it
 // one M step ahead on a side stream, overlapped with the latency-bound kernels.
+// With `logu` (PROPOSAL streams), also plog of the step's ACCEPT uniform of each
+// particle (R16), so the accept test on the critical path is one comparison.
 __global__ void __launch_bounds__(256) k_normals(int64_t P, int64_t p0, int np, int ldz, uint64_t seed, uint32_t step,
-                                                 uint32_t tag, uint32_t pass, double* __restrict__ Z) {
+                                                 uint32_t tag, uint32_t pass, double* __restrict__ Z,
+                                                 double* __restrict__ logu) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= P * np) return;
   const int64_t p = t / np;
@@ -43,6 +46,10 @@ __global__ void __launch_bounds__(256) k_normals(int64_t P, int64_t p0, int np, 
   double z0, z1;
   normal_pair(seed, (uint32_t)pr, (uint32_t)(p0 + p), step, tag, pass, &z0, &z1);
   reinterpret_cast<double2*>(Z + p * ldz)[pr] = make_double2(z0, z1);
+  if (logu && pr == 0) {
+    const u4 w = stream_block(seed, 0u, (uint32_t)(p0 + p), step, TAG_ACCEPT, pass);
+    logu[p] = plog(u01(w.x, w.y));
+  }
 }
 
 
@@ -149,7 +156,7 @@ __global__ void __launch_bounds__(256) k_propose(DrawArgs a) {
 // DMMA costs one shared load of its A fragment (the two-operand smem version
 // is shared-memory-bandwidth bound: 512 B of LDS per 4-cycle DMMA).
 template <int KK>
-__global__ void __launch_bounds__(256, 1) k_propose_rb(DrawArgs a) {
+__global__ void __launch_bounds__(256, 2) k_propose_rb(DrawArgs a) {
   constexpr int KP = 4 * KK, NT = (KP + 7) / 8, NP = 8 * NT;
   extern __shared__ double sm[];
   if (a.stop && *a.stop) return;
@@ -166,7 +173,7 @@ __global__ void __launch_bounds__(256, 1) k_propose_rb(DrawArgs a) {
   for (int i = threadIdx.x; i < KP; i += blockDim.x) smu[i] = i < d ? a.mu[i] : 0.0;
   __syncthreads();
   const int64_t ntl = (a.P + PR_TILE - 1) / PR_TILE;
-  double bL[NT][KK], bS[NT][KK];
+  double bL[NT][KK];  // Lz B-fragments in registers; Sinv fragments are read from shared memory
   unsigned phase = 0;
   for (int64_t tile = blockIdx.x; tile < ntl; tile += gridDim.x) {
     const int64_t pb = tile * PR_TILE;
@@ -191,7 +198,6 @@ __global__ void __launch_bounds__(256, 1) k_propose_rb(DrawArgs a) {
 #pragma unroll
         for (int kk = 0; kk < KK; ++kk) {
           bL[nt][kk] = sL[(nt * 8 + ar) * KP + kk * 4 + ac];
-          bS[nt][kk] = sS[(nt * 8 + ar) * KP + kk * 4 + ac];
         }
     }
     ++phase;
@@ -227,7 +233,7 @@ __global__ void __launch_bounds__(256, 1) k_propose_rb(DrawArgs a) {
     for (int kk = 0; kk < KK; ++kk) {
       const double av = Ds[p * KP + kk * 4 + ac];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) dmma884(c[nt][0], c[nt][1], av, bS[nt][kk]);
+      for (int nt = 0; nt < NT; ++nt) dmma884(c[nt][0], c[nt][1], av, sS[(nt * 8 + ar) * KP + kk * 4 + ac]);
     }
     double q = 0.0;
 #pragma unroll
@@ -259,6 +265,7 @@ struct AccArgs {
   const double* part;
   const double* lp_s;
   const double* shift;
+  const double* logu;  // plog of the ACCEPT uniforms of this step (precomputed), or nullptr
   double* bpart;
   Ctl* ctl;
   const int* stop;
@@ -293,8 +300,14 @@ __global__ void __launch_bounds__(256) k_accept_mom(AccArgs a) {
       const double Lc = a.L[p], lpc = a.lp[p], lps = a.lp_s[p];
       if (!isfinite(Ls)) atomicExch(&a.ctl->err, ERR_NUMERIC);
       const double delta = a.temper * (Ls - Lc) + (lps - lpc);
-      const u4 wv = stream_block(a.seed, 0u, (uint32_t)(a.p0 + p), a.step, TAG_ACCEPT, a.pass);
-      if (plog(u01(wv.x, wv.y)) < delta) {
+      double lu;
+      if (a.logu) {
+        lu = a.logu[p];
+      } else {
+        const u4 wv = stream_block(a.seed, 0u, (uint32_t)(a.p0 + p), a.step, TAG_ACCEPT, a.pass);
+        lu = plog(u01(wv.x, wv.y));
+      }
+      if (lu < delta) {
         ok = 1;
         a.L[p] = Ls;
         a.lp[p] = lps;
@@ -424,8 +437,14 @@ __global__ void __launch_bounds__(256) k_accept_mom_rb(AccArgs a) {
       const double Lc = a.L[p], lpc = a.lp[p], lps = a.lp_s[p];
       if (!isfinite(Ls)) atomicExch(&a.ctl->err, ERR_NUMERIC);
       const double delta = a.temper * (Ls - Lc) + (lps - lpc);
-      const u4 wv = stream_block(a.seed, 0u, (uint32_t)(a.p0 + p), a.step, TAG_ACCEPT, a.pass);
-      if (plog(u01(wv.x, wv.y)) < delta) {
+      double lu;
+      if (a.logu) {
+        lu = a.logu[p];
+      } else {
+        const u4 wv = stream_block(a.seed, 0u, (uint32_t)(a.p0 + p), a.step, TAG_ACCEPT, a.pass);
+        lu = plog(u01(wv.x, wv.y));
+      }
+      if (lu < delta) {
         ok = 1;
         a.L[p] = Ls;
         a.lp[p] = lps;
@@ -600,7 +619,7 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
 
 template <int D>
 __device__ bool warp_cholesky(const double* A, int d, double scale, double ridge, double* Lout, double* colbuf,
-                              int ldo) {
+                              int ldo, bool write = true) {
   const int lane = threadIdx.x & 31;
   double a[D];
 #pragma unroll
@@ -626,7 +645,7 @@ __device__ bool warp_cholesky(const double* A, int d, double scale, double ridge
   for (int l = 0; l < D; ++l)
     if (lane == l) diag = a[l];
   const bool ok = __all_sync(0xffffffffu, lane >= d || (diag > 0.0 && isfinite(diag)));
-  if (lane < d)
+  if (write && lane < d)
 #pragma unroll
     for (int l = 0; l < D; ++l)
       if (l < d) Lout[lane * ldo + l] = l <= lane ? a[l] : 0.0;
@@ -666,6 +685,7 @@ __global__ void __launch_bounds__(32) k_chol_warp(const double* __restrict__ V, 
 // every rank computes the identical result from the gathered stats.  All
 // inputs are first staged into shared memory with independent loads (the
 // kernel is latency-bound: one block, a handful of dependent phases).
+template <int D>  // D > 0: d <= D <= 32, Cholesky by the warps redundantly (no divergent region); D = 0: block path
 __global__ void __launch_bounds__(256) k_finalize2(FinArgs f) {
   extern __shared__ double sm[];
   __shared__ int flag;
@@ -718,7 +738,7 @@ __global__ void __launch_bounds__(256) k_finalize2(FinArgs f) {
   // warp 0: h update (from the pooled acceptance) then chol((h/100) V) in registers (d <= 32);
   // warps 1..: monitor RNEs, one warp per monitor (lanes over groups / V entries)
   __shared__ int s_h;
-  __shared__ double s_col[33];
+  __shared__ double s_col[8 * 32];
   if (w == 0) {
     int h = f.ctl->h;
     if (f.mode == 1) {
@@ -784,7 +804,23 @@ __global__ void __launch_bounds__(256) k_finalize2(FinArgs f) {
   }
   const double hd = (double)s_h / 100.0;
   if (f.trace && threadIdx.x == 0) f.trace[3] = clock64();
-  if (d > 32) {  // block Cholesky (larger d)
+  if constexpr (D > 0) {
+    // every warp factors (h/100) V (identical results, no divergent region around the
+    // shuffles); warp 0 writes the padded factor (ld = round_up(d, 4))
+    const int ld = round_up(d, 4);
+    bool ok = warp_cholesky<D>(sV, d, hd, 0.0, f.Lprop, s_col + 32 * w, ld, w == 0);
+    int ridge_used = 0;
+    if (!ok) {
+      double tr = 0.0;
+      for (int i = 0; i < d; ++i) tr += sV[i * d + i];
+      ok = warp_cholesky<D>(sV, d, hd, 1e-8 * tr / (double)d, f.Lprop, s_col + 32 * w, ld, w == 0);
+      ridge_used = 1;
+    }
+    if (threadIdx.x == 0) {
+      f.ctl->chol_ridge = ridge_used;
+      if (!ok) f.ctl->err = ERR_NUMERIC;
+    }
+  } else {  // block Cholesky (larger d)
     for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) sA[idx] = hd * sV[idx];
     __syncthreads();
     bool ok = block_cholesky(sA, d, &flag);
@@ -802,12 +838,11 @@ __global__ void __launch_bounds__(256) k_finalize2(FinArgs f) {
         return;
       }
     }
+    for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) f.Lprop[(idx / d) * round_up(d, 4) + idx % d] = sA[idx];
   }
   if (f.trace && threadIdx.x == 0) f.trace[4] = clock64();
   for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) f.V[idx] = sV[idx];
   if (f.trace && threadIdx.x == 0) f.trace[5] = clock64();
-  if (d > 32)
-    for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) f.Lprop[(idx / d) * round_up(d, 4) + idx % d] = sA[idx];
   for (int i = threadIdx.x; i < d; i += blockDim.x) f.shift[i] = sbar[i];
   __syncthreads();
   if (f.host_out && threadIdx.x == 0) *f.host_out = *f.ctl;  // into mapped pinned host memory (visible at kernel end)

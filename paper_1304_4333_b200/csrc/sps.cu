@@ -141,6 +141,7 @@ struct sps_ctx {
   Ctl* dslot = nullptr;          // device view of hslot
   long long* fin_trace = nullptr;  // debug (SPS_FIN_TRACE): k_finalize2 phase clocks
   double* Zbuf[2] = {nullptr, nullptr};  // standard normals, one M step ahead (side stream)
+  double* LUbuf[2] = {nullptr, nullptr}; // plog of the ACCEPT uniforms, same schedule
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_zready[2] = {nullptr, nullptr}, ev_zfree[2] = {nullptr, nullptr};
   cudaEvent_t evs[2] = {nullptr, nullptr};
@@ -455,7 +456,8 @@ sps_status launch_normals(sps_ctx* c, uint32_t tag, uint32_t step, int slot) {
   const int64_t tasks = c->Pl * np;
   if (serial) PROF_BEGIN(c);
   k_normals<<<(unsigned)((tasks + 255) / 256), 256, 0, st>>>(c->Pl, c->p0, np, round_up(c->d, 4), c->cfg.seed,
-                                                                 step, tag, (uint32_t)c->cfg.pass, c->Zbuf[slot]);
+                                                                 step, tag, (uint32_t)c->cfg.pass, c->Zbuf[slot],
+                                                                 tag == TAG_PROPOSAL ? c->LUbuf[slot] : nullptr);
   CHECK_LAUNCH(c);
   if (serial) PROF_END(c, CAT_OTHER);
   CU(c, cudaEventRecord(c->ev_zready[slot], st));
@@ -488,7 +490,7 @@ sps_status launch_draw(sps_ctx* c, int slot, const double* base, const double* L
   if (d <= 32) {  // register-blocked DMMA proposal
     const int KK = (d + 3) / 4, KPr = 4 * KK, NPr = 8 * ((KPr + 7) / 8);
     const size_t sm = (size_t)(2 * PR_TILE * KPr + KPr + 2 * NPr * KPr + PR_TILE * d) * sizeof(double);
-    const unsigned grid = (unsigned)std::min<int64_t>(ntl, (int64_t)num_sms() * 2);
+    const unsigned grid = (unsigned)ntl;  // one tile per block; 2 blocks per SM overlap their latencies
     switch (KK) {
       case 1: k_propose_rb<1><<<grid, 256, sm, c->stream>>>(a); break;
       case 2: k_propose_rb<2><<<grid, 256, sm, c->stream>>>(a); break;
@@ -508,13 +510,13 @@ sps_status launch_draw(sps_ctx* c, int slot, const double* base, const double* L
   }
   CHECK_LAUNCH(c);
   PROF_END(c, CAT_PROPOSE);
-  CU(c, cudaEventRecord(c->ev_zfree[slot], c->stream));
   return SPS_OK;
 }
 
 // K9 + K6 (decide = true) or K6 only, then the deterministic reduction into this
 // rank's stats slice and the gather across ranks -> `gath`.
-sps_status accept_moments(sps_ctx* c, bool decide, int nchunks, double temper, uint32_t step, const int* stop) {
+sps_status accept_moments(sps_ctx* c, bool decide, int nchunks, double temper, uint32_t step, const int* stop,
+                          const double* logu = nullptr) {
   AccArgs a{};
   a.theta = c->theta;
   a.L = c->L;
@@ -523,6 +525,7 @@ sps_status accept_moments(sps_ctx* c, bool decide, int nchunks, double temper, u
   a.part = c->part;
   a.lp_s = c->lp_s;
   a.shift = c->shift;
+  a.logu = logu;
   a.bpart = c->bpart;
   a.ctl = c->ctl;
   a.stop = stop;
@@ -599,21 +602,18 @@ sps_status finalize(sps_ctx* c, int mode, bool allow_stop, const int* stop, int 
                                 (size_t)c->J * c->d) * sizeof(double);
   if (smem > 200 * 1024) return fail(c, SPS_E_CONFIG, "J x d too large for the finalize stage (%zu bytes)", smem);
   PROF_BEGIN(c);
-  k_finalize2<<<1, 256, smem, c->stream>>>(f);
-  CHECK_LAUNCH(c);
-  if (c->d <= 32) {  // chol((h/100) V) by one warp, after h is known
-    switch ((c->d + 3) / 4) {
-      case 1: k_chol_warp<4><<<1, 32, 0, c->stream>>>(c->V, c->d, c->ctl, c->Lprop, stop); break;
-      case 2: k_chol_warp<8><<<1, 32, 0, c->stream>>>(c->V, c->d, c->ctl, c->Lprop, stop); break;
-      case 3: k_chol_warp<12><<<1, 32, 0, c->stream>>>(c->V, c->d, c->ctl, c->Lprop, stop); break;
-      case 4: k_chol_warp<16><<<1, 32, 0, c->stream>>>(c->V, c->d, c->ctl, c->Lprop, stop); break;
-      case 5: k_chol_warp<20><<<1, 32, 0, c->stream>>>(c->V, c->d, c->ctl, c->Lprop, stop); break;
-      case 6: k_chol_warp<24><<<1, 32, 0, c->stream>>>(c->V, c->d, c->ctl, c->Lprop, stop); break;
-      case 7: k_chol_warp<28><<<1, 32, 0, c->stream>>>(c->V, c->d, c->ctl, c->Lprop, stop); break;
-      default: k_chol_warp<32><<<1, 32, 0, c->stream>>>(c->V, c->d, c->ctl, c->Lprop, stop); break;
-    }
-    CHECK_LAUNCH(c);
+  switch (c->d <= 32 ? (c->d + 3) / 4 : 0) {
+    case 1: k_finalize2<4><<<1, 256, smem, c->stream>>>(f); break;
+    case 2: k_finalize2<8><<<1, 256, smem, c->stream>>>(f); break;
+    case 3: k_finalize2<12><<<1, 256, smem, c->stream>>>(f); break;
+    case 4: k_finalize2<16><<<1, 256, smem, c->stream>>>(f); break;
+    case 5: k_finalize2<20><<<1, 256, smem, c->stream>>>(f); break;
+    case 6: k_finalize2<24><<<1, 256, smem, c->stream>>>(f); break;
+    case 7: k_finalize2<28><<<1, 256, smem, c->stream>>>(f); break;
+    case 8: k_finalize2<32><<<1, 256, smem, c->stream>>>(f); break;
+    default: k_finalize2<0><<<1, 256, smem, c->stream>>>(f); break;
   }
+  CHECK_LAUNCH(c);
   PROF_END(c, CAT_FINALIZE);
   return SPS_OK;
 }
@@ -639,6 +639,8 @@ void free_ctx(sps_ctx* c) {
     c->gath = c->essgath = c->grp_ms_gath = c->Lj_gath = c->pw_gath = c->mx_gath = nullptr;
   }
   for (double* z : c->Zbuf)
+    if (z) cudaFree(z);
+  for (double* z : c->LUbuf)
     if (z) cudaFree(z);
   if (c->aux) cudaStreamSynchronize(c->aux);
   for (int q = 0; q < 2; ++q) {
@@ -836,6 +838,8 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
     const size_t zn = (size_t)(Pl + PR_TILE) * round_up(d, 4);
     TRY(dalloc(c, &c->Zbuf[0], zn));
     TRY(dalloc(c, &c->Zbuf[1], zn));
+    TRY(dalloc(c, &c->LUbuf[0], (size_t)Pl));
+    TRY(dalloc(c, &c->LUbuf[1], (size_t)Pl));
     CU(c, cudaMemsetAsync(c->Zbuf[0], 0, zn * sizeof(double), c->stream));
     CU(c, cudaMemsetAsync(c->Zbuf[1], 0, zn * sizeof(double), c->stream));
     CU(c, cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
@@ -930,7 +934,7 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
                            (const void*)k_propose<true>, (const void*)k_propose<false>, (const void*)k_accept_mom,
                            (const void*)k_accept_mom_rb<1>, (const void*)k_accept_mom_rb<2>,
                            (const void*)k_accept_mom_rb<3>, (const void*)k_accept_mom_rb<4>, (const void*)k_mom_reduce,
-                           (const void*)k_finalize2, (const void*)k_chol_warp<4>, (const void*)k_chol_warp<8>,
+                           (const void*)k_finalize2<0>, (const void*)k_chol_warp<4>, (const void*)k_chol_warp<8>,
                            (const void*)k_chol_warp<12>, (const void*)k_chol_warp<16>, (const void*)k_chol_warp<20>,
                            (const void*)k_chol_warp<24>, (const void*)k_chol_warp<28>, (const void*)k_chol_warp<32>,
                            (const void*)k_normals};
@@ -939,7 +943,15 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
     }
     CU(c, cudaFuncSetAttribute(k_propose<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(c, cudaFuncSetAttribute(k_propose<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    CU(c, cudaFuncSetAttribute(k_finalize2, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_finalize2<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_finalize2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_finalize2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_finalize2<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_finalize2<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_finalize2<20>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_finalize2<24>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_finalize2<28>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_finalize2<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(c, cudaFuncSetAttribute(k_accept_mom, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(c, cudaFuncSetAttribute(k_accept_mom_rb<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(c, cudaFuncSetAttribute(k_accept_mom_rb<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
@@ -1006,6 +1018,7 @@ sps_status sps_reset(sps_ctx* c, uint64_t seed, int32_t pass) {
   // Algorithm 1 step 1: theta_jn ~iid p(theta)
   TRY(launch_normals(c, TAG_INIT, 0u, 0));
   TRY(launch_draw(c, 0, nullptr, c->LpriorP, c->theta, c->lp, nullptr));
+  CU(c, cudaEventRecord(c->ev_zfree[0], c->stream));
   if (c->cfg.tempering == SPS_POWER_TEMPERING) {
     int nch = 1;
     TRY(launch_loglik(c, c->theta, c->d, Pl, 0, c->n, c->part, c->max_chunks, &nch));
@@ -1230,11 +1243,13 @@ static sps_status launch_mstep(sps_ctx* c, uint32_t step, int slot, bool allow_s
   const int t1 = power ? c->n : c->t;
   const double temper = power ? c->phi : 1.0;
   const int* stop = &c->ctl->stop;
-  TRY(launch_draw(c, (int)(step & 1u), c->theta, c->Lprop, c->theta_s, c->lp_s, stop));
+  const int zs = (int)(step & 1u);
+  TRY(launch_draw(c, zs, c->theta, c->Lprop, c->theta_s, c->lp_s, stop));
   TRY(launch_normals(c, TAG_PROPOSAL, step + 1u, (int)((step + 1u) & 1u)));  // next step's normals, overlapped
   int nch = 1;
   TRY(launch_loglik(c, c->theta_s, c->d, c->Pl, 0, t1, c->part, c->max_chunks, &nch, stop));
-  TRY(accept_moments(c, true, nch, temper, step, stop));
+  TRY(accept_moments(c, true, nch, temper, step, stop, c->LUbuf[zs]));
+  CU(c, cudaEventRecord(c->ev_zfree[zs], c->stream));  // Zbuf / LUbuf[zs] consumed
   TRY(finalize(c, 1, allow_stop, stop, slot));
   CU(c, cudaEventRecord(c->evs[slot], c->stream));
   return SPS_OK;
