@@ -177,6 +177,7 @@ struct FinArgs {
   double* rne_out;     // nmon RNEs (may be null)
   Ctl* host_out;       // mapped pinned host slot for the control block (may be null)
   long long* trace;    // debug: clock64 at phase boundaries (may be null)
+  int stage_S;         // group sums staged in shared memory (else read from gath)
 };
 
 // Reported functional moments (K11) from the gathered

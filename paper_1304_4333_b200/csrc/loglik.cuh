@@ -122,6 +122,7 @@ struct LLArgs {
   int32_t t0, t1, chunk;
   int32_t k;           // covariates; theta block stride (K template >= k, zero padded)
   const int* stop;     // speculative M-step launches: return if set
+  int32_t sub;         // DMMA kernel: observations per shared-memory sub-chunk (0: whole chunk)
 };
 
 // max(s, 0) and min(|s|, 708) with integer ops on the ALU pipe (sm_100a has no
@@ -409,15 +410,8 @@ __global__ void __launch_bounds__(128, MINB) k_loglik_bin_mma(LLArgs a) {
   double* sX = smem + 256;  // (chunk rounded up to 16) x KP
   const int c0 = a.t0 + blockIdx.y * a.chunk;
   const int c1 = min(c0 + a.chunk, a.t1);
-  const int nobs = max(c1 - c0, 0);
-  const int nobs16 = (nobs + 15) & ~15;
+  const int ntot = max(c1 - c0, 0);
   for (int i = threadIdx.x; i < TAB; i += blockDim.x) sT[i] = TAB == 256 ? c_exp2tab256[i] : c_exp2tab[i];
-  {
-    const double2* src = reinterpret_cast<const double2*>(a.X + (int64_t)c0 * KP);
-    double2* dst = reinterpret_cast<double2*>(sX);
-    const int nv = nobs * KP / 2, nv16 = nobs16 * KP / 2;
-    for (int i = threadIdx.x; i < nv16; i += blockDim.x) dst[i] = i < nv ? __ldg(src + i) : make_double2(0.0, 0.0);
-  }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, ar = lane >> 2, ac = lane & 3;
   const int64_t pw = ((int64_t)blockIdx.x * 4 + w) * (NTW * 8);  // first particle of this warp
   double b[NTW][KKD > 0 ? KKD : 1];
@@ -451,6 +445,18 @@ __global__ void __launch_bounds__(128, MINB) k_loglik_bin_mma(LLArgs a) {
       E[nt][e] = 0;
     }
   int nit = 0;
+  const int sub = a.sub > 0 ? a.sub : ntot;  // X sub-chunk resident in shared memory (multiple of 16)
+  for (int cs = 0; cs < ntot; cs += sub) {
+  const int nobs = min(sub, ntot - cs);
+  const int nobs16 = (nobs + 15) & ~15;
+  __syncthreads();  // previous sub-chunk consumed
+  {
+    const double2* src = reinterpret_cast<const double2*>(a.X + (int64_t)(c0 + cs) * KP);
+    double2* dst = reinterpret_cast<double2*>(sX);
+    const int nv = nobs * KP / 2, nv16 = nobs16 * KP / 2;
+    for (int i = threadIdx.x; i < nv16; i += blockDim.x) dst[i] = i < nv ? __ldg(src + i) : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
   for (int t0 = 0; t0 < nobs; t0 += 8 * H) {
     double acc[H][NTW][2];
 #pragma unroll
@@ -529,6 +535,7 @@ __global__ void __launch_bounds__(128, MINB) k_loglik_bin_mma(LLArgs a) {
       }
     }
   }
+  }  // sub-chunks
   // combine the 8 lanes (ar = 0..7) of each particle column: sums of M and E, product of P
 #pragma unroll
   for (int nt = 0; nt < NTW; ++nt)

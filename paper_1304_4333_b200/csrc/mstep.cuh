@@ -69,9 +69,9 @@ __global__ void __launch_bounds__(256) k_propose(DrawArgs a) {
   double* Ds = Zs + PR_TILE * KP;   // PR_TILE x KP  (theta* - mu)
   double* qp = Ds + PR_TILE * KP;   // PR_TILE x NT  quad partials
   double* smu = qp + PR_TILE * NT;  // KP
-  double* sL = smu + KP;            // NP x KP (STAGE)
-  double* sS = sL + NP * KP;        // NP x KP (STAGE)
-  double* Bs = sS + (STAGE ? NP * KP : 0);  // PR_TILE x d base rows (theta)
+  double* sL = smu + KP;                    // NP x KP (STAGE)
+  double* sS = sL + NP * KP;                // NP x KP (STAGE)
+  double* Bs = STAGE ? sS + NP * KP : sL;   // PR_TILE x d base rows (theta)
   // mu; Lz and Sinv arrive in the padded DMMA layout (NP x KP, zeros outside d x d) -> bulk copies
   for (int i = threadIdx.x; i < KP; i += blockDim.x) smu[i] = i < d ? a.mu[i] : 0.0;
   auto Lf = [&](int i, int j) -> double { return STAGE ? sL[i * KP + j] : __ldg(a.Lz + i * KP + j); };
@@ -695,20 +695,23 @@ __global__ void __launch_bounds__(256) k_finalize2(FinArgs f) {
   const int gs_len = f.Jl * d;
   double* sV = sm;                 // d x d
   double* sbar = sV + d * d;       // d
-  double* sA = sbar + d;           // d x d
+  double* sA = sbar + d;           // d x d (Cholesky work of the block path; also the summed M)
   double* sg = sA + d * d;         // nmon x J group means + nmon RNEs
   double* sshift = sg + f.nmon * J + f.nmon;  // d
   double* smon = sshift + d;       // nmon x d
-  double* sS = smon + f.nmon * d;  // J x d group sums (rank order == group order)
-  double* sM = sS + (int64_t)J * d;  // d x d summed second moment
+  double* sS = smon + f.nmon * d;  // J x d group sums (rank order == group order), when staged
+  double* sM = sA;                 // consumed (into V) before sA is written
   const double P = (double)J * (double)f.N;
-  if (f.trace && threadIdx.x == 0) f.trace[0] = clock64();
+  auto S = [&](int j, int i) -> double {
+    return f.stage_S ? sS[j * d + i] : f.gath[(int64_t)(j / f.Jl) * f.slice_len + (int64_t)(j % f.Jl) * d + i];
+  };
   // ---- stage (one cp.async round)
   for (int i = threadIdx.x; i < d; i += blockDim.x) cp_async8(sshift + i, f.shift + i);
   for (int i = threadIdx.x; i < f.nmon * d; i += blockDim.x) cp_async8(smon + i, f.mon + i);
-  for (int r = 0; r < f.G; ++r)
-    for (int off = threadIdx.x; off < gs_len; off += blockDim.x)
-      cp_async8(sS + (int64_t)r * gs_len + off, f.gath + (int64_t)r * f.slice_len + off);
+  if (f.stage_S)
+    for (int r = 0; r < f.G; ++r)
+      for (int off = threadIdx.x; off < gs_len; off += blockDim.x)
+        cp_async8(sS + (int64_t)r * gs_len + off, f.gath + (int64_t)r * f.slice_len + off);
   if (f.G == 1)
     for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) cp_async8(sM + idx, f.gath + gs_len + idx);
   cp_async_wait_all();
@@ -723,7 +726,7 @@ __global__ void __launch_bounds__(256) k_finalize2(FinArgs f) {
   // ---- theta-bar: warp per coordinate, lanes over groups, fixed shuffle tree
   for (int i = w; i < d; i += nw) {
     double s = 0.0;
-    for (int j = lane; j < J; j += 32) s += sS[j * d + i];
+    for (int j = lane; j < J; j += 32) s += S(j, i);
     s = warp_sum(s);
     if (lane == 0) sbar[i] = s / P;
   }
@@ -760,14 +763,13 @@ __global__ void __launch_bounds__(256) k_finalize2(FinArgs f) {
       const double* av = smon + m * d;
       double gp = 0.0;
       for (int j = lane; j < J; j += 32) {
-        const double* Sj = sS + j * d;
         double s0 = 0.0, s1 = 0.0;
         int i = 0;
         for (; i + 2 <= d; i += 2) {
-          s0 = fma(av[i], Sj[i], s0);
-          s1 = fma(av[i + 1], Sj[i + 1], s1);
+          s0 = fma(av[i], S(j, i), s0);
+          s1 = fma(av[i + 1], S(j, i + 1), s1);
         }
-        if (i < d) s0 = fma(av[i], Sj[i], s0);
+        if (i < d) s0 = fma(av[i], S(j, i), s0);
         const double g = (s0 + s1) / (double)f.N;
         sg[m * J + j] = g;
         gp += g;

@@ -105,6 +105,8 @@ using LLKernel = void (*)(LLArgs);
 struct LLChoice_t {
   LLKernel fn = nullptr;
   int KT = 0, PPT = 1;
+  int ppb = 0;          // particles per block (0: LL_THREADS * PPT)
+  bool streams = false; // streams X through smem in sub-chunks (any chunk length)
 };
 
 struct sps_ctx {
@@ -149,7 +151,7 @@ struct sps_ctx {
   int ll_regs = 0;
   struct Plan {
     int64_t P = -1;
-    int range = -1, max_chunks = -1, S = 1, chunk = 0;
+    int range = -1, max_chunks = -1, S = 1, chunk = 0, sub = 0;
     size_t smem = 0;
   } plans[8];
   int plan_next = 0;
@@ -337,7 +339,7 @@ bool choose_ll(int k, int C, LLChoice* o) {
     switch (k) {
 #define MMA_CASE(K_, KKD_, REM_)                                       \
   case K_:                                                             \
-    *o = {k_loglik_bin_mma<KKD_, REM_, 4>, 4 * KKD_ + (REM_ ? 4 : 0), 1}; \
+    *o = {k_loglik_bin_mma<KKD_, REM_, 4>, 4 * KKD_ + (REM_ ? 4 : 0), 1, 128, true}; \
     return true;
       MMA_CASE(1, 0, 1) MMA_CASE(2, 0, 2) MMA_CASE(3, 1, 0) MMA_CASE(4, 1, 0) MMA_CASE(5, 1, 1) MMA_CASE(6, 1, 2)
       MMA_CASE(7, 2, 0) MMA_CASE(8, 2, 0) MMA_CASE(9, 2, 1) MMA_CASE(10, 2, 2) MMA_CASE(11, 3, 0) MMA_CASE(12, 3, 0)
@@ -346,6 +348,19 @@ bool choose_ll(int k, int C, LLChoice* o) {
       MMA_CASE(23, 6, 0) MMA_CASE(24, 6, 0) MMA_CASE(25, 6, 1) MMA_CASE(26, 6, 2) MMA_CASE(27, 7, 0)
       MMA_CASE(28, 7, 0) MMA_CASE(29, 7, 1) MMA_CASE(30, 7, 2) MMA_CASE(31, 8, 0) MMA_CASE(32, 8, 0)
 #undef MMA_CASE
+      default: break;
+    }
+  }
+  if (cm1 == 1 && k <= 128 && !force_dfma) {  // wide: 2 n-tiles per warp (64 particles per block), k padded to 4
+    switch ((k + 3) / 4) {
+#define MMA_W(KK_)                                   \
+  case KK_:                                          \
+    *o = {k_loglik_bin_mma<KK_, 0, 2>, 4 * KK_, 1, 64, true}; \
+    return true;
+      MMA_W(9) MMA_W(10) MMA_W(11) MMA_W(12) MMA_W(13) MMA_W(14) MMA_W(15) MMA_W(16) MMA_W(17) MMA_W(18)
+      MMA_W(19) MMA_W(20) MMA_W(21) MMA_W(22) MMA_W(23) MMA_W(24) MMA_W(25) MMA_W(26) MMA_W(27) MMA_W(28)
+      MMA_W(29) MMA_W(30) MMA_W(31) MMA_W(32)
+#undef MMA_W
       default: break;
     }
   }
@@ -391,7 +406,8 @@ sps_status launch_loglik(sps_ctx* c, const double* theta, int64_t ldt, int64_t P
     *nchunks_out = 1;
     return SPS_OK;
   }
-  const int64_t tiles = (P + LL_THREADS * ch.PPT - 1) / (LL_THREADS * ch.PPT);
+  const int ppb = ch.ppb > 0 ? ch.ppb : LL_THREADS * ch.PPT;
+  const int64_t tiles = (P + ppb - 1) / ppb;
   const size_t row_bytes = (size_t)c->ldx * 8 + (c->C > 2 ? 4 : 0);
   sps_ctx::Plan* pl = nullptr;
   for (auto& q : c->plans)
@@ -400,8 +416,9 @@ sps_status launch_loglik(sps_ctx* c, const double* theta, int64_t ldt, int64_t P
     pl = &c->plans[c->plan_next];
     c->plan_next = (c->plan_next + 1) % 8;
     const int smem_budget = 100 * 1024;
-    const int chunk_cap = std::max(1, (int)((smem_budget - 64 * 8 - 64) / row_bytes));
-    const int S_min = std::max(1, (range + chunk_cap - 1) / chunk_cap);
+    const int chunk_cap = std::max(1, (int)((smem_budget - 256 * 8 - 64) / row_bytes) - 16);
+    const int sub_cap = std::max(16, chunk_cap / 16 * 16);  // streaming kernels: sub-chunk in smem
+    const int S_min = ch.streams ? 1 : std::max(1, (range + chunk_cap - 1) / chunk_cap);
     const int S_hi = std::min(max_chunks, std::max(S_min, std::min(S_min + 24, range / 8)));
     const int warp_regs = ((c->ll_regs * 32 + 255) / 256) * 256;
     const int by_regs = 65536 / ((LL_THREADS / 32) * warp_regs);
@@ -412,7 +429,8 @@ sps_status launch_loglik(sps_ctx* c, const double* theta, int64_t ldt, int64_t P
     for (int S = S_min; S <= S_hi; ++S) {
       const int chunk = (range + S - 1) / S;
       const int Se = (range + chunk - 1) / chunk;
-      const size_t smem = 256 * 8 + (size_t)(chunk + 16) * row_bytes + 16;
+      const int rows = ch.streams ? std::min(chunk, sub_cap) : chunk;
+      const size_t smem = 256 * 8 + (size_t)(rows + 16) * row_bytes + 16;
       const int by_smem = (int)(233472 / (smem + 1024));
       const int occ = std::max(1, std::min(std::min(by_regs, by_smem), 16));
       const double slots = (double)num_sms() * occ;
@@ -429,12 +447,15 @@ sps_status launch_loglik(sps_ctx* c, const double* theta, int64_t ldt, int64_t P
     pl->max_chunks = max_chunks;
     pl->chunk = chunk;
     pl->S = (range + chunk - 1) / chunk;
-    pl->smem = 256 * 8 + (size_t)(chunk + 16) * c->ldx * 8 + (c->C > 2 ? (size_t)chunk * 4 : 0);
+    pl->sub = ch.streams ? std::min(((chunk + 15) / 16) * 16, sub_cap) : 0;
+    const int rows = ch.streams ? pl->sub : chunk;
+    pl->smem = 256 * 8 + (size_t)(rows + 16) * c->ldx * 8 + (c->C > 2 ? (size_t)chunk * 4 : 0);
     if (pl->S > max_chunks) return fail(c, SPS_E_CONFIG, "observation range too long for the chunk buffer");
   }
   LLArgs a{c->Xs, c->y, theta, part, ldt, P, t0, t1, pl->chunk};
   a.k = c->k;
   a.stop = stop;
+  a.sub = pl->sub;
   dim3 grid((unsigned)tiles, (unsigned)pl->S);
   PROF_BEGIN(c);
   ch.fn<<<grid, LL_THREADS, pl->smem, c->stream>>>(a);
@@ -598,9 +619,12 @@ sps_status finalize(sps_ctx* c, int mode, bool allow_stop, const int* stop, int 
   f.ctl = c->ctl;
   f.stop_in = stop;
   f.rne_out = c->rne;
-  const size_t smem = (size_t)(3 * c->d * c->d + 2 * c->d + c->nmon * c->J + c->nmon + c->nmon * c->d +
-                                (size_t)c->J * c->d) * sizeof(double);
-  if (smem > 200 * 1024) return fail(c, SPS_E_CONFIG, "J x d too large for the finalize stage (%zu bytes)", smem);
+  const size_t base_sm =
+      (size_t)(2 * c->d * c->d + 2 * c->d + c->nmon * c->J + c->nmon + c->nmon * c->d) * sizeof(double);
+  const size_t s_sm = (size_t)c->J * c->d * sizeof(double);
+  f.stage_S = base_sm + s_sm <= 200 * 1024 ? 1 : 0;
+  const size_t smem = base_sm + (f.stage_S ? s_sm : 0);
+  if (smem > 200 * 1024) return fail(c, SPS_E_CONFIG, "d = %d too large for the finalize kernel", c->d);
   PROF_BEGIN(c);
   switch (c->d <= 32 ? (c->d + 3) / 4 : 0) {
     case 1: k_finalize2<4><<<1, 256, smem, c->stream>>>(f); break;

@@ -1,0 +1,83 @@
+"""Parity at BASELINE.json's full sizes (the other configs are parity cases):
+configs[3] (n = 1e5, k = 100; one GPU's shard of 1024 x 1024 particles) and the
+configs[4] particle sweep (2^14 .. 2^22 at the configs[1] shape) on sampled
+particles the oracle recomputes one by one; the large-d path of the whole
+engine (d = 100) against the oracle; configs[2] (multinomial C = 4) end to end."""
+import numpy as np
+import pytest
+
+import sps_synth
+
+pytestmark = pytest.mark.gpu
+LL_RTOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def sps():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_1304_4333_b200 as pkg
+
+    pkg.build()
+    return pkg
+
+
+def _sampled(sps, orc, X, y, C, theta, nsample, seed=0):
+    import torch
+
+    n, k = X.shape
+    d = k * (C - 1)
+    s = sps.Sps(X, y, np.zeros(d), np.eye(d), J=2, N=4, seed=1, C_=C)
+    got = s.loglik_tensor(torch.tensor(theta, device="cuda")).cpu().numpy()
+    s.close()
+    idx = np.random.default_rng(seed).choice(theta.shape[0], nsample, replace=False)
+    want = orc.loglik_range(theta[idx], X, y, C)
+    err = np.abs(got[idx] - want) / np.abs(want)
+    assert np.all(err <= LL_RTOL), err.max()
+    assert np.all(np.isfinite(got))
+
+
+def test_loglik_cfg4_shard_sampled(sps, orc):
+    X, y = sps_synth.config_data("cfg4")  # n = 1e5, k = 100
+    P = 1024 * 1024 // 8  # one GPU's shard of configs[3]
+    theta = sps_synth.particles(P, 100, scale=0.05, seed=4)
+    _sampled(sps, orc, X, y, 2, theta, 16)
+
+
+@pytest.mark.parametrize("logP", [14, 20, 22])
+def test_loglik_cfg5_sweep_sampled(sps, orc, logP):
+    X, y = sps_synth.config_data("cfg2")
+    theta = sps_synth.particles(1 << logP, 25, scale=0.3, seed=logP)
+    _sampled(sps, orc, X, y, 2, theta, 64, seed=logP)
+
+
+def test_run_parity_large_d(sps, orc):
+    """d = 100: generic (non register-blocked) proposal / moments / block Cholesky paths."""
+    X, y = sps_synth.make_data(200, 100, 2, 30, (0.0,), 0.15, seed=5)
+    cov = orc.g_prior(X, 2, 0.25)
+    o = orc.run(X, y, 2, 4, 128, seed=2, prior_mean=np.zeros(100), prior_cov=cov)
+    s = sps.Sps(X, y, np.zeros(100), cov, J=4, N=128, seed=2)
+    g = s.run()
+    s.close()
+    assert o["status"] == 0 and g["L"] == o["L"]
+    assert np.array_equal(g["t_cycle"], o["t_cycle"]) and np.array_equal(g["R_cycle"], o["R_cycle"])
+    assert abs(g["logml"] - o["logml"]) <= 1e-6
+    assert np.all(np.abs(g["mean"] - o["mean"]) <= 1e-6)
+
+
+def test_cfg3_multinomial_full_run(sps, orc):
+    """configs[2] end to end on one GPU: C = 4, k = 10, n = 5000, J = 128 x N = 1024."""
+    X, y = sps_synth.config_data("cfg3")
+    cov = sps.g_prior(X, 4, 1.0)
+    s = sps.Sps(X, y, np.zeros(30), cov, J=128, N=1024, seed=1, C_=4)
+    r = s.run()
+    th, L, lp = s.particles()
+    s.close()
+    assert r["status"] == 0 and r["t_cycle"][-1] == 5000
+    assert np.isfinite(r["logml"]) and r["min_rne"][-1] >= 0.9
+    # cached log-likelihoods of the final particles are exact: recompute a sample with the oracle
+    idx = np.random.default_rng(0).choice(th.shape[0], 8, replace=False)
+    want = orc.loglik_range(th[idx], X, y, 4)
+    assert np.all(np.abs(L[idx] - want) <= 1e-9 * np.abs(want))
