@@ -147,6 +147,13 @@ __device__ __forceinline__ void normal_pair(uint64_t seed, uint32_t i, uint32_t 
   *z1 = __dmul_rn(r, s);
 }
 
+// Debug phase clock (ns); callers place it after a __syncthreads.
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) : : "memory");
+  return t;
+}
+
 // ----------------------------------------------------------------- async copies
 // cp.async (LDGSTS) of 8 bytes global -> shared; all issued copies of a thread
 // are waited by cp_async_wait_all (one latency round for a whole staging phase).

@@ -176,7 +176,8 @@ struct FinArgs {
   const int* stop_in;  // skip if already stopped (speculative launches)
   double* rne_out;     // nmon RNEs (may be null)
   Ctl* host_out;       // mapped pinned host slot for the control block (may be null)
-  long long* trace;    // debug: clock64 at phase boundaries (may be null)
+  unsigned* ticket;    // k_mom_reduce: arrival counter; the last block runs the finalize (null: separate launch)
+  unsigned long long* trace;  // debug (SPS_TRACE): %globaltimer at phase boundaries, or null
   int stage_S;         // group sums staged in shared memory (else read from gath)
 };
 

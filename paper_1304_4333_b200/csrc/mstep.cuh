@@ -547,14 +547,309 @@ __global__ void __launch_bounds__(256) k_accept_mom_rb(AccArgs a) {
   if (threadIdx.x == 0) out[W - 1] = (double)nacc;
 }
 
+// 1/sqrt(x) without a slow-path call: MUFU approximation + 2 Newton steps
+// (relative error ~1 ulp); non-positive / non-finite x give non-finite results.
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+  y = fma(y, fma(-h * y, y, 0.5), y);
+  y = fma(y, fma(-h * y, y, 0.5), y);
+  return y;
+}
+
+// Cholesky (lower) of the d x d SPD matrix held in shared memory as Ap (D x D,
+// identity-padded beyond d; D = round_up(d, 4) <= 32) by ONE warp, rows in
+// registers (lane i holds row i), columns fully unrolled: per column a 64-bit
+// shuffle of the pivot, rsqrt + 2 Newton steps, then the column through shared
+// memory for the trailing update (tools/chol_bench3.cu: ~250 cycles per column,
+// ~3x faster than run-time-loop shared-memory variants, whose row updates
+// serialize on shared-memory ordering).  One out-of-line copy per D serves
+// both factorization attempts (code size: this runs once per M step from a
+// cold instruction cache).  Writes the lower factor with row stride ldo >= D
+// (zeros above the diagonal and in the padding columns) for rows < d.
+// Returns false if a pivot is not positive and finite.
+template <int D>
+__device__ __noinline__ bool warp_cholesky(const double* Ap, double* Lout, int ldo, int d) {
+  __shared__ double colbuf[32];
+  const int lane = threadIdx.x & 31, row = lane < D ? lane : D - 1;
+  double a[D];
+#pragma unroll
+  for (int l = 0; l < D; ++l) a[l] = Ap[row * D + l];
+  bool ok = true;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    const double piv = __shfl_sync(0xffffffffu, a[j], j);
+    ok = ok && piv > 0.0 && isfinite(piv);
+    const double r = rsqrt_nr(piv);
+    const double lij = lane >= j ? a[j] * r : 0.0;  // lane j: sqrt(pivot)
+    a[j] = lij;
+    if (j + 1 < D) {
+      colbuf[lane] = lij;
+      __syncwarp();
+#pragma unroll
+      for (int l = j + 1; l < D; ++l) a[l] = fma(-lij, colbuf[l], a[l]);
+      __syncwarp();
+    }
+  }
+  if (lane < d)
+#pragma unroll
+    for (int l = 0; l < D; ++l) Lout[lane * ldo + l] = l <= lane ? a[l] : 0.0;
+  return ok;
+}
+
+__device__ bool warp_cholesky_d(const double* Ap, double* Lout, int ldo, int d) {
+  switch ((d + 3) >> 2) {
+    case 1: return warp_cholesky<4>(Ap, Lout, ldo, d);
+    case 2: return warp_cholesky<8>(Ap, Lout, ldo, d);
+    case 3: return warp_cholesky<12>(Ap, Lout, ldo, d);
+    case 4: return warp_cholesky<16>(Ap, Lout, ldo, d);
+    case 5: return warp_cholesky<20>(Ap, Lout, ldo, d);
+    case 6: return warp_cholesky<24>(Ap, Lout, ldo, d);
+    case 7: return warp_cholesky<28>(Ap, Lout, ldo, d);
+    default: return warp_cholesky<32>(Ap, Lout, ldo, d);
+  }
+}
+
+// n doubles global -> shared through L2 (ld.global.cg: coherent with the other
+// blocks' writes of the same kernel), 4 independent loads in flight per thread.
+__device__ __forceinline__ void stage_cg(double* dst, const double* src, int n) {
+  for (int i0 = threadIdx.x; i0 < n; i0 += 4 * blockDim.x) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * blockDim.x;
+      v[u] = i < n ? __ldcg(src + i) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i < n) dst[i] = v[u];
+    }
+  }
+}
+
+// Group sum S_j[i] read from the gathered slices (when J x d is too large to stage).
+__device__ __noinline__ double group_sum_global(const FinArgs& f, int j, int i) {
+  return __ldcg(f.gath + (int64_t)(j / f.Jl) * f.slice_len + (int64_t)(j % f.Jl) * f.d + i);
+}
+
+// chol((h/100) V) by the whole block for d > 32 (sA: d x d, (h/100) V), one
+// ridge retry (R13); factor -> f.Lprop (row stride ldp).
+__device__ __noinline__ void block_factor(const FinArgs& f, double* sA, const double* sV, double hd, int ldp, int* s_flag) {
+  const int d = f.d, lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  bool ok = block_cholesky(sA, d, s_flag);
+  if (threadIdx.x == 0) f.ctl->chol_ridge = ok ? 0 : 1;
+  if (!ok) {
+    double tr = 0.0;
+    for (int i = 0; i < d; ++i) tr += sV[i * d + i];
+    const double ridge = 1e-8 * tr / (double)d;
+    for (int i = w; i < d; i += nw)
+      for (int l = lane; l < d; l += 32) sA[i * d + l] = hd * (sV[i * d + l] + (i == l ? ridge : 0.0));
+    __syncthreads();
+    ok = block_cholesky(sA, d, s_flag);
+    if (!ok) {
+      if (threadIdx.x == 0) f.ctl->err = ERR_NUMERIC;
+      return;
+    }
+  }
+  for (int i = w; i < d; i += nw)
+    for (int l = lane; l < d; l += 32) f.Lprop[i * ldp + l] = sA[i * d + l];
+}
+
+// Dynamic shared memory of finalize_body (doubles).
+__host__ __device__ inline int64_t fin_smem_doubles(int d, int J, int nmon, bool stage_S) {
+  const int D = (d + 3) / 4 * 4;
+  return (int64_t)2 * d * d + (d > 32 ? 0 : (int64_t)D * D) + 2 * d + (int64_t)nmon * d + (int64_t)nmon * J + nmon +
+         (stage_S ? (int64_t)J * d : 0);
+}
+
+// ---------------------------------------------------------------- K7
+// theta-bar, pooled V (R11), h update (R6), monitor RNEs + stop flag (R12,
+// R14), chol((h/100) V) with one ridge retry (R13), new shift, from the
+// gathered stats [Jl x d group sums | d x d second moment | accepts | error]
+// of the G ranks (rank order == group order).  One block of 256 threads; every
+// rank computes the identical result.  Latency-bound: one staging round, then
+// warp 0 factors while warps 1.. compute the monitor RNEs (d <= 32).
+__device__ void finalize_body(const FinArgs& f, double* sm) {
+  const int d = f.d, J = f.J, dd = d * d, lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int gs_len = f.Jl * d, D = round_up(d, 4), ldc = d > 32 ? d : D;
+  const double P = (double)J * (double)f.N;
+  double* sM = sm;                    // d x d second moment about the old shift
+  double* sV = sM + dd;               // d x d pooled covariance
+  // (h/100) V: d <= 32: D x D, identity-padded (warp_cholesky input); d > 32:
+  // d x d factored in place, overlaying sM (each (i, l) entry is read from sM
+  // and written to sA by the same thread)
+  double* sA = d > 32 ? sM : sV + dd;
+  double* sbar = sV + dd + (d > 32 ? 0 : D * D);  // d
+  double* sshift = sbar + d;          // d
+  double* smon = sshift + d;          // nmon x d
+  double* sg = smon + f.nmon * d;     // nmon x J group means, then nmon RNEs
+  double* sS = sg + f.nmon * J + f.nmon;  // J x d group sums (staged)
+  __shared__ int s_h, s_flag;
+  if (f.trace && threadIdx.x == 0) f.trace[0] = gtimer();
+  // ---- stage: independent L2 loads
+  stage_cg(sshift, f.shift, d);
+  stage_cg(smon, f.mon, f.nmon * d);
+  if (f.stage_S)
+#pragma unroll 1
+    for (int r = 0; r < f.G; ++r) stage_cg(sS + (int64_t)r * gs_len, f.gath + (int64_t)r * f.slice_len, gs_len);
+  if (f.G == 1) {
+    stage_cg(sM, f.gath + gs_len, dd);
+  } else {
+#pragma unroll 1
+    for (int idx = threadIdx.x; idx < dd; idx += blockDim.x) {
+      double m = 0.0;
+#pragma unroll 1
+      for (int r = 0; r < f.G; ++r) m += __ldcg(f.gath + (int64_t)r * f.slice_len + gs_len + idx);
+      sM[idx] = m;
+    }
+  }
+  if (threadIdx.x == 0) {  // h update from the pooled acceptance (R6)
+    int h = f.ctl->h;
+    if (f.mode == 1) {
+      double acc = 0.0, err = 0.0;
+#pragma unroll 1
+      for (int r = 0; r < f.G; ++r) {
+        acc += __ldcg(f.gath + (int64_t)r * f.slice_len + gs_len + dd);
+        err = fmax(err, __ldcg(f.gath + (int64_t)r * f.slice_len + gs_len + dd + 1));
+      }
+      h = (acc > f.accept_target * P) ? min(h + f.h_step, f.h_max) : max(h - f.h_step, f.h_min);
+      if (err > 0.0) f.ctl->err = (int)err;
+      f.ctl->h = h;
+      f.ctl->acc = (unsigned long long)acc;
+    }
+    s_h = h;
+  }
+  __syncthreads();
+  if (f.trace && threadIdx.x == 0) f.trace[1] = gtimer();
+  auto S = [&](int j, int i) -> double { return f.stage_S ? sS[j * d + i] : group_sum_global(f, j, i); };
+  // ---- theta-bar: warp per coordinate, lanes over groups, fixed shuffle tree
+#pragma unroll 1
+  for (int i = w; i < d; i += nw) {
+    double s = 0.0;
+#pragma unroll 1
+    for (int j = lane; j < J; j += 32) s += S(j, i);
+    s = warp_sum(s);
+    if (lane == 0) sbar[i] = s / P;
+  }
+  __syncthreads();
+  if (f.trace && threadIdx.x == 0) f.trace[2] = gtimer();
+  const double hd = (double)s_h / 100.0;
+#pragma unroll 1
+  for (int i = w; i < d; i += nw) {
+    const double ci = sbar[i] - sshift[i];
+#pragma unroll 1
+    for (int l = lane; l < d; l += 32) {
+      const double cl = sbar[l] - sshift[l];
+      const double v = (sM[i * d + l] - P * ci * cl) / (P - 1.0);
+      sV[i * d + l] = v;
+      sA[i * ldc + l] = hd * v;
+    }
+  }
+  if (d <= 32)  // identity padding of the D x D factorization input
+    for (int idx = threadIdx.x; idx < D * D; idx += blockDim.x) {
+      const int i = idx / D, l = idx - i * D;
+      if (i >= d || l >= d) sA[idx] = i == l ? 1.0 : 0.0;
+    }
+  __syncthreads();
+  if (f.trace && threadIdx.x == 0) f.trace[3] = gtimer();
+  const int ldp = round_up(d, 4);  // padded (DMMA) layout of the factor
+  if (w == 0 && d <= 32) {         // chol((h/100) V), one ridge retry (R13)
+    bool ok = warp_cholesky_d(sA, f.Lprop, ldp, d);
+    int ridge_used = 0;
+    if (!ok) {
+      double tr = 0.0;
+#pragma unroll 1
+      for (int i = 0; i < d; ++i) tr += sV[i * d + i];
+      const double ridge = 1e-8 * tr / (double)d;
+      if (lane < d)
+#pragma unroll 1
+        for (int l = 0; l < d; ++l) sA[lane * ldc + l] = hd * (sV[lane * d + l] + (lane == l ? ridge : 0.0));
+      __syncwarp();
+      ok = warp_cholesky_d(sA, f.Lprop, ldp, d);
+      ridge_used = 1;
+    }
+    if (lane == 0) {
+      f.ctl->chol_ridge = ridge_used;
+      if (!ok) f.ctl->err = ERR_NUMERIC;
+    }
+  } else if (w > 0 && f.mode == 1) {  // monitor RNEs: warp per monitor, lanes over groups
+#pragma unroll 1
+    for (int m = w - 1; m < f.nmon; m += nw - 1) {
+      const double* av = smon + m * d;
+      double gp = 0.0;
+#pragma unroll 1
+      for (int j = lane; j < J; j += 32) {
+        double s0 = 0.0, s1 = 0.0;
+        int i = 0;
+        for (; i + 2 <= d; i += 2) {
+          s0 = fma(av[i], S(j, i), s0);
+          s1 = fma(av[i + 1], S(j, i + 1), s1);
+        }
+        if (i < d) s0 = fma(av[i], S(j, i), s0);
+        const double g = (s0 + s1) / (double)f.N;
+        sg[m * J + j] = g;
+        gp += g;
+      }
+      const double gbar = warp_sum(gp) / (double)J;
+      double dev = 0.0;
+#pragma unroll 1
+      for (int j = lane; j < J; j += 32) {
+        const double t = sg[m * J + j] - gbar;
+        dev = fma(t, t, dev);
+      }
+      dev = warp_sum(dev);
+      double quad = 0.0;
+#pragma unroll 2
+      for (int i = 0; i < d; ++i)
+#pragma unroll 1
+        for (int l = lane; l < d; l += 32) quad += av[i] * sV[i * d + l] * av[l];
+      quad = warp_sum(quad);
+      const double vhat = (double)f.N / (double)(J - 1) * dev;
+      const double var = quad * (P - 1.0) / P;
+      if (lane == 0) sg[f.nmon * J + m] = vhat > 0.0 ? var / vhat : INFINITY;
+    }
+  }
+  __syncthreads();
+  if (f.trace && threadIdx.x == 0) f.trace[4] = gtimer();
+  if (d > 32) {  // block Cholesky (larger d)
+    block_factor(f, sA, sV, hd, ldp, &s_flag);
+  }
+  if (f.mode == 1 && threadIdx.x == 0) {
+    double minrne = INFINITY;
+#pragma unroll 1
+    for (int m = 0; m < f.nmon; ++m) {
+      const double rne = sg[f.nmon * J + m];
+      if (f.rne_out) f.rne_out[m] = rne;
+      minrne = fmin(minrne, rne);
+    }
+    f.ctl->minrne = minrne;
+    f.ctl->stop = (f.K > 0.0 && minrne >= f.K) ? 1 : 0;
+    f.ctl->steps_done += 1;
+  }
+#pragma unroll 1
+  for (int idx = threadIdx.x; idx < dd; idx += blockDim.x) f.V[idx] = sV[idx];
+  for (int i = threadIdx.x; i < d; i += blockDim.x) f.shift[i] = sbar[i];
+  __syncthreads();
+  if (f.trace && threadIdx.x == 0) f.trace[5] = gtimer();
+  if (f.host_out && threadIdx.x == 0) *f.host_out = *f.ctl;  // into mapped pinned host memory (visible at kernel end)
+  if (f.trace && threadIdx.x == 0) f.trace[6] = gtimer();
+}
+
 // Deterministic reduction of the block partials into this rank's stats slice
 // [Jl x d group sums | d x d second moment | accepts | error].  Blocks
 // [0, nm): 32 moment entries each (8 warps x 8 independent rows per round,
 // fixed-order combine); blocks [nm, nm + ng): group sums; last block: accepts.
+// With f.ticket (one rank: the slice is the gathered stats) the last block to
+// finish runs finalize_body on them (saves a launch and a dependent-launch gap).
 __global__ void __launch_bounds__(256) k_mom_reduce(const double* __restrict__ bpart, int nblk, int bpg, int Jl,
                                                     int d, Ctl* ctl, double* __restrict__ slice,
-                                                    const int* __restrict__ stop) {
+                                                    const int* __restrict__ stop, FinArgs f) {
+  extern __shared__ double fin_sm[];
   __shared__ double part[8][33];
+  __shared__ int s_last;
+  if (f.trace && threadIdx.x == 0) f.trace[8 + blockIdx.x] = gtimer();
   if (stop && *stop) return;
   const int dd = d * d, W = d + dd + 1;
   const int nm = (dd + 31) / 32, ng = (Jl * d + 255) / 256;
@@ -596,259 +891,23 @@ __global__ void __launch_bounds__(256) k_mom_reduce(const double* __restrict__ b
       slice[Jl * d + dd + 1] = (double)ctl->err;
     }
   }
+  if (!f.ticket) return;
+  __threadfence();  // this block's slice writes before its ticket
+  __syncthreads();
+  if (f.trace && threadIdx.x == 0) f.trace[8 + gridDim.x + blockIdx.x] = gtimer();
+  if (threadIdx.x == 0) s_last = atomicAdd(f.ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x == 0) *f.ticket = 0u;  // re-armed for the next launch (stream order)
+  finalize_body(f, fin_sm);
 }
 
-// Cholesky of a d x d SPD matrix (d <= D <= 32, D a multiple of 4 known at
-// compile time; rows/cols d..D-1 are identity padding) by ONE warp, rows in
-// registers (lane i holds row i).  Column j: every lane takes rsqrt of the
-// pivot broadcast by shuffle (measured B200 latencies: rsqrt ~67 cycles,
-// 64-bit shuffle ~31, DFMA 8); the column goes through shared memory for the
-// off-diagonal updates, each lane's own diagonal stays in registers, so the
-// pivot chain is ~110 cycles per column.  A: row-major d x d (read),
-// Lout: lower factor (write), colbuf: 32 doubles of shared memory.
-// 1/sqrt(x) without a slow-path call: MUFU approximation + 2 Newton steps
-// (relative error ~1 ulp); non-positive / non-finite x give non-finite results.
-__device__ __forceinline__ double rsqrt_nr(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double h = 0.5 * x;
-  y = fma(y, fma(-h * y, y, 0.5), y);
-  y = fma(y, fma(-h * y, y, 0.5), y);
-  return y;
-}
-
-template <int D>
-__device__ bool warp_cholesky(const double* A, int d, double scale, double ridge, double* Lout, double* colbuf,
-                              int ldo, bool write = true) {
-  const int lane = threadIdx.x & 31;
-  double a[D];
-#pragma unroll
-  for (int l = 0; l < D; ++l)
-    a[l] = (lane < d && l < d) ? scale * (A[lane * d + l] + (lane == l ? ridge : 0.0)) : (lane == l ? 1.0 : 0.0);
-#pragma unroll
-  for (int j = 0; j < D; ++j) {
-    const double r = rsqrt_nr(__shfl_sync(0xffffffffu, a[j], j));
-    const double lij = lane >= j ? a[j] * r : 0.0;  // L[lane][j]; lane j: sqrt(pivot)
-    a[j] = lij;
-    if (j + 1 < D) {
-      colbuf[lane] = lij;
-      __syncwarp();
-      // branch-free: lanes < j carry lij = 0; entries above the diagonal are scratch
-#pragma unroll
-      for (int l = j + 1; l < D; ++l) a[l] = fma(-lij, (lane == l) ? lij : colbuf[l], a[l]);
-      __syncwarp();
-    }
-  }
-  // a non-positive or non-finite pivot leaves a non-finite or non-positive diagonal
-  double diag = 1.0;
-#pragma unroll
-  for (int l = 0; l < D; ++l)
-    if (lane == l) diag = a[l];
-  const bool ok = __all_sync(0xffffffffu, lane >= d || (diag > 0.0 && isfinite(diag)));
-  if (write && lane < d)
-#pragma unroll
-    for (int l = 0; l < D; ++l)
-      if (l < d) Lout[lane * ldo + l] = l <= lane ? a[l] : 0.0;
-  return ok;
-}
-
-
-// chol((h/100) V) for d <= 32 by one warp (no divergent enclosing code, so
-// shuffles need no convergence barriers); one ridge retry (R13).
-template <int D>
-__global__ void __launch_bounds__(32) k_chol_warp(const double* __restrict__ V, int d, Ctl* ctl,
-                                                  double* __restrict__ Lout, const int* __restrict__ stop_in) {
-  __shared__ double sV[D * D];
-  __shared__ double col[32];
-  if (stop_in && *stop_in) return;
-  for (int i = threadIdx.x; i < d * d; i += 32) sV[i] = V[i];
-  __syncwarp();
-  const double hd = (double)ctl->h / 100.0;
-  const int ld = round_up(d, 4);  // padded (DMMA) layout of the factor
-  bool ok = warp_cholesky<D>(sV, d, hd, 0.0, Lout, col, ld);
-  if (!ok) {
-    double tr = 0.0;
-    for (int i = 0; i < d; ++i) tr += sV[i * d + i];
-    ok = warp_cholesky<D>(sV, d, hd, 1e-8 * tr / (double)d, Lout, col, ld);
-    if (threadIdx.x == 0) {
-      ctl->chol_ridge = 1;
-      if (!ok) ctl->err = ERR_NUMERIC;
-    }
-  } else if (threadIdx.x == 0) {
-    ctl->chol_ridge = 0;
-  }
-}
-
-// ---------------------------------------------------------------- K7
-// theta-bar, pooled V (R11), h update (R6), monitor RNEs + stop flag (R12,
-// R14), chol((h/100) V) with one ridge retry (R13), new shift.  One block;
-// every rank computes the identical result from the gathered stats.  All
-// inputs are first staged into shared memory with independent loads (the
-// kernel is latency-bound: one block, a handful of dependent phases).
-template <int D>  // D > 0: d <= D <= 32, Cholesky by the warps redundantly (no divergent region); D = 0: block path
-__global__ void __launch_bounds__(256) k_finalize2(FinArgs f) {
-  extern __shared__ double sm[];
-  __shared__ int flag;
-  __shared__ double red[32];
+// Finalize as its own launch (G > 1: after the all-gather of the slices; mode 0).
+__global__ void __launch_bounds__(256) k_finalize(FinArgs f) {
+  extern __shared__ double fin_sm[];
   if (f.stop_in && *f.stop_in) return;
-  const int d = f.d, J = f.J, lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int gs_len = f.Jl * d;
-  double* sV = sm;                 // d x d
-  double* sbar = sV + d * d;       // d
-  double* sA = sbar + d;           // d x d (Cholesky work of the block path; also the summed M)
-  double* sg = sA + d * d;         // nmon x J group means + nmon RNEs
-  double* sshift = sg + f.nmon * J + f.nmon;  // d
-  double* smon = sshift + d;       // nmon x d
-  double* sS = smon + f.nmon * d;  // J x d group sums (rank order == group order), when staged
-  double* sM = sA;                 // consumed (into V) before sA is written
-  const double P = (double)J * (double)f.N;
-  auto S = [&](int j, int i) -> double {
-    return f.stage_S ? sS[j * d + i] : f.gath[(int64_t)(j / f.Jl) * f.slice_len + (int64_t)(j % f.Jl) * d + i];
-  };
-  // ---- stage (one cp.async round)
-  for (int i = threadIdx.x; i < d; i += blockDim.x) cp_async8(sshift + i, f.shift + i);
-  for (int i = threadIdx.x; i < f.nmon * d; i += blockDim.x) cp_async8(smon + i, f.mon + i);
-  if (f.stage_S)
-    for (int r = 0; r < f.G; ++r)
-      for (int off = threadIdx.x; off < gs_len; off += blockDim.x)
-        cp_async8(sS + (int64_t)r * gs_len + off, f.gath + (int64_t)r * f.slice_len + off);
-  if (f.G == 1)
-    for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) cp_async8(sM + idx, f.gath + gs_len + idx);
-  cp_async_wait_all();
-  if (f.G > 1)
-    for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) {
-      double m = 0.0;
-      for (int r = 0; r < f.G; ++r) m += f.gath[(int64_t)r * f.slice_len + gs_len + idx];
-      sM[idx] = m;
-    }
-  __syncthreads();
-  if (f.trace && threadIdx.x == 0) f.trace[1] = clock64();
-  // ---- theta-bar: warp per coordinate, lanes over groups, fixed shuffle tree
-  for (int i = w; i < d; i += nw) {
-    double s = 0.0;
-    for (int j = lane; j < J; j += 32) s += S(j, i);
-    s = warp_sum(s);
-    if (lane == 0) sbar[i] = s / P;
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) {
-    const int i = idx / d, l = idx - i * d;
-    const double ci = sbar[i] - sshift[i], cl = sbar[l] - sshift[l];
-    sV[idx] = (sM[idx] - P * ci * cl) / (P - 1.0);
-  }
-  __syncthreads();
-  if (f.trace && threadIdx.x == 0) f.trace[2] = clock64();
-  // warp 0: h update (from the pooled acceptance) then chol((h/100) V) in registers (d <= 32);
-  // warps 1..: monitor RNEs, one warp per monitor (lanes over groups / V entries)
-  __shared__ int s_h;
-  __shared__ double s_col[8 * 32];
-  if (w == 0) {
-    int h = f.ctl->h;
-    if (f.mode == 1) {
-      double acc = 0.0, err = 0.0;
-      for (int r = 0; r < f.G; ++r) {
-        acc += f.gath[(int64_t)r * f.slice_len + gs_len + d * d];
-        err = fmax(err, f.gath[(int64_t)r * f.slice_len + gs_len + d * d + 1]);
-      }
-      h = (acc > f.accept_target * P) ? min(h + f.h_step, f.h_max) : max(h - f.h_step, f.h_min);
-      if (lane == 0) {
-        if (err > 0.0) f.ctl->err = (int)err;
-        f.ctl->h = h;
-        f.ctl->acc = (unsigned long long)acc;
-      }
-    }
-    if (lane == 0) s_h = h;
-  } else if (f.mode == 1 && w - 1 < f.nmon) {
-    for (int m = w - 1; m < f.nmon; m += nw - 1) {
-      const double* av = smon + m * d;
-      double gp = 0.0;
-      for (int j = lane; j < J; j += 32) {
-        double s0 = 0.0, s1 = 0.0;
-        int i = 0;
-        for (; i + 2 <= d; i += 2) {
-          s0 = fma(av[i], S(j, i), s0);
-          s1 = fma(av[i + 1], S(j, i + 1), s1);
-        }
-        if (i < d) s0 = fma(av[i], S(j, i), s0);
-        const double g = (s0 + s1) / (double)f.N;
-        sg[m * J + j] = g;
-        gp += g;
-      }
-      const double gbar = warp_sum(gp) / (double)J;
-      double dev = 0.0;
-      for (int j = lane; j < J; j += 32) {
-        const double t = sg[m * J + j] - gbar;
-        dev = fma(t, t, dev);
-      }
-      dev = warp_sum(dev);
-      double quad = 0.0;
-      for (int idx = lane; idx < d * d; idx += 32) {
-        const int i = idx / d;
-        quad += av[i] * sV[idx] * av[idx - i * d];
-      }
-      quad = warp_sum(quad);
-      const double vhat = (double)f.N / (double)(J - 1) * dev;
-      const double var = quad * (P - 1.0) / P;
-      if (lane == 0) sg[f.nmon * J + m] = vhat > 0.0 ? var / vhat : INFINITY;
-    }
-  }
-  __syncthreads();
-  if (f.mode == 1 && threadIdx.x == 0) {
-    double minrne = INFINITY;
-    for (int m = 0; m < f.nmon; ++m) {
-      const double rne = sg[f.nmon * J + m];
-      if (f.rne_out) f.rne_out[m] = rne;
-      minrne = fmin(minrne, rne);
-    }
-    f.ctl->minrne = minrne;
-    f.ctl->stop = (f.K > 0.0 && minrne >= f.K) ? 1 : 0;
-    f.ctl->steps_done += 1;
-  }
-  const double hd = (double)s_h / 100.0;
-  if (f.trace && threadIdx.x == 0) f.trace[3] = clock64();
-  if constexpr (D > 0) {
-    // every warp factors (h/100) V (identical results, no divergent region around the
-    // shuffles); warp 0 writes the padded factor (ld = round_up(d, 4))
-    const int ld = round_up(d, 4);
-    bool ok = warp_cholesky<D>(sV, d, hd, 0.0, f.Lprop, s_col + 32 * w, ld, w == 0);
-    int ridge_used = 0;
-    if (!ok) {
-      double tr = 0.0;
-      for (int i = 0; i < d; ++i) tr += sV[i * d + i];
-      ok = warp_cholesky<D>(sV, d, hd, 1e-8 * tr / (double)d, f.Lprop, s_col + 32 * w, ld, w == 0);
-      ridge_used = 1;
-    }
-    if (threadIdx.x == 0) {
-      f.ctl->chol_ridge = ridge_used;
-      if (!ok) f.ctl->err = ERR_NUMERIC;
-    }
-  } else {  // block Cholesky (larger d)
-    for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) sA[idx] = hd * sV[idx];
-    __syncthreads();
-    bool ok = block_cholesky(sA, d, &flag);
-    if (threadIdx.x == 0) f.ctl->chol_ridge = ok ? 0 : 1;
-    if (!ok) {
-      double tr = 0.0;
-      for (int i = 0; i < d; ++i) tr += sV[i * d + i];
-      const double ridge = 1e-8 * tr / (double)d;
-      for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x)
-        sA[idx] = hd * (sV[idx] + ((idx / d == idx % d) ? ridge : 0.0));
-      __syncthreads();
-      ok = block_cholesky(sA, d, &flag);
-      if (!ok) {
-        if (threadIdx.x == 0) f.ctl->err = ERR_NUMERIC;
-        return;
-      }
-    }
-    for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) f.Lprop[(idx / d) * round_up(d, 4) + idx % d] = sA[idx];
-  }
-  if (f.trace && threadIdx.x == 0) f.trace[4] = clock64();
-  for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) f.V[idx] = sV[idx];
-  if (f.trace && threadIdx.x == 0) f.trace[5] = clock64();
-  for (int i = threadIdx.x; i < d; i += blockDim.x) f.shift[i] = sbar[i];
-  __syncthreads();
-  if (f.host_out && threadIdx.x == 0) *f.host_out = *f.ctl;  // into mapped pinned host memory (visible at kernel end)
-  if (f.trace && threadIdx.x == 0) f.trace[6] = clock64();
+  finalize_body(f, fin_sm);
 }
 
 // Prior precision Sinv = Lprior^-T Lprior^-1 (one block; smem: Linv d x d).

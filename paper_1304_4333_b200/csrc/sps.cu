@@ -139,9 +139,12 @@ struct sps_ctx {
   double *LpriorP = nullptr, *SinvP = nullptr;  // padded copies (NP x KP) for the DMMA proposal kernel
   double* bpart = nullptr;       // accept+moments block partials
   int tp = 0, QE = 1, W = 0, nblk = 0;
-  Ctl* hslot = nullptr;          // 2 mapped pinned Ctl slots (pipelined M steps), written by k_finalize2
+  Ctl* hslot = nullptr;          // 2 mapped pinned Ctl slots (pipelined M steps), written by finalize_body
   Ctl* dslot = nullptr;          // device view of hslot
-  long long* fin_trace = nullptr;  // debug (SPS_FIN_TRACE): k_finalize2 phase clocks
+  unsigned* ticket = nullptr;      // arrival counter of the fused reduce + finalize (k_mom_reduce)
+  unsigned long long* trace = nullptr;  // debug (SPS_TRACE): finalize / reduce phase clocks (managed)
+  double trace_acc[80] = {};
+  int trace_n = 0;
   double* Zbuf[2] = {nullptr, nullptr};  // standard normals, one M step ahead (side stream)
   double* LUbuf[2] = {nullptr, nullptr}; // plog of the ACCEPT uniforms, same schedule
   cudaStream_t aux = nullptr;
@@ -537,7 +540,7 @@ sps_status launch_draw(sps_ctx* c, int slot, const double* base, const double* L
 // K9 + K6 (decide = true) or K6 only, then the deterministic reduction into this
 // rank's stats slice and the gather across ranks -> `gath`.
 sps_status accept_moments(sps_ctx* c, bool decide, int nchunks, double temper, uint32_t step, const int* stop,
-                          const double* logu = nullptr) {
+                          const double* logu = nullptr, const FinArgs* fin = nullptr, size_t fin_smem = 0) {
   AccArgs a{};
   a.theta = c->theta;
   a.L = c->L;
@@ -580,10 +583,13 @@ sps_status accept_moments(sps_ctx* c, bool decide, int nchunks, double temper, u
   PROF_END(c, CAT_ACCEPT);
   const int d = c->d;
   const int nm = (d * d + 31) / 32, ng = (c->Jl * d + 255) / 256;
+  FinArgs none{};
   PROF_BEGIN(c);
-  k_mom_reduce<<<nm + ng + 1, 256, 0, c->stream>>>(c->bpart, c->nblk, c->N / c->tp, c->Jl, d, c->ctl, c->slice, stop);
+  k_mom_reduce<<<nm + ng + 1, 256, fin ? fin_smem : 0, c->stream>>>(c->bpart, c->nblk, c->N / c->tp, c->Jl, d, c->ctl,
+                                                                   c->slice, stop, fin ? *fin : none);
   CHECK_LAUNCH(c);
-  PROF_END(c, CAT_REDUCE);
+  PROF_END(c, fin ? CAT_FINALIZE : CAT_REDUCE);
+  if (fin) return SPS_OK;  // one rank: the slice is the gathered stats, finalized by the last block
   PROF_BEGIN(c);
   TRY(gather(c, c->slice, c->gath, (size_t)c->slice_len));
   PROF_END(c, CAT_GATHER);
@@ -594,10 +600,10 @@ bool final_cycle(const sps_ctx* c) {
   return c->cfg.tempering == SPS_POWER_TEMPERING ? (c->phi == 1.0) : (c->t == c->n);
 }
 
-sps_status finalize(sps_ctx* c, int mode, bool allow_stop, const int* stop, int slot = -1) {
+// Arguments of finalize_body (K7) and its dynamic shared memory.
+sps_status make_fin(sps_ctx* c, int mode, bool allow_stop, const int* stop, int slot, FinArgs* fo, size_t* smem_out) {
   FinArgs f{};
   f.host_out = slot >= 0 ? c->dslot + slot : nullptr;
-  f.trace = c->fin_trace;
   f.gath = c->gath;
   f.G = c->G;
   f.slice_len = c->slice_len;
@@ -619,27 +625,39 @@ sps_status finalize(sps_ctx* c, int mode, bool allow_stop, const int* stop, int 
   f.ctl = c->ctl;
   f.stop_in = stop;
   f.rne_out = c->rne;
-  const size_t base_sm =
-      (size_t)(2 * c->d * c->d + 2 * c->d + c->nmon * c->J + c->nmon + c->nmon * c->d) * sizeof(double);
-  const size_t s_sm = (size_t)c->J * c->d * sizeof(double);
-  f.stage_S = base_sm + s_sm <= 200 * 1024 ? 1 : 0;
-  const size_t smem = base_sm + (f.stage_S ? s_sm : 0);
+  f.trace = c->trace;
+  f.stage_S = fin_smem_doubles(c->d, c->J, c->nmon, true) * 8 <= 200 * 1024 ? 1 : 0;
+  const size_t smem = (size_t)fin_smem_doubles(c->d, c->J, c->nmon, f.stage_S != 0) * sizeof(double);
   if (smem > 200 * 1024) return fail(c, SPS_E_CONFIG, "d = %d too large for the finalize kernel", c->d);
+  *fo = f;
+  *smem_out = smem;
+  return SPS_OK;
+}
+
+// K7 as its own launch (after the gather; G > 1).
+sps_status finalize(sps_ctx* c, int mode, bool allow_stop, const int* stop, int slot = -1) {
+  FinArgs f;
+  size_t smem = 0;
+  TRY(make_fin(c, mode, allow_stop, stop, slot, &f, &smem));
   PROF_BEGIN(c);
-  switch (c->d <= 32 ? (c->d + 3) / 4 : 0) {
-    case 1: k_finalize2<4><<<1, 256, smem, c->stream>>>(f); break;
-    case 2: k_finalize2<8><<<1, 256, smem, c->stream>>>(f); break;
-    case 3: k_finalize2<12><<<1, 256, smem, c->stream>>>(f); break;
-    case 4: k_finalize2<16><<<1, 256, smem, c->stream>>>(f); break;
-    case 5: k_finalize2<20><<<1, 256, smem, c->stream>>>(f); break;
-    case 6: k_finalize2<24><<<1, 256, smem, c->stream>>>(f); break;
-    case 7: k_finalize2<28><<<1, 256, smem, c->stream>>>(f); break;
-    case 8: k_finalize2<32><<<1, 256, smem, c->stream>>>(f); break;
-    default: k_finalize2<0><<<1, 256, smem, c->stream>>>(f); break;
-  }
+  k_finalize<<<1, 256, smem, c->stream>>>(f);
   CHECK_LAUNCH(c);
   PROF_END(c, CAT_FINALIZE);
   return SPS_OK;
+}
+
+// K9 + K6 -> reduce -> (gather) -> K7: fused into the reduce launch on one rank.
+sps_status moments_finalize(sps_ctx* c, bool decide, int nchunks, double temper, uint32_t step, const int* stop,
+                            const double* logu, int mode, bool allow_stop, int slot) {
+  if (c->G > 1) {
+    TRY(accept_moments(c, decide, nchunks, temper, step, stop, logu));
+    return finalize(c, mode, allow_stop, stop, slot);
+  }
+  FinArgs f;
+  size_t smem = 0;
+  TRY(make_fin(c, mode, allow_stop, stop, slot, &f, &smem));
+  f.ticket = c->ticket;
+  return accept_moments(c, decide, nchunks, temper, step, stop, logu, &f, smem);
 }
 
 sps_status validate(const sps_config* cfg) {
@@ -681,6 +699,8 @@ void free_ctx(sps_ctx* c) {
     if (p) cudaFree(p);
   if (c->hctl) cudaFreeHost(c->hctl);
   if (c->hslot) cudaFreeHost(c->hslot);
+  if (c->ticket) cudaFree(c->ticket);
+  if (c->trace) cudaFree(c->trace);
   for (cudaEvent_t e : c->evs)
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : c->prof_pool) cudaEventDestroy(e);
@@ -851,7 +871,9 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
   TRY(dalloc(c, &c->Sinv, (size_t)d * d));
   CU(c, cudaHostAlloc((void**)&c->hslot, 2 * sizeof(Ctl), cudaHostAllocMapped));
   CU(c, cudaHostGetDevicePointer((void**)&c->dslot, c->hslot, 0));
-  if (getenv("SPS_FIN_TRACE")) CU(c, cudaMallocManaged((void**)&c->fin_trace, 8 * sizeof(long long)));
+  CU(c, cudaMalloc((void**)&c->ticket, sizeof(unsigned)));
+  if (getenv("SPS_TRACE")) CU(c, cudaMallocManaged((void**)&c->trace, 128 * sizeof(unsigned long long)));
+  CU(c, cudaMemsetAsync(c->ticket, 0, sizeof(unsigned), c->stream));
   CU(c, cudaEventCreateWithFlags(&c->evs[0], cudaEventDisableTiming));
   CU(c, cudaEventCreateWithFlags(&c->evs[1], cudaEventDisableTiming));
   TRY(dalloc(c, &c->slice, (size_t)c->slice_len));
@@ -958,24 +980,15 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
                            (const void*)k_propose<true>, (const void*)k_propose<false>, (const void*)k_accept_mom,
                            (const void*)k_accept_mom_rb<1>, (const void*)k_accept_mom_rb<2>,
                            (const void*)k_accept_mom_rb<3>, (const void*)k_accept_mom_rb<4>, (const void*)k_mom_reduce,
-                           (const void*)k_finalize2<0>, (const void*)k_chol_warp<4>, (const void*)k_chol_warp<8>,
-                           (const void*)k_chol_warp<12>, (const void*)k_chol_warp<16>, (const void*)k_chol_warp<20>,
-                           (const void*)k_chol_warp<24>, (const void*)k_chol_warp<28>, (const void*)k_chol_warp<32>,
+                           (const void*)k_finalize,
                            (const void*)k_normals};
       for (const void* fn : fns)
         CU(c, cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
     }
     CU(c, cudaFuncSetAttribute(k_propose<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(c, cudaFuncSetAttribute(k_propose<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    CU(c, cudaFuncSetAttribute(k_finalize2<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    CU(c, cudaFuncSetAttribute(k_finalize2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    CU(c, cudaFuncSetAttribute(k_finalize2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    CU(c, cudaFuncSetAttribute(k_finalize2<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    CU(c, cudaFuncSetAttribute(k_finalize2<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    CU(c, cudaFuncSetAttribute(k_finalize2<20>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    CU(c, cudaFuncSetAttribute(k_finalize2<24>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    CU(c, cudaFuncSetAttribute(k_finalize2<28>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    CU(c, cudaFuncSetAttribute(k_finalize2<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_mom_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(c, cudaFuncSetAttribute(k_accept_mom, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(c, cudaFuncSetAttribute(k_accept_mom_rb<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(c, cudaFuncSetAttribute(k_accept_mom_rb<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
@@ -1066,10 +1079,10 @@ sps_status sps_get_counters(const sps_ctx* cc, sps_counters* out) {
   if (!cc || !out) return SPS_E_CONFIG;
   sps_ctx* c = const_cast<sps_ctx*>(cc);
   TRY(prof_resolve(c));
-  if (c->fin_trace) {
-    CU(c, cudaStreamSynchronize(c->stream));
-    fprintf(stderr, "fin_trace cycles:");
-    for (int q = 1; q < 7; ++q) fprintf(stderr, " %lld", c->fin_trace[q] - c->fin_trace[q - 1]);
+  if (c->trace && c->trace_n) {
+    static const char* nm[] = {"reduce", "ticket->fin", "stage", "theta-bar", "V", "chol|RNE", "stats+writes", "host slot"};
+    fprintf(stderr, "SPS_TRACE mean ns over %d finalizes:", c->trace_n);
+    for (int q = 0; q < 8; ++q) fprintf(stderr, " %s=%.0f", nm[q], c->trace_acc[q] / c->trace_n);
     fprintf(stderr, "\n");
   }
   out->launches = c->launches;
@@ -1256,6 +1269,24 @@ sps_status sps_cphase(sps_ctx* c, int32_t t_target, double phi_target, int32_t* 
   return SPS_OK;
 }
 
+// Debug (SPS_TRACE): accumulate the phase clocks of the last finished fused
+// reduce + finalize (serializes the pipeline; timings of phases only).
+static void trace_accumulate(sps_ctx* c) {
+  cudaStreamSynchronize(c->stream);
+  const unsigned long long* t = c->trace;
+  const int d = c->d, nb = (d * d + 31) / 32 + (c->Jl * d + 255) / 256 + 1;
+  unsigned long long s0 = ~0ull, e1 = 0;
+  for (int b = 0; b < nb; ++b) {
+    s0 = std::min(s0, t[8 + b]);
+    e1 = std::max(e1, t[8 + nb + b]);
+  }
+  if (t[0] < s0 || t[6] < t[0]) return;  // stopped step (no finalize)
+  c->trace_acc[0] += (double)(e1 - s0);      // reduce phase: first block start -> last block ticket
+  c->trace_acc[1] += (double)(t[0] - e1);    // ticket -> finalize start
+  for (int q = 1; q <= 6; ++q) c->trace_acc[1 + q] += (double)(t[q] - t[q - 1]);
+  c->trace_n += 1;
+}
+
 // One M step (Algorithm 2 step 2(c)), fully enqueued:
 // K8 propose -> K1 loglik of theta* on [0, t_l) -> K9+K6 accept & moments ->
 // stats reduce -> gather -> K7 finalize (h, RNE, stop, chol(h V)) -> D2H of
@@ -1272,9 +1303,8 @@ static sps_status launch_mstep(sps_ctx* c, uint32_t step, int slot, bool allow_s
   TRY(launch_normals(c, TAG_PROPOSAL, step + 1u, (int)((step + 1u) & 1u)));  // next step's normals, overlapped
   int nch = 1;
   TRY(launch_loglik(c, c->theta_s, c->d, c->Pl, 0, t1, c->part, c->max_chunks, &nch, stop));
-  TRY(accept_moments(c, true, nch, temper, step, stop, c->LUbuf[zs]));
+  TRY(moments_finalize(c, true, nch, temper, step, stop, c->LUbuf[zs], 1, allow_stop, slot));
   CU(c, cudaEventRecord(c->ev_zfree[zs], c->stream));  // Zbuf / LUbuf[zs] consumed
-  TRY(finalize(c, 1, allow_stop, stop, slot));
   CU(c, cudaEventRecord(c->evs[slot], c->stream));
   return SPS_OK;
 }
@@ -1291,8 +1321,7 @@ sps_status sps_mphase(sps_ctx* c, int32_t R_fixed, int32_t* R_out, double* min_r
   CU(c, cudaMemsetAsync(&c->ctl->stop, 0, sizeof(int), c->stream));
   CU(c, cudaMemsetAsync(&c->ctl->steps_done, 0, sizeof(int), c->stream));
   if (c->need_pre_moments) {
-    TRY(accept_moments(c, false, 1, 1.0, 0u, nullptr));
-    TRY(finalize(c, 0, false, nullptr));
+    TRY(moments_finalize(c, false, 1, 1.0, 0u, nullptr, nullptr, 0, false, -1));
     c->need_pre_moments = false;
   }
   const uint32_t step0 = c->mstep;
@@ -1310,6 +1339,7 @@ sps_status sps_mphase(sps_ctx* c, int32_t R_fixed, int32_t* R_out, double* min_r
     c->host_launch_us += std::chrono::duration<double, std::micro>(h1 - h0).count();
     c->host_wait_us += std::chrono::duration<double, std::micro>(h2 - h1).count();
     c->syncs += 1;
+    if (c->trace) trace_accumulate(c);
     got = c->hslot[(r - 1) % 2];
     c->pairs += (double)c->P * t1;
     if (got.err == ERR_NUMERIC)

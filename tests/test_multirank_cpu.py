@@ -33,7 +33,7 @@ def _slice_stats(theta, J, N, G, r, shift):
 
 
 def _combine(gathered, J, N, G, d, shift, a):
-    """Rank-order combination (as k_finalize2): theta-bar, V, RNE of monitor a."""
+    """Rank-order combination (as finalize_body): theta-bar, V, RNE of monitor a."""
     Jl = J // G
     S = np.concatenate([g[:Jl * d].reshape(Jl, d) for g in gathered])
     M = sum(g[Jl * d:].reshape(d, d) for g in gathered)
