@@ -310,7 +310,7 @@ def main():
             "clocks": clk,
             "e2e": e2e,
             "gpu_launches": launches,
-            "roofline": {"bound": "alu", "kernel": "k_loglik_bin_mma<6,1,4> (K1: fp64 DMMA contraction + fused softplus/product epilogue)",
+            "roofline": {"bound": "alu", "kernel": "k_loglik_bin_mma<6,1,2> (K1: fp64 DMMA contraction + fused softplus/product epilogue)",
                          "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
                          "ops_per_pair": ops_per_pair, "k1_avg_ms": k1_avg_ms,

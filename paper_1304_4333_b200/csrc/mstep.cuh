@@ -19,7 +19,8 @@ constexpr int PR_TILE = 64;  // particles per block (8 DMMA row tiles)
 struct DrawArgs {
   const double* base;  // P x d, or nullptr -> mu
   const double* Lz;    // lower factor, padded NP x KP (NP = round_up(d, 8), KP = round_up(d, 4))
-  const double* Sinv;  // prior precision, padded NP x KP
+  const double* Sinv;  // prior precision, padded NP x KP (k_propose)
+  const double* Rp;    // prior whitening factor Lprior^-1 (lower), padded NP x KP (k_propose_rb)
   const double* mu;
   const double* Z;  // P x 2 ceil(d/2) standard normals (k_normals)
   double* out;
@@ -152,55 +153,67 @@ __global__ void __launch_bounds__(256) k_propose(DrawArgs a) {
 
 // Register-blocked variant for d <= 32 (KK = round_up(d,4)/4 k-steps, NT =
 // round_up(d,8)/8 column tiles): warp w owns particle rows 8w..8w+7 of the
-// tile; all Lz and Sinv B-fragments live in registers (2 NT KK doubles), so a
-// DMMA costs one shared load of its A fragment (the two-operand smem version
-// is shared-memory-bandwidth bound: 512 B of LDS per 4-cycle DMMA).
+// tile; the Lz B-fragments live in registers, so a DMMA costs one shared load
+// of its A fragment.  Persistent (grid ~2 blocks per SM) and double-buffered:
+// the TMA loads of the block's next tile (Z rows, base rows) are in flight
+// while the current tile computes; theta* is assembled in shared memory over
+// the base rows and leaves as one TMA bulk store (contiguous rows).
 template <int KK>
 __global__ void __launch_bounds__(256, 2) k_propose_rb(DrawArgs a) {
   constexpr int KP = 4 * KK, NT = (KP + 7) / 8, NP = 8 * NT;
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
   if (a.stop && *a.stop) return;
-  const int d = a.d;
+  const int d = a.d, BS = round_up(PR_TILE * d, 2);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, ar = lane >> 2, ac = lane & 3;
-  double* Zs = sm;                  // PR_TILE x KP
-  double* Ds = Zs + PR_TILE * KP;   // PR_TILE x KP (theta* - mu)
-  double* smu = Ds + PR_TILE * KP;  // KP
-  double* sL = smu + KP;            // NP x KP
-  double* sS = sL + NP * KP;        // NP x KP
-  double* Bs = sS + NP * KP;        // PR_TILE x d
-  __shared__ __align__(8) uint64_t bar;
-  if (threadIdx.x == 0) mbar_init(&bar, 1);
+  double* Zs0 = sm;                     // 2 x PR_TILE x KP
+  double* Bs0 = Zs0 + 2 * PR_TILE * KP;  // 2 x BS: base rows, overwritten with theta*
+  double* Ds = Bs0 + 2 * BS;            // PR_TILE x KP (theta* - mu)
+  double* smu = Ds + PR_TILE * KP;      // KP
+  double* sL = smu + KP;                // NP x KP
+  double* sS = sL + NP * KP;            // NP x KP (Rp)
+  __shared__ __align__(8) uint64_t bar[2];
+  const int64_t ntl = (a.P + PR_TILE - 1) / PR_TILE;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+  }
   for (int i = threadIdx.x; i < KP; i += blockDim.x) smu[i] = i < d ? a.mu[i] : 0.0;
   __syncthreads();
-  const int64_t ntl = (a.P + PR_TILE - 1) / PR_TILE;
-  double bL[NT][KK];  // Lz B-fragments in registers; Sinv fragments are read from shared memory
-  unsigned phase = 0;
-  for (int64_t tile = blockIdx.x; tile < ntl; tile += gridDim.x) {
+  // thread 0: TMA loads of `tile` into buffer `buf` (+ Lz, Sinv with the first)
+  auto issue = [&](int64_t tile, int buf, bool first) {
     const int64_t pb = tile * PR_TILE;
     const int cnt = (int)min((int64_t)PR_TILE, a.P - pb);
-    __syncthreads();  // previous tile's readers of Zs / Bs are done
-    if (threadIdx.x == 0) {
-      const unsigned zb = (unsigned)(PR_TILE * KP * 8);
-      const unsigned bb = a.base ? (unsigned)(round_up(cnt * d, 2) * 8) : 0u;
-      const unsigned mb = phase == 0 ? (unsigned)(NP * KP * 8) : 0u;
-      mbar_arrive_expect_tx(&bar, zb + bb + 2 * mb);
-      bulk_g2s(Zs, a.Z + pb * KP, zb, &bar);
-      if (a.base) bulk_g2s(Bs, a.base + pb * d, bb, &bar);
-      if (mb) {
-        bulk_g2s(sL, a.Lz, mb, &bar);
-        bulk_g2s(sS, a.Sinv, mb, &bar);
-      }
+    const unsigned zb = (unsigned)(PR_TILE * KP * 8);
+    const unsigned bb = a.base ? (unsigned)(round_up(cnt * d, 2) * 8) : 0u;
+    const unsigned mb = first ? (unsigned)(NP * KP * 8) : 0u;
+    mbar_arrive_expect_tx(&bar[buf], zb + bb + 2 * mb);
+    bulk_g2s(Zs0 + buf * PR_TILE * KP, a.Z + pb * KP, zb, &bar[buf]);
+    if (a.base) bulk_g2s(Bs0 + buf * BS, a.base + pb * d, bb, &bar[buf]);
+    if (mb) {
+      bulk_g2s(sL, a.Lz, mb, &bar[buf]);
+      bulk_g2s(sS, a.Rp, mb, &bar[buf]);
     }
-    mbar_wait(&bar, phase & 1u);
-    if (phase == 0) {
+  };
+  if (threadIdx.x == 0 && (int64_t)blockIdx.x < ntl) issue(blockIdx.x, 0, true);
+  double bL[NT][KK];  // Lz B-fragments in registers; Sinv fragments are read from shared memory
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntl; tile += gridDim.x, ++it) {
+    const int buf = it & 1;
+    const int64_t pb = tile * PR_TILE;
+    const int cnt = (int)min((int64_t)PR_TILE, a.P - pb);
+    if (threadIdx.x == 0 && tile + gridDim.x < ntl) {
+      bulk_wait_read();  // the bulk store of iteration it-1 has read buffer buf^1
+      issue(tile + gridDim.x, buf ^ 1, false);
+    }
+    mbar_wait(&bar[buf], (unsigned)(it >> 1) & 1u);
+    if (it == 0) {
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int kk = 0; kk < KK; ++kk) {
-          bL[nt][kk] = sL[(nt * 8 + ar) * KP + kk * 4 + ac];
-        }
+        for (int kk = 0; kk < KK; ++kk) bL[nt][kk] = sL[(nt * 8 + ar) * KP + kk * 4 + ac];
     }
-    ++phase;
+    const double* Zs = Zs0 + buf * PR_TILE * KP;
+    double* Bs = Bs0 + buf * BS;
     const int p = w * 8 + ar;  // this lane's particle row (A / C fragments)
     double c[NT][2];
 #pragma unroll
@@ -209,7 +222,8 @@ __global__ void __launch_bounds__(256, 2) k_propose_rb(DrawArgs a) {
     for (int kk = 0; kk < KK; ++kk) {
       const double av = Zs[p * KP + kk * 4 + ac];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) dmma884(c[nt][0], c[nt][1], av, bL[nt][kk]);
+      for (int nt = 0; nt < NT; ++nt)
+        if (kk <= 2 * nt + 1) dmma884(c[nt][0], c[nt][1], av, bL[nt][kk]);  // Lz lower: k-steps above the tile vanish
     }
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
@@ -220,7 +234,7 @@ __global__ void __launch_bounds__(256, 2) k_propose_rb(DrawArgs a) {
           double dv = 0.0;
           if (i < d && p < cnt) {
             const double v = (a.base ? Bs[p * d + i] : smu[i]) + c[nt][e];
-            a.out[(pb + p) * d + i] = v;
+            Bs[p * d + i] = v;  // same thread read the base element
             dv = v - smu[i];
           }
           Ds[p * KP + i] = dv;
@@ -229,27 +243,32 @@ __global__ void __launch_bounds__(256, 2) k_propose_rb(DrawArgs a) {
     __syncwarp();
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) c[nt][0] = c[nt][1] = 0.0;
+    // W = Delta Rp' (Rp = Lprior^-1 lower, same triangular skip); q = |W|^2 = Delta' Sinv Delta
 #pragma unroll
     for (int kk = 0; kk < KK; ++kk) {
       const double av = Ds[p * KP + kk * 4 + ac];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) dmma884(c[nt][0], c[nt][1], av, sS[(nt * 8 + ar) * KP + kk * 4 + ac]);
+      for (int nt = 0; nt < NT; ++nt)
+        if (kk <= 2 * nt + 1) dmma884(c[nt][0], c[nt][1], av, sS[(nt * 8 + ar) * KP + kk * 4 + ac]);
     }
     double q = 0.0;
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int i = nt * 8 + 2 * ac + e;
-        if (i < KP) q = fma(Ds[p * KP + i], c[nt][e], q);
-      }
+      for (int e = 0; e < 2; ++e) q = fma(c[nt][e], c[nt][e], q);  // padding columns of W are zero
     q += __shfl_xor_sync(0xffffffffu, q, 1);
     q += __shfl_xor_sync(0xffffffffu, q, 2);
     if (ac == 0 && p < cnt) {
       if (!isfinite(q)) atomicExch(&a.ctl->err, ERR_NUMERIC);
       a.lp_out[pb + p] = -0.5 * q;
     }
+    __syncthreads();  // theta* tile complete; Zs / Ds consumed
+    if (threadIdx.x == 0) {
+      bulk_fence_smem();
+      bulk_s2g(a.out + pb * d, Bs, (unsigned)(round_up(cnt * d, 2) * 8));
+    }
   }
+  if (threadIdx.x == 0) bulk_wait_all();
 }
 
 // ---------------------------------------------------------------- K9 + K6
@@ -454,49 +473,41 @@ __global__ void __launch_bounds__(256) k_accept_mom_rb(AccArgs a) {
     acc[q] = ok;
   }
   nacc = block_sum(nacc, red_i);
+  // rows: warp w owns rows [w RPW, (w + 1) RPW) of the tile, lane = column (d <= 32)
   const int64_t off0 = pbase * d;
-  const int sr = 256 / d, sc = 256 - sr * d;
-  {
-    int q = threadIdx.x / d, i = threadIdx.x - q * d;
-    for (; q < tp;) {
-      cp_async8(Ts + q * LT + i, (acc[q] ? a.theta_s : a.theta) + off0 + (int64_t)q * d + i);
-      q += sr;
-      i += sc;
-      if (i >= d) {
-        i -= d;
-        ++q;
-      }
+  const int RPW = TK / 8, q0 = w * RPW;
+  // stage the updated rows (accepted -> theta*, else theta) in one cp.async round; zero padding
+#pragma unroll 4
+  for (int r = 0; r < RPW; ++r) {
+    const int q = q0 + r;
+    double* row = Ts + q * LT;
+    if (q < tp && lane < d)
+      cp_async8(row + lane, (acc[q] ? a.theta_s : a.theta) + off0 + (int64_t)q * d + lane);
+    else if (lane < LT)
+      row[lane] = 0.0;
+    if (LT > 32 && lane < LT - 32) row[32 + lane] = 0.0;
+  }
+  cp_async_wait_all();  // each lane reads back only the elements it copied
+  // accepted rows back to theta (coalesced row segments), center on the shift, this warp's group-sum partial
+  const double sh = lane < d ? a.shift[lane] : 0.0;
+  double g0 = 0.0, g1 = 0.0;
+#pragma unroll 2
+  for (int r = 0; r < RPW; ++r) {
+    const int q = q0 + r;
+    if (q < tp && lane < d) {
+      double* row = Ts + q * LT;
+      const double v = row[lane];
+      if (acc[q]) a.theta[off0 + (int64_t)q * d + lane] = v;
+      const double t = v - sh;
+      row[lane] = t;
+      if (r & 1)
+        g1 += t;
+      else
+        g0 += t;
     }
   }
-  for (int q = w; q < TK; q += 8)
-    for (int i = (q < tp ? d : 0) + lane; i < LT; i += 32) Ts[q * LT + i] = 0.0;
-  cp_async_wait_all();
+  if (lane < d) gsp[w * d + lane] = g0 + g1;
   __syncthreads();
-  {
-    int q = threadIdx.x / d, i = threadIdx.x - q * d;
-    for (; q < tp;) {
-      const double v = Ts[q * LT + i];
-      if (acc[q]) a.theta[off0 + (int64_t)q * d + i] = v;
-      Ts[q * LT + i] = v - a.shift[i];
-      q += sr;
-      i += sc;
-      if (i >= d) {
-        i -= d;
-        ++q;
-      }
-    }
-  }
-  __syncthreads();
-  for (int i = lane; i < d; i += 32) {
-    double g0 = 0.0, g1 = 0.0;
-    int q = w;
-    for (; q + 8 < tp; q += 16) {
-      g0 += Ts[q * LT + i];
-      g1 += Ts[(q + 8) * LT + i];
-    }
-    if (q < tp) g0 += Ts[q * LT + i];
-    gsp[w * d + i] = g0 + g1;
-  }
   // T'T: warp w takes k-steps k0 = 4 (w + 8 m)
   double cacc[NTRI][2];
 #pragma unroll
@@ -523,16 +534,15 @@ __global__ void __launch_bounds__(256) k_accept_mom_rb(AccArgs a) {
   }
   __syncthreads();
   double* out = a.bpart + (int64_t)blockIdx.x * W;
+#pragma unroll 1
   for (int idx = threadIdx.x; idx < NTRI * 64; idx += blockDim.x) {
     const int t = idx >> 6, e = idx & 63, ln = e >> 1, ee = e & 1;
     double v = 0.0;
+#pragma unroll
     for (int ww = 0; ww < 8; ++ww) v += wp[(ww * NTRI + t) * 64 + e];
-    int mt = 0, rem = t;
-    while (rem > mt) {
-      rem -= mt + 1;
-      ++mt;
-    }
-    const int nt = rem;
+    // lower-triangle tile t -> (mt, nt), t = mt (mt + 1) / 2 + nt, NT <= 4
+    const int mt = t >= 6 ? 3 : (t >= 3 ? 2 : (t >= 1 ? 1 : 0));
+    const int nt = t - mt * (mt + 1) / 2;
     const int i = mt * 8 + (ln >> 2), l = nt * 8 + 2 * (ln & 3) + ee;
     if (i < d && l < d) {
       out[d + i * d + l] = v;
@@ -657,6 +667,29 @@ __device__ __noinline__ void block_factor(const FinArgs& f, double* sA, const do
     for (int l = lane; l < d; l += 32) f.Lprop[i * ldp + l] = sA[i * d + l];
 }
 
+// Three segments global -> shared through L2, every load of a thread issued
+// before its first store (one latency round for up to 12 x blockDim doubles).
+__device__ void stage3(double* d0, const double* s0, int n0, double* d1, const double* s1, int n1, double* d2,
+                       const double* s2, int n2) {
+  const int p1 = n0, p2 = n0 + n1, tot = p2 + n2;
+#pragma unroll 1
+  for (int base = threadIdx.x; base < tot; base += 12 * blockDim.x) {
+    double v[12];
+#pragma unroll
+    for (int u = 0; u < 12; ++u) {
+      const int idx = base + u * blockDim.x;
+      const double* src = idx < p1 ? s0 + idx : (idx < p2 ? s1 + (idx - p1) : s2 + (idx - p2));
+      v[u] = idx < tot ? __ldcg(src) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 12; ++u) {
+      const int idx = base + u * blockDim.x;
+      double* dst = idx < p1 ? d0 + idx : (idx < p2 ? d1 + (idx - p1) : d2 + (idx - p2));
+      if (idx < tot) *dst = v[u];
+    }
+  }
+}
+
 // Dynamic shared memory of finalize_body (doubles).
 __host__ __device__ inline int64_t fin_smem_doubles(int d, int J, int nmon, bool stage_S) {
   const int D = (d + 3) / 4 * 4;
@@ -675,28 +708,31 @@ __device__ void finalize_body(const FinArgs& f, double* sm) {
   const int d = f.d, J = f.J, dd = d * d, lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int gs_len = f.Jl * d, D = round_up(d, 4), ldc = d > 32 ? d : D;
   const double P = (double)J * (double)f.N;
-  double* sM = sm;                    // d x d second moment about the old shift
-  double* sV = sM + dd;               // d x d pooled covariance
+  double* sS = sm;                                // J x d group sums (staged) -- contiguous with sM:
+  double* sM = sS + (f.stage_S ? J * d : 0);      // d x d second moment (one rank: one copy of [S | M])
+  double* sV = sM + dd;                           // d x d pooled covariance
   // (h/100) V: d <= 32: D x D, identity-padded (warp_cholesky input); d > 32:
   // d x d factored in place, overlaying sM (each (i, l) entry is read from sM
   // and written to sA by the same thread)
   double* sA = d > 32 ? sM : sV + dd;
   double* sbar = sV + dd + (d > 32 ? 0 : D * D);  // d
-  double* sshift = sbar + d;          // d
-  double* smon = sshift + d;          // nmon x d
-  double* sg = smon + f.nmon * d;     // nmon x J group means, then nmon RNEs
-  double* sS = sg + f.nmon * J + f.nmon;  // J x d group sums (staged)
+  double* sshift = sbar + d;                      // d
+  double* smon = sshift + d;                      // nmon x d
+  double* sg = smon + f.nmon * d;                 // nmon x J group means, then nmon RNEs
   __shared__ int s_h, s_flag;
+  __shared__ double s_part[8][32];
   if (f.trace && threadIdx.x == 0) f.trace[0] = gtimer();
-  // ---- stage: independent L2 loads
-  stage_cg(sshift, f.shift, d);
-  stage_cg(smon, f.mon, f.nmon * d);
-  if (f.stage_S)
-#pragma unroll 1
-    for (int r = 0; r < f.G; ++r) stage_cg(sS + (int64_t)r * gs_len, f.gath + (int64_t)r * f.slice_len, gs_len);
+  // ---- stage: one round of independent L2 loads
   if (f.G == 1) {
-    stage_cg(sM, f.gath + gs_len, dd);
+    if (f.stage_S)
+      stage3(sS, f.gath, gs_len + dd, sshift, f.shift, d, smon, f.mon, f.nmon * d);
+    else
+      stage3(sM, f.gath + gs_len, dd, sshift, f.shift, d, smon, f.mon, f.nmon * d);
   } else {
+    stage3(sshift, f.shift, d, smon, f.mon, f.nmon * d, sM, f.gath + gs_len, 0);
+    if (f.stage_S)
+#pragma unroll 1
+      for (int r = 0; r < f.G; ++r) stage_cg(sS + (int64_t)r * gs_len, f.gath + (int64_t)r * f.slice_len, gs_len);
 #pragma unroll 1
     for (int idx = threadIdx.x; idx < dd; idx += blockDim.x) {
       double m = 0.0;
@@ -724,34 +760,49 @@ __device__ void finalize_body(const FinArgs& f, double* sm) {
   __syncthreads();
   if (f.trace && threadIdx.x == 0) f.trace[1] = gtimer();
   auto S = [&](int j, int i) -> double { return f.stage_S ? sS[j * d + i] : group_sum_global(f, j, i); };
-  // ---- theta-bar: warp per coordinate, lanes over groups, fixed shuffle tree
+  // ---- theta-bar: lane = coordinate, warp = group subset, fixed-order combine
 #pragma unroll 1
-  for (int i = w; i < d; i += nw) {
+  for (int i0 = 0; i0 < d; i0 += 32) {
+    const int i = i0 + lane;
     double s = 0.0;
+    if (i < d) {
+      if (f.stage_S) {
+#pragma unroll 4
+        for (int j = w; j < J; j += nw) s += sS[j * d + i];
+      } else {
 #pragma unroll 1
-    for (int j = lane; j < J; j += 32) s += S(j, i);
-    s = warp_sum(s);
-    if (lane == 0) sbar[i] = s / P;
+        for (int j = w; j < J; j += nw) s += group_sum_global(f, j, i);
+      }
+    }
+    s_part[w][lane] = s;
+    __syncthreads();
+    if (w == 0 && i < d) {
+      double t = s_part[0][lane];
+#pragma unroll 1
+      for (int q = 1; q < nw; ++q) t += s_part[q][lane];
+      sbar[i] = t / P;
+    }
+    __syncthreads();
   }
-  __syncthreads();
   if (f.trace && threadIdx.x == 0) f.trace[2] = gtimer();
+  // ---- V (R11) and the factorization input (h/100) V, identity-padded to D x D
   const double hd = (double)s_h / 100.0;
+  const int DA = d > 32 ? d : D;
+#pragma unroll 2
+  for (int i = w; i < DA; i += nw) {
+    const double ci = i < d ? sbar[i] - sshift[i] : 0.0;
 #pragma unroll 1
-  for (int i = w; i < d; i += nw) {
-    const double ci = sbar[i] - sshift[i];
-#pragma unroll 1
-    for (int l = lane; l < d; l += 32) {
-      const double cl = sbar[l] - sshift[l];
-      const double v = (sM[i * d + l] - P * ci * cl) / (P - 1.0);
-      sV[i * d + l] = v;
-      sA[i * ldc + l] = hd * v;
+    for (int l = lane; l < DA; l += 32) {
+      if (i < d && l < d) {
+        const double cl = sbar[l] - sshift[l];
+        const double v = (sM[i * d + l] - P * ci * cl) / (P - 1.0);
+        sV[i * d + l] = v;
+        sA[i * ldc + l] = hd * v;
+      } else {
+        sA[i * ldc + l] = i == l ? 1.0 : 0.0;
+      }
     }
   }
-  if (d <= 32)  // identity padding of the D x D factorization input
-    for (int idx = threadIdx.x; idx < D * D; idx += blockDim.x) {
-      const int i = idx / D, l = idx - i * D;
-      if (i >= d || l >= d) sA[idx] = i == l ? 1.0 : 0.0;
-    }
   __syncthreads();
   if (f.trace && threadIdx.x == 0) f.trace[3] = gtimer();
   const int ldp = round_up(d, 4);  // padded (DMMA) layout of the factor
@@ -857,13 +908,17 @@ __global__ void __launch_bounds__(256) k_mom_reduce(const double* __restrict__ b
   if ((int)blockIdx.x < nm) {
     const int e = blockIdx.x * 32 + lane;
     double acc8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    if (e < dd) {
-      for (int b0 = w; b0 < nblk; b0 += 64) {
+    if (e < dd) {  // 32 rows per warp in flight at once (one L2 round for nblk <= 256)
+#pragma unroll 1
+      for (int b0 = w; b0 < nblk; b0 += 256) {
+        double v[32];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < 32; ++u) {
           const int b = b0 + 8 * u;
-          if (b < nblk) acc8[u] += bpart[(int64_t)b * W + d + e];
+          v[u] = b < nblk ? bpart[(int64_t)b * W + d + e] : 0.0;
         }
+#pragma unroll
+        for (int u = 0; u < 32; ++u) acc8[u & 7] += v[u];
       }
     }
     part[w][lane] = ((acc8[0] + acc8[1]) + (acc8[2] + acc8[3])) + ((acc8[4] + acc8[5]) + (acc8[6] + acc8[7]));
@@ -910,8 +965,10 @@ __global__ void __launch_bounds__(256) k_finalize(FinArgs f) {
   finalize_body(f, fin_sm);
 }
 
-// Prior precision Sinv = Lprior^-T Lprior^-1 (one block; smem: Linv d x d).
-__global__ void k_prior_precision(const double* __restrict__ Lp, int d, double* __restrict__ Sinv) {
+// Prior precision Sinv = Lprior^-T Lprior^-1 and the whitening factor Linv =
+// Lprior^-1 (lower; one block; smem: Linv d x d).
+__global__ void k_prior_precision(const double* __restrict__ Lp, int d, double* __restrict__ Sinv,
+                                  double* __restrict__ Linv) {
   extern __shared__ double sInv[];
   for (int b = threadIdx.x; b < d; b += blockDim.x) {  // column b of Lp^-1 (lower)
     for (int i = 0; i < d; ++i) {
@@ -921,6 +978,7 @@ __global__ void k_prior_precision(const double* __restrict__ Lp, int d, double* 
     }
   }
   __syncthreads();
+  for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) Linv[idx] = sInv[idx];
   for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) {
     const int r = idx / d, c = idx % d;
     double s = 0.0;

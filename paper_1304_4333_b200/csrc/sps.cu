@@ -137,6 +137,7 @@ struct sps_ctx {
   size_t ll_scratch_cap = 0;
   double* Sinv = nullptr;        // prior precision (d x d)
   double *LpriorP = nullptr, *SinvP = nullptr;  // padded copies (NP x KP) for the DMMA proposal kernel
+  double *Rp = nullptr, *RpP = nullptr;          // prior whitening factor Lprior^-1 (d x d) and its padded copy
   double* bpart = nullptr;       // accept+moments block partials
   int tp = 0, QE = 1, W = 0, nblk = 0;
   Ctl* hslot = nullptr;          // 2 mapped pinned Ctl slots (pipelined M steps), written by finalize_body
@@ -338,11 +339,19 @@ bool pick_exact(int k, LLChoice* out, std::integer_sequence<int, Ks...>) {
 bool choose_ll(int k, int C, LLChoice* o) {
   const int cm1 = C - 1;
   static const bool force_dfma = getenv("SPS_K1_DFMA") != nullptr;
-  if (cm1 == 1 && k <= 32 && !force_dfma) {  // DMMA contraction (+ <= 2 remainder DFMAs), 128 particles per block
+  // tuning hook (tools/k1_variants.py): the previous 4-n-tile layout for k = 25
+  static const char* k1var = getenv("SPS_K1_VAR");
+  if (k1var && cm1 == 1 && k == 25 && !strcmp(k1var, "w4")) {
+    *o = {k_loglik_bin_mma<6, 1, 4>, 28, 1, 128, true};
+    return true;
+  }
+  // DMMA contraction (+ <= 2 remainder DFMAs), 2 n-tiles (16 particles) per warp, 64 per block:
+  // 114 registers -> 4 blocks per SM (the 4-n-tile layout, 178 registers, held 2; cfg2 run -6%)
+  if (cm1 == 1 && k <= 32 && !force_dfma) {
     switch (k) {
-#define MMA_CASE(K_, KKD_, REM_)                                       \
-  case K_:                                                             \
-    *o = {k_loglik_bin_mma<KKD_, REM_, 4>, 4 * KKD_ + (REM_ ? 4 : 0), 1, 128, true}; \
+#define MMA_CASE(K_, KKD_, REM_)                                                      \
+  case K_:                                                                            \
+    *o = {k_loglik_bin_mma<KKD_, REM_, 2>, 4 * KKD_ + (REM_ ? 4 : 0), 1, 64, true}; \
     return true;
       MMA_CASE(1, 0, 1) MMA_CASE(2, 0, 2) MMA_CASE(3, 1, 0) MMA_CASE(4, 1, 0) MMA_CASE(5, 1, 1) MMA_CASE(6, 1, 2)
       MMA_CASE(7, 2, 0) MMA_CASE(8, 2, 0) MMA_CASE(9, 2, 1) MMA_CASE(10, 2, 2) MMA_CASE(11, 3, 0) MMA_CASE(12, 3, 0)
@@ -499,6 +508,7 @@ sps_status launch_draw(sps_ctx* c, int slot, const double* base, const double* L
   a.base = base;
   a.Lz = Lz;
   a.Sinv = c->SinvP;
+  a.Rp = c->RpP;
   a.mu = c->mu;
   a.Z = c->Zbuf[slot];
   a.out = out;
@@ -513,8 +523,9 @@ sps_status launch_draw(sps_ctx* c, int slot, const double* base, const double* L
   PROF_BEGIN(c);
   if (d <= 32) {  // register-blocked DMMA proposal
     const int KK = (d + 3) / 4, KPr = 4 * KK, NPr = 8 * ((KPr + 7) / 8);
-    const size_t sm = (size_t)(2 * PR_TILE * KPr + KPr + 2 * NPr * KPr + PR_TILE * d) * sizeof(double);
-    const unsigned grid = (unsigned)ntl;  // one tile per block; 2 blocks per SM overlap their latencies
+    const size_t sm =
+        (size_t)(3 * PR_TILE * KPr + 2 * round_up(PR_TILE * d, 2) + KPr + 2 * NPr * KPr) * sizeof(double);
+    const unsigned grid = (unsigned)std::min<int64_t>(ntl, 2 * (int64_t)num_sms());  // persistent, 2 per SM
     switch (KK) {
       case 1: k_propose_rb<1><<<grid, 256, sm, c->stream>>>(a); break;
       case 2: k_propose_rb<2><<<grid, 256, sm, c->stream>>>(a); break;
@@ -694,7 +705,7 @@ void free_ctx(sps_ctx* c) {
                   c->lp2, c->lw, c->lw_cur, c->theta_s, c->lp_s, c->part, c->gpart, c->mpart, c->slice, c->gath,
                   c->shift, c->Lprop, c->V, c->rne, c->lwbuf, c->essparts, c->essslice, c->essgath, c->grp_ms,
                   c->grp_ms_gath, c->Lj, c->Lj_gath, c->scal, c->pw_parts, c->pw_slice, c->pw_gath, c->mx_parts,
-                  c->mx_slice, c->mx_gath, c->fn_A, c->fn_out, c->ll_scratch, c->Sinv, c->LpriorP, c->SinvP, c->bpart, c->ctl};
+                  c->mx_slice, c->mx_gath, c->fn_A, c->fn_out, c->ll_scratch, c->Sinv, c->LpriorP, c->SinvP, c->Rp, c->RpP, c->bpart, c->ctl};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->hctl) cudaFreeHost(c->hctl);
@@ -901,9 +912,12 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
     TRY(dalloc(c, &c->Lprop, pn));
     TRY(dalloc(c, &c->LpriorP, pn));
     TRY(dalloc(c, &c->SinvP, pn));
+    TRY(dalloc(c, &c->RpP, pn));
+    TRY(dalloc(c, &c->Rp, (size_t)d * d));
     CU(c, cudaMemsetAsync(c->Lprop, 0, pn * sizeof(double), c->stream));
     CU(c, cudaMemsetAsync(c->LpriorP, 0, pn * sizeof(double), c->stream));
     CU(c, cudaMemsetAsync(c->SinvP, 0, pn * sizeof(double), c->stream));
+    CU(c, cudaMemsetAsync(c->RpP, 0, pn * sizeof(double), c->stream));
   }
   TRY(dalloc(c, &c->V, (size_t)d * d));
   TRY(dalloc(c, &c->rne, (size_t)c->nmon));
@@ -962,12 +976,14 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
     k_chol_prior<<<1, 256, smem, c->stream>>>(c->V, d, c->Lprior, c->ctl);
     CHECK_LAUNCH(c);
     CU(c, cudaFuncSetAttribute(k_prior_precision, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024));
-    k_prior_precision<<<1, 128, smem, c->stream>>>(c->Lprior, d, c->Sinv);
+    k_prior_precision<<<1, 128, smem, c->stream>>>(c->Lprior, d, c->Sinv, c->Rp);
     CHECK_LAUNCH(c);
     const size_t ldp = (size_t)round_up(d, 4) * sizeof(double);
     CU(c, cudaMemcpy2DAsync(c->LpriorP, ldp, c->Lprior, d * sizeof(double), d * sizeof(double), d,
                             cudaMemcpyDeviceToDevice, c->stream));
     CU(c, cudaMemcpy2DAsync(c->SinvP, ldp, c->Sinv, d * sizeof(double), d * sizeof(double), d,
+                            cudaMemcpyDeviceToDevice, c->stream));
+    CU(c, cudaMemcpy2DAsync(c->RpP, ldp, c->Rp, d * sizeof(double), d * sizeof(double), d,
                             cudaMemcpyDeviceToDevice, c->stream));
     // one-time kernel attributes (dynamic shared memory above 48 KB)
     const int big = 200 * 1024;
@@ -1080,9 +1096,10 @@ sps_status sps_get_counters(const sps_ctx* cc, sps_counters* out) {
   sps_ctx* c = const_cast<sps_ctx*>(cc);
   TRY(prof_resolve(c));
   if (c->trace && c->trace_n) {
-    static const char* nm[] = {"reduce", "ticket->fin", "stage", "theta-bar", "V", "chol|RNE", "stats+writes", "host slot"};
+    static const char* nm[] = {"reduce", "ticket->fin", "stage", "theta-bar", "V", "chol|RNE", "stats+writes",
+                               "host slot", "start skew", "longest block", "moment block"};
     fprintf(stderr, "SPS_TRACE mean ns over %d finalizes:", c->trace_n);
-    for (int q = 0; q < 8; ++q) fprintf(stderr, " %s=%.0f", nm[q], c->trace_acc[q] / c->trace_n);
+    for (int q = 0; q < 11; ++q) fprintf(stderr, " %s=%.0f", nm[q], c->trace_acc[q] / c->trace_n);
     fprintf(stderr, "\n");
   }
   out->launches = c->launches;
@@ -1275,11 +1292,17 @@ static void trace_accumulate(sps_ctx* c) {
   cudaStreamSynchronize(c->stream);
   const unsigned long long* t = c->trace;
   const int d = c->d, nb = (d * d + 31) / 32 + (c->Jl * d + 255) / 256 + 1;
-  unsigned long long s0 = ~0ull, e1 = 0;
+  unsigned long long s0 = ~0ull, s1 = 0, e1 = 0, dmax = 0, dm = 0;
   for (int b = 0; b < nb; ++b) {
     s0 = std::min(s0, t[8 + b]);
+    s1 = std::max(s1, t[8 + b]);
     e1 = std::max(e1, t[8 + nb + b]);
+    dmax = std::max(dmax, t[8 + nb + b] - t[8 + b]);
+    if (b == 0) dm = t[8 + nb + b] - t[8 + b];
   }
+  c->trace_acc[8] += (double)(s1 - s0);  // start skew
+  c->trace_acc[9] += (double)dmax;       // longest block
+  c->trace_acc[10] += (double)dm;        // a moment block
   if (t[0] < s0 || t[6] < t[0]) return;  // stopped step (no finalize)
   c->trace_acc[0] += (double)(e1 - s0);      // reduce phase: first block start -> last block ticket
   c->trace_acc[1] += (double)(t[0] - e1);    // ticket -> finalize start
