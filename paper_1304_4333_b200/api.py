@@ -154,7 +154,7 @@ class Sps:
         c = Counters()
         _check(lib().sps_get_counters(self.ctx, C.byref(c)), self.ctx)
         cats = ["k1", "propose", "accept_moments", "moments_reduce", "gather", "finalize", "ctl_copy", "cphase",
-                "resample", "other", "c10", "c11", "c12", "c13", "host_mstep_launch", "host_mstep_wait"]
+                "resample", "other", "c10", "c11", "c12", "host_graph_build", "host_mstep_launch", "host_mstep_wait"]
         return dict(launches=c.launches, k1_launches=c.k1_launches, k1_pairs=c.k1_pairs, k1_ms=c.k1_ms,
                     syncs=c.syncs, cat_ms={k: c.cat_ms[i] for i, k in enumerate(cats)},
                     cat_n={k: c.cat_n[i] for i, k in enumerate(cats)})

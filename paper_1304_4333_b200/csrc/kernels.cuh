@@ -25,7 +25,7 @@ struct Ctl {
   double ess;      // ESS at the cycle end (diagnostic)
   unsigned long long q_lo, q_hi;  // power search bracket on the 2^-48 grid
   int q_ok_full;   // ESS(1 - phi) >= threshold
-  int pad1;
+  uint32_t step_cur;  // M step of the running proposal (written by K8; the next step's normals use step_cur + 1)
 };
 
 // ============================================================ data preparation

@@ -29,6 +29,8 @@ struct DrawArgs {
   const int* stop;
   int64_t P, p0;
   int d;
+  uint32_t step0;  // set_step: ctl->step_cur = step0 + ctl->steps_done (device-resident step of a graph replay)
+  int set_step;
 };
 
 // Standard normals of the streams (id = p0 + p, step, tag) for every local
@@ -37,11 +39,15 @@ struct DrawArgs {
 // one M step ahead on a side stream, overlapped with the latency-bound kernels.
 // With `logu` (PROPOSAL streams), also plog of the step's ACCEPT uniform of each
 // particle (R16), so the accept test on the critical path is one comparison.
+// With `sctl` (M steps replayed from a CUDA graph) the step is device-resident:
+// step = sctl->step_cur + 1, written by the proposal kernel of the running step.
 __global__ void __launch_bounds__(256) k_normals(int64_t P, int64_t p0, int np, int ldz, uint64_t seed, uint32_t step,
                                                  uint32_t tag, uint32_t pass, double* __restrict__ Z,
-                                                 double* __restrict__ logu) {
+                                                 double* __restrict__ logu, const Ctl* sctl, const int* stop) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= P * np) return;
+  if (stop && *stop) return;
+  if (sctl) step = sctl->step_cur + 1u;
   const int64_t p = t / np;
   const int pr = (int)(t - p * np);
   double z0, z1;
@@ -64,6 +70,7 @@ template <bool STAGE>
 __global__ void __launch_bounds__(256) k_propose(DrawArgs a) {
   extern __shared__ double sm[];
   if (a.stop && *a.stop) return;
+  if (a.set_step && blockIdx.x == 0 && threadIdx.x == 0) a.ctl->step_cur = a.step0 + (uint32_t)a.ctl->steps_done;
   const int d = a.d, np = (d + 1) / 2, d2 = 2 * np, KP = round_up(d, 4), NP = round_up(d, 8), NT = NP / 8;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   double* Zs = sm;                  // PR_TILE x KP
@@ -163,6 +170,7 @@ __global__ void __launch_bounds__(256, 2) k_propose_rb(DrawArgs a) {
   constexpr int KP = 4 * KK, NT = (KP + 7) / 8, NP = 8 * NT;
   extern __shared__ __align__(16) double sm[];
   if (a.stop && *a.stop) return;
+  if (a.set_step && blockIdx.x == 0 && threadIdx.x == 0) a.ctl->step_cur = a.step0 + (uint32_t)a.ctl->steps_done;
   const int d = a.d, BS = round_up(PR_TILE * d, 2);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, ar = lane >> 2, ac = lane & 3;
   double* Zs0 = sm;                     // 2 x PR_TILE x KP

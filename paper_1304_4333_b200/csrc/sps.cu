@@ -151,6 +151,12 @@ struct sps_ctx {
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_zready[2] = {nullptr, nullptr}, ev_zfree[2] = {nullptr, nullptr};
   cudaEvent_t evs[2] = {nullptr, nullptr};
+  // M steps replayed from CUDA graphs (one per slot parity, captured per M phase; one rank)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+  int64_t g_launches[2] = {0, 0}, g_k1[2] = {0, 0};
+  double g_pairs[2] = {0, 0};
+  int graph_updates = 0, graph_instantiations = 0;
   LLChoice_t llc{};
   int ll_regs = 0;
   struct Plan {
@@ -167,6 +173,7 @@ struct sps_ctx {
   double phi = 0.0;     // tempering level (power mode)
   int ell = 0;          // cycles completed
   uint32_t mstep = 0;   // global M-step counter (PROPOSAL / ACCEPT streams)
+  uint32_t phase_step0 = 0;  // first M step of the running M phase
   bool need_pre_moments = false;
   bool cphase_done = false;  // a C phase ran since the last M phase
   bool finished = false;
@@ -184,7 +191,7 @@ struct sps_ctx {
   std::vector<std::pair<int, int>> prof_open; // (event index pair base, category) awaiting resolution
   int prof_next = 0;
   int prof_cur = -1;
-  double host_launch_us = 0.0, host_wait_us = 0.0;
+  double host_launch_us = 0.0, host_wait_us = 0.0, host_graph_us = 0.0;
   std::string err;
 };
 
@@ -481,25 +488,28 @@ sps_status launch_loglik(sps_ctx* c, const double* theta, int64_t ldt, int64_t P
 
 // Standard normals of (step, tag) for every local particle into Zbuf[slot], on
 // the side stream `aux` (waits until Zbuf[slot] is free; signals ev_zready).
-sps_status launch_normals(sps_ctx* c, uint32_t tag, uint32_t step, int slot) {
+// graph: inside an M-step capture -- forked from the main stream after the
+// proposal (ev_fork), step = ctl->step_cur + 1 on the device, joined back
+// through ev_join (graph replays are stream-ordered: no Zbuf events needed).
+sps_status launch_normals(sps_ctx* c, uint32_t tag, uint32_t step, int slot, bool graph = false) {
   const int np = (c->d + 1) / 2;
   static const bool serial = getenv("SPS_SERIAL_NORMALS") != nullptr;  // debug: no overlap, own profile category
-  cudaStream_t st = serial ? c->stream : c->aux;
-  CU(c, cudaStreamWaitEvent(st, c->ev_zfree[slot], 0));
+  cudaStream_t st = serial && !graph ? c->stream : c->aux;
+  CU(c, cudaStreamWaitEvent(st, graph ? c->ev_fork : c->ev_zfree[slot], 0));
   const int64_t tasks = c->Pl * np;
-  if (serial) PROF_BEGIN(c);
-  k_normals<<<(unsigned)((tasks + 255) / 256), 256, 0, st>>>(c->Pl, c->p0, np, round_up(c->d, 4), c->cfg.seed,
-                                                                 step, tag, (uint32_t)c->cfg.pass, c->Zbuf[slot],
-                                                                 tag == TAG_PROPOSAL ? c->LUbuf[slot] : nullptr);
+  if (serial && !graph) PROF_BEGIN(c);
+  k_normals<<<(unsigned)((tasks + 255) / 256), 256, 0, st>>>(
+      c->Pl, c->p0, np, round_up(c->d, 4), c->cfg.seed, step, tag, (uint32_t)c->cfg.pass, c->Zbuf[slot],
+      tag == TAG_PROPOSAL ? c->LUbuf[slot] : nullptr, graph ? c->ctl : nullptr, graph ? &c->ctl->stop : nullptr);
   CHECK_LAUNCH(c);
-  if (serial) PROF_END(c, CAT_OTHER);
-  CU(c, cudaEventRecord(c->ev_zready[slot], st));
+  if (serial && !graph) PROF_END(c, CAT_OTHER);
+  CU(c, cudaEventRecord(graph ? c->ev_join : c->ev_zready[slot], st));
   return SPS_OK;
 }
 
 // K8 / K10: theta = base + Lz z with z = Zbuf[slot], lp = prior kernel.
 sps_status launch_draw(sps_ctx* c, int slot, const double* base, const double* Lz, double* out, double* lp_out,
-                       const int* stop) {
+                       const int* stop, bool graph = false, bool set_step = false) {
   const int d = c->d, KP = round_up(d, 4), NP = round_up(d, 8);
   const size_t base_sm = (size_t)(2 * PR_TILE * KP + PR_TILE * (NP / 8) + KP + PR_TILE * d);
   const bool stage = (base_sm + 2 * (size_t)NP * KP) * sizeof(double) <= 160 * 1024;
@@ -518,7 +528,9 @@ sps_status launch_draw(sps_ctx* c, int slot, const double* base, const double* L
   a.P = c->Pl;
   a.p0 = c->p0;
   a.d = d;
-  CU(c, cudaStreamWaitEvent(c->stream, c->ev_zready[slot], 0));
+  a.step0 = c->phase_step0;
+  a.set_step = set_step ? 1 : 0;
+  if (!graph) CU(c, cudaStreamWaitEvent(c->stream, c->ev_zready[slot], 0));
   const int64_t ntl = (c->Pl + PR_TILE - 1) / PR_TILE;
   PROF_BEGIN(c);
   if (d <= 32) {  // register-blocked DMMA proposal
@@ -691,15 +703,19 @@ void free_ctx(sps_ctx* c) {
   if (c->G == 1) {  // aliases of the local slices
     c->gath = c->essgath = c->grp_ms_gath = c->Lj_gath = c->pw_gath = c->mx_gath = nullptr;
   }
+  if (c->aux) cudaStreamSynchronize(c->aux);
+  if (c->stream) cudaStreamSynchronize(c->stream);
   for (double* z : c->Zbuf)
     if (z) cudaFree(z);
   for (double* z : c->LUbuf)
     if (z) cudaFree(z);
-  if (c->aux) cudaStreamSynchronize(c->aux);
   for (int q = 0; q < 2; ++q) {
+    if (c->gexec[q]) cudaGraphExecDestroy(c->gexec[q]);
     if (c->ev_zready[q]) cudaEventDestroy(c->ev_zready[q]);
     if (c->ev_zfree[q]) cudaEventDestroy(c->ev_zfree[q]);
   }
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->aux) cudaStreamDestroy(c->aux);
   void* ptrs[] = {c->X, c->Xs, c->mu, c->Lprior, c->xbar, c->mon, c->y, c->theta, c->theta2, c->L, c->L2, c->lp,
                   c->lp2, c->lw, c->lw_cur, c->theta_s, c->lp_s, c->part, c->gpart, c->mpart, c->slice, c->gath,
@@ -886,6 +902,8 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
   if (getenv("SPS_TRACE")) CU(c, cudaMallocManaged((void**)&c->trace, 128 * sizeof(unsigned long long)));
   CU(c, cudaMemsetAsync(c->ticket, 0, sizeof(unsigned), c->stream));
   CU(c, cudaEventCreateWithFlags(&c->evs[0], cudaEventDisableTiming));
+  CU(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  CU(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   CU(c, cudaEventCreateWithFlags(&c->evs[1], cudaEventDisableTiming));
   TRY(dalloc(c, &c->slice, (size_t)c->slice_len));
   if (c->G > 1) TRY(dalloc(c, &c->gath, (size_t)c->slice_len * c->G));
@@ -1054,7 +1072,8 @@ sps_status sps_reset(sps_ctx* c, uint64_t seed, int32_t pass) {
   c->tr_rne.clear();
   c->launches = c->k1_launches = c->syncs = 0;
   c->k1_pairs = c->k1_ms = 0.0;
-  c->host_launch_us = c->host_wait_us = 0.0;
+  c->host_launch_us = c->host_wait_us = c->host_graph_us = 0.0;
+  c->graph_updates = c->graph_instantiations = 0;
   for (int q = 0; q < 16; ++q) {
     c->cat_ms[q] = 0.0;
     c->cat_n[q] = 0;
@@ -1114,6 +1133,8 @@ sps_status sps_get_counters(const sps_ctx* cc, sps_counters* out) {
     out->cat_ms[q] = c->cat_ms[q];
     out->cat_n[q] = c->cat_n[q];
   }
+  out->cat_ms[13] = c->host_graph_us / 1e3;  // host: M-step graph capture + update / instantiate
+  out->cat_n[13] = c->graph_updates + 1000 * c->graph_instantiations;
   return SPS_OK;
 }
 
@@ -1312,23 +1333,84 @@ static void trace_accumulate(sps_ctx* c) {
 
 // One M step (Algorithm 2 step 2(c)), fully enqueued:
 // K8 propose -> K1 loglik of theta* on [0, t_l) -> K9+K6 accept & moments ->
-// stats reduce -> gather -> K7 finalize (h, RNE, stop, chol(h V)) -> D2H of
-// the control block into pinned slot `slot`, event evs[slot].  Every kernel
-// returns at once when the device stop flag is already set, so a step
-// launched speculatively after the stopping step is a no-op.
-static sps_status launch_mstep(sps_ctx* c, uint32_t step, int slot, bool allow_stop) {
+// stats reduce -> gather -> K7 finalize (h, RNE, stop, chol(h V)) -> control
+// block into mapped host slot `step & 1`, event evs[step & 1]; the next step's
+// normals run alongside on the side stream.  Every kernel returns at once when
+// the device stop flag is already set, so a step launched speculatively after
+// the stopping step is a no-op.  graph: captured for replay (only the parity of
+// `step` matters; the step number itself is device-resident).
+static sps_status launch_mstep(sps_ctx* c, uint32_t step, bool allow_stop, bool graph = false) {
   const bool power = c->cfg.tempering == SPS_POWER_TEMPERING;
   const int t1 = power ? c->n : c->t;
   const double temper = power ? c->phi : 1.0;
   const int* stop = &c->ctl->stop;
   const int zs = (int)(step & 1u);
-  TRY(launch_draw(c, zs, c->theta, c->Lprop, c->theta_s, c->lp_s, stop));
-  TRY(launch_normals(c, TAG_PROPOSAL, step + 1u, (int)((step + 1u) & 1u)));  // next step's normals, overlapped
+  TRY(launch_draw(c, zs, c->theta, c->Lprop, c->theta_s, c->lp_s, stop, graph, true));
+  if (graph) CU(c, cudaEventRecord(c->ev_fork, c->stream));
+  TRY(launch_normals(c, TAG_PROPOSAL, step + 1u, zs ^ 1, graph));  // next step's normals, overlapped
   int nch = 1;
   TRY(launch_loglik(c, c->theta_s, c->d, c->Pl, 0, t1, c->part, c->max_chunks, &nch, stop));
-  TRY(moments_finalize(c, true, nch, temper, step, stop, c->LUbuf[zs], 1, allow_stop, slot));
-  CU(c, cudaEventRecord(c->ev_zfree[zs], c->stream));  // Zbuf / LUbuf[zs] consumed
-  CU(c, cudaEventRecord(c->evs[slot], c->stream));
+  TRY(moments_finalize(c, true, nch, temper, step, stop, c->LUbuf[zs], 1, allow_stop, zs));
+  if (graph) {
+    CU(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+    CU(c, cudaEventRecordWithFlags(c->evs[zs], c->stream, cudaEventRecordExternal));
+  } else {
+    CU(c, cudaEventRecord(c->ev_zfree[zs], c->stream));  // Zbuf / LUbuf[zs] consumed
+    CU(c, cudaEventRecord(c->evs[zs], c->stream));
+  }
+  return SPS_OK;
+}
+
+// Capture the M step of both slot parities for this phase (t1, tempering, K
+// fixed) and instantiate, or update the executable graphs of the previous phase
+// in place (same topology; only kernel parameters and grids change).
+static sps_status build_mstep_graphs(sps_ctx* c, bool allow_stop) {
+  for (int par = 0; par < 2; ++par) {
+    const int64_t l0 = c->launches, k0 = c->k1_launches;
+    const double p0 = c->k1_pairs;
+    CU(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    const sps_status st = launch_mstep(c, c->phase_step0 + (uint32_t)((par ^ (int)(c->phase_step0 & 1u)) & 1), allow_stop,
+                                       true);
+    cudaGraph_t g = nullptr;
+    const cudaError_t ee = cudaStreamEndCapture(c->stream, &g);
+    if (st != SPS_OK) {
+      if (g) cudaGraphDestroy(g);
+      return st;
+    }
+    CU(c, ee);
+    c->g_launches[par] = c->launches - l0;
+    c->g_k1[par] = c->k1_launches - k0;
+    c->g_pairs[par] = c->k1_pairs - p0;
+    c->launches = l0;
+    c->k1_launches = k0;
+    c->k1_pairs = p0;
+    bool ok = false;
+    if (c->gexec[par]) {
+      cudaGraphExecUpdateResultInfo info;
+      ok = cudaGraphExecUpdate(c->gexec[par], g, &info) == cudaSuccess;
+      if (ok) c->graph_updates += 1;
+      cudaGetLastError();
+    }
+    if (!ok) {
+      if (c->gexec[par]) cudaGraphExecDestroy(c->gexec[par]);
+      c->gexec[par] = nullptr;
+      const cudaError_t ei = cudaGraphInstantiate(&c->gexec[par], g, 0);
+      cudaGraphDestroy(g);
+      CU(c, ei);
+      c->graph_instantiations += 1;
+    } else {
+      cudaGraphDestroy(g);
+    }
+  }
+  return SPS_OK;
+}
+
+static sps_status replay_mstep(sps_ctx* c, uint32_t step) {
+  const int par = (int)(step & 1u);
+  CU(c, cudaGraphLaunch(c->gexec[par], c->stream));
+  c->launches += c->g_launches[par];
+  c->k1_launches += c->g_k1[par];
+  c->k1_pairs += c->g_pairs[par];
   return SPS_OK;
 }
 
@@ -1348,22 +1430,37 @@ sps_status sps_mphase(sps_ctx* c, int32_t R_fixed, int32_t* R_out, double* min_r
     c->need_pre_moments = false;
   }
   const uint32_t step0 = c->mstep;
+  c->phase_step0 = step0;
+  static const bool no_graph = getenv("SPS_NO_GRAPH") != nullptr;
+  const bool graph = c->G == 1 && !c->profiling && !no_graph;
+  // the first step's normals after all earlier work of the main stream (graph replays record no Zbuf events)
+  CU(c, cudaEventRecord(c->ev_zfree[step0 & 1u], c->stream));
   TRY(launch_normals(c, TAG_PROPOSAL, step0, (int)(step0 & 1u)));
-  TRY(launch_mstep(c, step0, 0, adaptive));
+  if (graph) {
+    const auto g0 = std::chrono::steady_clock::now();
+    TRY(build_mstep_graphs(c, adaptive));
+    c->host_graph_us +=
+        std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - g0).count();
+    CU(c, cudaStreamWaitEvent(c->stream, c->ev_zready[step0 & 1u], 0));
+  }
+  auto launch_step = [&](uint32_t s) -> sps_status {
+    return graph ? replay_mstep(c, s) : launch_mstep(c, s, adaptive);
+  };
+  TRY(launch_step(step0));
   int r = 1;
   Ctl got{};
   for (;;) {
     // keep one step queued behind the one being checked
     auto h0 = std::chrono::steady_clock::now();
-    if (r < Rmax) TRY(launch_mstep(c, step0 + (uint32_t)r, r % 2, adaptive));
+    if (r < Rmax) TRY(launch_step(step0 + (uint32_t)r));
     auto h1 = std::chrono::steady_clock::now();
-    CU(c, cudaEventSynchronize(c->evs[(r - 1) % 2]));
+    CU(c, cudaEventSynchronize(c->evs[(step0 + (uint32_t)r - 1u) & 1u]));
     auto h2 = std::chrono::steady_clock::now();
     c->host_launch_us += std::chrono::duration<double, std::micro>(h1 - h0).count();
     c->host_wait_us += std::chrono::duration<double, std::micro>(h2 - h1).count();
     c->syncs += 1;
     if (c->trace) trace_accumulate(c);
-    got = c->hslot[(r - 1) % 2];
+    got = c->hslot[(step0 + (uint32_t)r - 1u) & 1u];
     c->pairs += (double)c->P * t1;
     if (got.err == ERR_NUMERIC)
       return fail(c, SPS_E_NUMERIC, "numerical failure in the M phase (non-finite loglik or Cholesky failure "
