@@ -160,23 +160,23 @@ __global__ void __launch_bounds__(256) k_propose(DrawArgs a) {
 
 // Register-blocked variant for d <= 32 (KK = round_up(d,4)/4 k-steps, NT =
 // round_up(d,8)/8 column tiles): warp w owns particle rows 8w..8w+7 of the
-// tile; the Lz B-fragments live in registers, so a DMMA costs one shared load
-// of its A fragment.  Persistent (grid ~2 blocks per SM) and double-buffered:
+// tile (A / C fragments in registers; Lz, Rp fragments from shared memory;
+// k-steps above the lower-triangular factors skipped).  Persistent (3 blocks
+// per SM) and double-buffered:
 // the TMA loads of the block's next tile (Z rows, base rows) are in flight
 // while the current tile computes; theta* is assembled in shared memory over
 // the base rows and leaves as one TMA bulk store (contiguous rows).
 template <int KK>
-__global__ void __launch_bounds__(256, 2) k_propose_rb(DrawArgs a) {
+__global__ void __launch_bounds__(256, 3) k_propose_rb(DrawArgs a) {
   constexpr int KP = 4 * KK, NT = (KP + 7) / 8, NP = 8 * NT;
   extern __shared__ __align__(16) double sm[];
   if (a.stop && *a.stop) return;
   if (a.set_step && blockIdx.x == 0 && threadIdx.x == 0) a.ctl->step_cur = a.step0 + (uint32_t)a.ctl->steps_done;
   const int d = a.d, BS = round_up(PR_TILE * d, 2);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, ar = lane >> 2, ac = lane & 3;
-  double* Zs0 = sm;                     // 2 x PR_TILE x KP
+  double* Zs0 = sm;                     // 2 x PR_TILE x KP: Z rows, then (theta* - mu) rows (per warp, in place)
   double* Bs0 = Zs0 + 2 * PR_TILE * KP;  // 2 x BS: base rows, overwritten with theta*
-  double* Ds = Bs0 + 2 * BS;            // PR_TILE x KP (theta* - mu)
-  double* smu = Ds + PR_TILE * KP;      // KP
+  double* smu = Bs0 + 2 * BS;           // KP
   double* sL = smu + KP;                // NP x KP
   double* sS = sL + NP * KP;            // NP x KP (Rp)
   __shared__ __align__(8) uint64_t bar[2];
@@ -203,7 +203,6 @@ __global__ void __launch_bounds__(256, 2) k_propose_rb(DrawArgs a) {
     }
   };
   if (threadIdx.x == 0 && (int64_t)blockIdx.x < ntl) issue(blockIdx.x, 0, true);
-  double bL[NT][KK];  // Lz B-fragments in registers; Sinv fragments are read from shared memory
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < ntl; tile += gridDim.x, ++it) {
     const int buf = it & 1;
@@ -214,13 +213,8 @@ __global__ void __launch_bounds__(256, 2) k_propose_rb(DrawArgs a) {
       issue(tile + gridDim.x, buf ^ 1, false);
     }
     mbar_wait(&bar[buf], (unsigned)(it >> 1) & 1u);
-    if (it == 0) {
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-        for (int kk = 0; kk < KK; ++kk) bL[nt][kk] = sL[(nt * 8 + ar) * KP + kk * 4 + ac];
-    }
-    const double* Zs = Zs0 + buf * PR_TILE * KP;
+    double* Zs = Zs0 + buf * PR_TILE * KP;
+    double* Ds = Zs;  // a warp's Z rows are dead once its first product is done
     double* Bs = Bs0 + buf * BS;
     const int p = w * 8 + ar;  // this lane's particle row (A / C fragments)
     double c[NT][2];
@@ -230,9 +224,10 @@ __global__ void __launch_bounds__(256, 2) k_propose_rb(DrawArgs a) {
     for (int kk = 0; kk < KK; ++kk) {
       const double av = Zs[p * KP + kk * 4 + ac];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
-        if (kk <= 2 * nt + 1) dmma884(c[nt][0], c[nt][1], av, bL[nt][kk]);  // Lz lower: k-steps above the tile vanish
+      for (int nt = 0; nt < NT; ++nt)  // Lz lower: k-steps above the tile vanish
+        if (kk <= 2 * nt + 1) dmma884(c[nt][0], c[nt][1], av, sL[(nt * 8 + ar) * KP + kk * 4 + ac]);
     }
+    __syncwarp();  // all lanes' Z reads of these rows precede the (theta* - mu) writes over them
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -301,6 +296,7 @@ struct AccArgs {
   uint64_t seed;
   int nchunks, d, tp, decide;
   uint32_t step, pass;
+  uint64_t dmagic, pmagic;  // ceil(2^32 / d), ceil(2^32 / (LT - d)): e / m = (e * magic) >> 32 for e < 2^16
 };
 
 // Block = tp (<= 256, divides N) particles of one group, 256 threads.
@@ -481,41 +477,48 @@ __global__ void __launch_bounds__(256) k_accept_mom_rb(AccArgs a) {
     acc[q] = ok;
   }
   nacc = block_sum(nacc, red_i);
-  // rows: warp w owns rows [w RPW, (w + 1) RPW) of the tile, lane = column (d <= 32)
+  // the tile's rows are contiguous in theta / theta*: flat element order e = q d + i (coalesced),
+  // q = e / d by multiply-shift (a.dmagic, exact for e < 2^16), one cp.async round
   const int64_t off0 = pbase * d;
-  const int RPW = TK / 8, q0 = w * RPW;
-  // stage the updated rows (accepted -> theta*, else theta) in one cp.async round; zero padding
-#pragma unroll 4
-  for (int r = 0; r < RPW; ++r) {
-    const int q = q0 + r;
-    double* row = Ts + q * LT;
-    if (q < tp && lane < d)
-      cp_async8(row + lane, (acc[q] ? a.theta_s : a.theta) + off0 + (int64_t)q * d + lane);
-    else if (lane < LT)
-      row[lane] = 0.0;
-    if (LT > 32 && lane < LT - 32) row[32 + lane] = 0.0;
+  const int ne = tp * d;
+#pragma unroll 5
+  for (int e = threadIdx.x; e < ne; e += 256) {
+    const int q = (int)(((uint64_t)e * a.dmagic) >> 32), i = e - q * d;
+    cp_async8(Ts + q * LT + i, (acc[q] ? a.theta_s : a.theta) + off0 + e);
   }
-  cp_async_wait_all();  // each lane reads back only the elements it copied
-  // accepted rows back to theta (coalesced row segments), center on the shift, this warp's group-sum partial
-  const double sh = lane < d ? a.shift[lane] : 0.0;
-  double g0 = 0.0, g1 = 0.0;
-#pragma unroll 2
-  for (int r = 0; r < RPW; ++r) {
-    const int q = q0 + r;
-    if (q < tp && lane < d) {
-      double* row = Ts + q * LT;
-      const double v = row[lane];
-      if (acc[q]) a.theta[off0 + (int64_t)q * d + lane] = v;
-      const double t = v - sh;
-      row[lane] = t;
-      if (r & 1)
-        g1 += t;
-      else
-        g0 += t;
-    }
+  // zero padding: columns [d, LT) of every row, full rows beyond tp
+  const int padw = LT - d;
+  for (int e = threadIdx.x; e < TK * padw; e += 256) {
+    const int q = (int)(((uint64_t)e * a.pmagic) >> 32);
+    const int i = d + e - q * padw;
+    Ts[q * LT + i] = 0.0;
   }
-  if (lane < d) gsp[w * d + lane] = g0 + g1;
+  for (int e = threadIdx.x; e < (TK - tp) * d; e += 256) {
+    const int q = (int)(((uint64_t)e * a.dmagic) >> 32);
+    Ts[(tp + q) * LT + e - q * d] = 0.0;
+  }
+  cp_async_wait_all();
   __syncthreads();
+  // accepted rows back to theta (same flat order), center on the shift
+#pragma unroll 5
+  for (int e = threadIdx.x; e < ne; e += 256) {
+    const int q = (int)(((uint64_t)e * a.dmagic) >> 32), i = e - q * d;
+    const double v = Ts[q * LT + i];
+    if (acc[q]) a.theta[off0 + e] = v;
+    Ts[q * LT + i] = v - a.shift[i];
+  }
+  __syncthreads();
+  // group-sum partials: warp w sums rows w, w + 8, ... (lane = coordinate), fixed order
+  if (lane < d) {
+    double g0 = 0.0, g1 = 0.0;
+    int q = w;
+    for (; q + 8 < tp; q += 16) {
+      g0 += Ts[q * LT + lane];
+      g1 += Ts[(q + 8) * LT + lane];
+    }
+    if (q < tp) g0 += Ts[q * LT + lane];
+    gsp[w * d + lane] = g0 + g1;
+  }
   // T'T: warp w takes k-steps k0 = 4 (w + 8 m)
   double cacc[NTRI][2];
 #pragma unroll

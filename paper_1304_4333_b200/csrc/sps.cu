@@ -536,8 +536,8 @@ sps_status launch_draw(sps_ctx* c, int slot, const double* base, const double* L
   if (d <= 32) {  // register-blocked DMMA proposal
     const int KK = (d + 3) / 4, KPr = 4 * KK, NPr = 8 * ((KPr + 7) / 8);
     const size_t sm =
-        (size_t)(3 * PR_TILE * KPr + 2 * round_up(PR_TILE * d, 2) + KPr + 2 * NPr * KPr) * sizeof(double);
-    const unsigned grid = (unsigned)std::min<int64_t>(ntl, 2 * (int64_t)num_sms());  // persistent, 2 per SM
+        (size_t)(2 * PR_TILE * KPr + 2 * round_up(PR_TILE * d, 2) + KPr + 2 * NPr * KPr) * sizeof(double);
+    const unsigned grid = (unsigned)std::min<int64_t>(ntl, 3 * (int64_t)num_sms());  // persistent, 3 per SM
     switch (KK) {
       case 1: k_propose_rb<1><<<grid, 256, sm, c->stream>>>(a); break;
       case 2: k_propose_rb<2><<<grid, 256, sm, c->stream>>>(a); break;
@@ -589,6 +589,9 @@ sps_status accept_moments(sps_ctx* c, bool decide, int nchunks, double temper, u
   PROF_BEGIN(c);
   if (c->d <= 32) {  // register-blocked T'T on DMMA
     const int NTr = (c->d + 7) / 8;
+    a.dmagic = ((1ull << 32) + (uint64_t)c->d - 1) / (uint64_t)c->d;
+    const uint64_t padw = (uint64_t)(8 * NTr + 4 - c->d);
+    a.pmagic = ((1ull << 32) + padw - 1) / padw;
     const size_t sm =
         ((size_t)round_up(c->tp, 32) * (8 * NTr + 4) + 8 * (size_t)c->d) * sizeof(double) + (size_t)c->tp + 16;
     switch (NTr) {
