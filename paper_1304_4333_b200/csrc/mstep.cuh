@@ -568,6 +568,139 @@ __global__ void __launch_bounds__(256) k_accept_mom_rb(AccArgs a) {
   if (threadIdx.x == 0) out[W - 1] = (double)nacc;
 }
 
+// Accept + moments, tile layout (d <= 8 NT - 1, tp and tp d even).  One thread
+// issues TMA bulk copies of everything the block needs at its start -- the
+// tile's theta and theta* rows (contiguous), L, lp, lp*, log u -- under one
+// mbarrier (the working set of an M step is L2-resident, so reading both row
+// tiles costs L2, not HBM, bandwidth); the chunk partials of K1 are loaded
+// into registers meanwhile.  The decision then runs from shared memory,
+// accepted rows go back to theta in flat coalesced order, and T'T is built by
+// DMMA with fragments formed on the fly, T[q][i] = (acc_q ? theta* : theta)[q][i]
+// - c_i, plus a constant-1 column at index d whose row of T'T is the group-sum
+// partial.  Output row: the NT(NT+1)/2 lower 8x8 tiles of T'T (fragment order
+// = row-major within the tile) | accepts.  Short chain: one load round, one
+// decision, one DMMA pass, one combine.
+template <int NT>
+__global__ void __launch_bounds__(256) k_accept_tile(AccArgs a) {
+  constexpr int NTRI = NT * (NT + 1) / 2;
+  extern __shared__ __align__(16) double sm[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ int red_i[32];
+  if (a.stop && *a.stop) return;
+  const int d = a.d, tp = a.tp, lane = threadIdx.x & 31, w = threadIdx.x >> 5, ar = lane >> 2, ac = lane & 3;
+  const int TD = tp * d;
+  const bool dec = a.decide != 0;
+  const int treg = max(2 * TD, 8 * NTRI * 64);  // row tiles, later the warp partials
+  double* sTh = sm;                              // tp x d
+  double* sTs = sTh + TD;                        // tp x d (theta*)
+  double* sv = sm + treg;                        // [L | lp | lp* | log u] x tp
+  unsigned char* acc = reinterpret_cast<unsigned char*>(sv + 4 * tp);
+  const int64_t pbase = (int64_t)blockIdx.x * tp;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    const unsigned rb = (unsigned)TD * 8u, vb = (unsigned)tp * 8u;
+    mbar_arrive_expect_tx(&bar, rb + (dec ? rb + (a.logu ? 4u : 3u) * vb : 0u));
+    bulk_g2s(sTh, a.theta + pbase * d, rb, &bar);
+    if (dec) {
+      bulk_g2s(sTs, a.theta_s + pbase * d, rb, &bar);
+      bulk_g2s(sv, a.L + pbase, vb, &bar);
+      bulk_g2s(sv + tp, a.lp + pbase, vb, &bar);
+      bulk_g2s(sv + 2 * tp, a.lp_s + pbase, vb, &bar);
+      if (a.logu) bulk_g2s(sv + 3 * tp, a.logu + pbase, vb, &bar);
+    }
+  }
+  double shv[NT];  // c_i of this lane's fragment columns
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+    const int i = t * 8 + ar;
+    shv[t] = i < d ? a.shift[i] : 0.0;
+  }
+  double Ls = 0.0;  // K1 chunk partials of this thread's particle (sum in chunk order)
+  const int q0 = threadIdx.x;
+  if (dec && q0 < tp) {
+    const int64_t p = pbase + q0;
+    Ls = a.part[p];
+    for (int c = 1; c < a.nchunks; ++c) Ls += a.part[(int64_t)c * a.P + p];
+  }
+  __syncthreads();  // barrier initialised
+  mbar_wait(&bar, 0);
+  int nacc = 0;
+  for (int q = q0; q < tp; q += blockDim.x) {
+    unsigned char ok = 0;
+    if (dec) {
+      const int64_t p = pbase + q;
+      if (q != q0) {
+        Ls = a.part[p];
+        for (int c = 1; c < a.nchunks; ++c) Ls += a.part[(int64_t)c * a.P + p];
+      }
+      if (!isfinite(Ls)) atomicExch(&a.ctl->err, ERR_NUMERIC);
+      const double delta = a.temper * (Ls - sv[q]) + (sv[2 * tp + q] - sv[tp + q]);
+      double lu;
+      if (a.logu) {
+        lu = sv[3 * tp + q];
+      } else {
+        const u4 wv = stream_block(a.seed, 0u, (uint32_t)(a.p0 + p), a.step, TAG_ACCEPT, a.pass);
+        lu = plog(u01(wv.x, wv.y));
+      }
+      if (lu < delta) {
+        ok = 1;
+        a.L[p] = Ls;
+        a.lp[p] = sv[2 * tp + q];
+        ++nacc;
+      }
+    }
+    acc[q] = ok;
+  }
+  nacc = block_sum(nacc, red_i);  // (barrier) acc visible
+  if (dec) {
+    double* th = a.theta + pbase * d;
+#pragma unroll 4
+    for (int e = threadIdx.x; e < TD; e += blockDim.x) {
+      const int q = (int)(((uint64_t)e * a.dmagic) >> 32);
+      if (acc[q]) th[e] = sTs[e];
+    }
+  }
+  // T'T, lower tiles; warp w takes k-steps k0 = 4 (w + 8 m)
+  double cacc[NTRI][2];
+#pragma unroll
+  for (int t = 0; t < NTRI; ++t) cacc[t][0] = cacc[t][1] = 0.0;
+  for (int k0 = 4 * w; k0 < tp; k0 += 32) {
+    const int q = k0 + ac;
+    const bool valid = q < tp;
+    const double* row = (valid && acc[q] ? sTs : sTh) + (valid ? q : 0) * d;
+    double f[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      const int i = t * 8 + ar;
+      f[t] = !valid ? 0.0 : (i < d ? row[i] - shv[t] : (i == d ? 1.0 : 0.0));
+    }
+    int tt = 0;
+#pragma unroll
+    for (int mt = 0; mt < NT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt <= mt; ++nt) {
+        dmma884(cacc[tt][0], cacc[tt][1], f[mt], f[nt]);
+        ++tt;
+      }
+  }
+  __syncthreads();  // row tiles consumed: the region holds the warp partials
+  double* wp = sm;  // 8 x NTRI x 64
+#pragma unroll
+  for (int t = 0; t < NTRI; ++t) {
+    wp[(w * NTRI + t) * 64 + lane * 2] = cacc[t][0];
+    wp[(w * NTRI + t) * 64 + lane * 2 + 1] = cacc[t][1];
+  }
+  __syncthreads();
+  double* out = a.bpart + (int64_t)blockIdx.x * (NTRI * 64 + 1);
+  for (int idx = threadIdx.x; idx < NTRI * 64; idx += blockDim.x) {
+    double v = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < 8; ++ww) v += wp[ww * NTRI * 64 + idx];
+    out[idx] = v;  // fragment index e = 2 lane + j = 8 r + c: row-major within the tile
+  }
+  if (threadIdx.x == 0) out[NTRI * 64] = (double)nacc;
+}
+
 // 1/sqrt(x) without a slow-path call: MUFU approximation + 2 Newton steps
 // (relative error ~1 ulp); non-positive / non-finite x give non-finite results.
 __device__ __forceinline__ double rsqrt_nr(double x) {
@@ -899,34 +1032,58 @@ __device__ void finalize_body(const FinArgs& f, double* sm) {
   if (f.trace && threadIdx.x == 0) f.trace[6] = gtimer();
 }
 
+// Block-partial layouts: full (k_accept_mom*): [d | d x d | accepts] (group
+// sums of theta, the shift added per block); tile (k_accept_tile, tnt > 0):
+// [tnt(tnt+1)/2 lower 8x8 tiles of T'T with the ones row at index d | accepts].
+struct RedArgs {
+  const double* bpart;
+  int nblk, bpg, Jl, d, W;
+  int tnt;             // tile layout: tiles per side (0: full layout)
+  int N;               // particles per group (tile layout: group sums += N c)
+  const double* shift;
+};
+__device__ __forceinline__ int red_col(const RedArgs& r, int i, int l) {  // entry (i, l), i >= l, of T'T
+  if (!r.tnt) return r.d + i * r.d + l;
+  const int mt = i >> 3, nt = l >> 3;
+  return (mt * (mt + 1) / 2 + nt) * 64 + (i & 7) * 8 + (l & 7);
+}
+
 // Deterministic reduction of the block partials into this rank's stats slice
 // [Jl x d group sums | d x d second moment | accepts | error].  Blocks
-// [0, nm): 32 moment entries each (8 warps x 8 independent rows per round,
-// fixed-order combine); blocks [nm, nm + ng): group sums; last block: accepts.
-// With f.ticket (one rank: the slice is the gathered stats) the last block to
-// finish runs finalize_body on them (saves a launch and a dependent-launch gap).
-__global__ void __launch_bounds__(256) k_mom_reduce(const double* __restrict__ bpart, int nblk, int bpg, int Jl,
-                                                    int d, Ctl* ctl, double* __restrict__ slice,
+// [0, nm): 32 lower-triangle moment entries each (8 warps x 32 rows in flight,
+// fixed-order combine, mirrored on write); blocks [nm, nm + ng): group sums;
+// last block: accepts.  With f.ticket (one rank: the slice is the gathered
+// stats) the last block to finish runs finalize_body on them (saves a launch
+// and a dependent-launch gap).
+__global__ void __launch_bounds__(256) k_mom_reduce(RedArgs r, Ctl* ctl, double* __restrict__ slice,
                                                     const int* __restrict__ stop, FinArgs f) {
   extern __shared__ double fin_sm[];
   __shared__ double part[8][33];
   __shared__ int s_last;
   if (f.trace && threadIdx.x == 0) f.trace[8 + blockIdx.x] = gtimer();
   if (stop && *stop) return;
-  const int dd = d * d, W = d + dd + 1;
-  const int nm = (dd + 31) / 32, ng = (Jl * d + 255) / 256;
+  const int d = r.d, Jl = r.Jl, W = r.W, nblk = r.nblk, dd = d * d, nl = d * (d + 1) / 2;
+  const int nm = (nl + 31) / 32, ng = (Jl * d + 255) / 256;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if ((int)blockIdx.x < nm) {
     const int e = blockIdx.x * 32 + lane;
+    int i = 0, l = 0;
+    if (e < nl) {  // e = i (i + 1) / 2 + l
+      i = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+      while (i * (i + 1) / 2 > e) --i;
+      while ((i + 1) * (i + 2) / 2 <= e) ++i;
+      l = e - i * (i + 1) / 2;
+    }
+    const int col = red_col(r, i, l);
     double acc8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    if (e < dd) {  // 32 rows per warp in flight at once (one L2 round for nblk <= 256)
+    if (e < nl) {
 #pragma unroll 1
       for (int b0 = w; b0 < nblk; b0 += 256) {
         double v[32];
 #pragma unroll
         for (int u = 0; u < 32; ++u) {
           const int b = b0 + 8 * u;
-          v[u] = b < nblk ? bpart[(int64_t)b * W + d + e] : 0.0;
+          v[u] = b < nblk ? r.bpart[(int64_t)b * W + col] : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 32; ++u) acc8[u & 7] += v[u];
@@ -934,22 +1091,25 @@ __global__ void __launch_bounds__(256) k_mom_reduce(const double* __restrict__ b
     }
     part[w][lane] = ((acc8[0] + acc8[1]) + (acc8[2] + acc8[3])) + ((acc8[4] + acc8[5]) + (acc8[6] + acc8[7]));
     __syncthreads();
-    if (w == 0 && e < dd) {
+    if (w == 0 && e < nl) {
       double t = part[0][lane];
       for (int q = 1; q < 8; ++q) t += part[q][lane];
-      slice[Jl * d + e] = t;
+      slice[Jl * d + i * d + l] = t;
+      slice[Jl * d + l * d + i] = t;
     }
   } else if ((int)blockIdx.x < nm + ng) {
     const int idx = (blockIdx.x - nm) * 256 + threadIdx.x;
     if (idx < Jl * d) {
       const int j = idx / d, c = idx % d;
+      const int col = r.tnt ? red_col(r, d, c) : c;
       double s = 0.0;
-      for (int b = 0; b < bpg; ++b) s += bpart[(int64_t)(j * bpg + b) * W + c];
+      for (int b = 0; b < r.bpg; ++b) s += r.bpart[(int64_t)(j * r.bpg + b) * W + col];
+      if (r.tnt) s += (double)r.N * r.shift[c];
       slice[idx] = s;
     }
   } else {
     double s = 0.0;
-    for (int b = threadIdx.x; b < nblk; b += 256) s += bpart[(int64_t)b * W + W - 1];
+    for (int b = threadIdx.x; b < nblk; b += 256) s += r.bpart[(int64_t)b * W + W - 1];
     __shared__ double red[32];
     s = block_sum(s, red);
     if (threadIdx.x == 0) {

@@ -140,6 +140,8 @@ struct sps_ctx {
   double *Rp = nullptr, *RpP = nullptr;          // prior whitening factor Lprior^-1 (d x d) and its padded copy
   double* bpart = nullptr;       // accept+moments block partials
   int tp = 0, QE = 1, W = 0, nblk = 0;
+  int acc_tnt = 0, Wt = 0;  // tile-layout accept kernel: tiles per side (0: full-layout kernels), partial row width
+  size_t acc_smem = 0;
   Ctl* hslot = nullptr;          // 2 mapped pinned Ctl slots (pipelined M steps), written by finalize_body
   Ctl* dslot = nullptr;          // device view of hslot
   unsigned* ticket = nullptr;      // arrival counter of the fused reduce + finalize (k_mom_reduce)
@@ -586,8 +588,17 @@ sps_status accept_moments(sps_ctx* c, bool decide, int nchunks, double temper, u
   a.decide = decide ? 1 : 0;
   a.step = step;
   a.pass = (uint32_t)c->cfg.pass;
+  a.dmagic = ((1ull << 32) + (uint64_t)c->d - 1) / (uint64_t)c->d;
   PROF_BEGIN(c);
-  if (c->d <= 32) {  // register-blocked T'T on DMMA
+  if (c->acc_tnt > 0) {  // tile layout: bulk-staged rows, on-the-fly DMMA fragments, ones column
+    switch (c->acc_tnt) {
+      case 1: k_accept_tile<1><<<c->nblk, 256, c->acc_smem, c->stream>>>(a); break;
+      case 2: k_accept_tile<2><<<c->nblk, 256, c->acc_smem, c->stream>>>(a); break;
+      case 3: k_accept_tile<3><<<c->nblk, 256, c->acc_smem, c->stream>>>(a); break;
+      case 4: k_accept_tile<4><<<c->nblk, 256, c->acc_smem, c->stream>>>(a); break;
+      default: k_accept_tile<5><<<c->nblk, 256, c->acc_smem, c->stream>>>(a); break;
+    }
+  } else if (c->d <= 32) {  // register-blocked T'T on DMMA
     const int NTr = (c->d + 7) / 8;
     a.dmagic = ((1ull << 32) + (uint64_t)c->d - 1) / (uint64_t)c->d;
     const uint64_t padw = (uint64_t)(8 * NTr + 4 - c->d);
@@ -608,11 +619,11 @@ sps_status accept_moments(sps_ctx* c, bool decide, int nchunks, double temper, u
   CHECK_LAUNCH(c);
   PROF_END(c, CAT_ACCEPT);
   const int d = c->d;
-  const int nm = (d * d + 31) / 32, ng = (c->Jl * d + 255) / 256;
+  const int nm = (d * (d + 1) / 2 + 31) / 32, ng = (c->Jl * d + 255) / 256;
+  RedArgs r{c->bpart, c->nblk, c->N / c->tp, c->Jl, d, c->acc_tnt > 0 ? c->Wt : c->W, c->acc_tnt, c->N, c->shift};
   FinArgs none{};
   PROF_BEGIN(c);
-  k_mom_reduce<<<nm + ng + 1, 256, fin ? fin_smem : 0, c->stream>>>(c->bpart, c->nblk, c->N / c->tp, c->Jl, d, c->ctl,
-                                                                   c->slice, stop, fin ? *fin : none);
+  k_mom_reduce<<<nm + ng + 1, 256, fin ? fin_smem : 0, c->stream>>>(r, c->ctl, c->slice, stop, fin ? *fin : none);
   CHECK_LAUNCH(c);
   PROF_END(c, fin ? CAT_FINALIZE : CAT_REDUCE);
   if (fin) return SPS_OK;  // one rank: the slice is the gathered stats, finalized by the last block
@@ -857,6 +868,16 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
   }
   c->nblk = (int)(c->Pl / c->tp);
   c->W = d + d * d + 1;
+  {  // tile-layout accept kernel when its bulk copies are 16-byte aligned and it fits in shared memory
+    const int tnt = (d + 8) / 8, ntri = tnt * (tnt + 1) / 2, TD = c->tp * d;
+    const size_t sm = (size_t)(std::max(2 * TD, 8 * ntri * 64) + 4 * c->tp) * sizeof(double) + (size_t)c->tp + 16;
+    static const bool no_tile = getenv("SPS_NO_ACC_TILE") != nullptr;
+    if (d <= 32 && c->tp % 2 == 0 && sm <= 200 * 1024 && !no_tile) {
+      c->acc_tnt = tnt;
+      c->Wt = ntri * 64 + 1;
+      c->acc_smem = sm;
+    }
+  }
   c->slice_len = c->Jl * d + d * d + 2;
   c->max_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(64, ((int64_t)1 << 26) / std::max<int64_t>(c->Pl, 1)));
   c->Bmax = (int)std::max<int64_t>(8, std::min<int64_t>(256, ((int64_t)1 << 23) / std::max<int64_t>(c->Pl, 1)));
@@ -897,7 +918,7 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
   for (double** p : {&c->theta, &c->theta2, &c->theta_s}) TRY(dalloc(c, p, (size_t)Pl * d + 2 * PR_TILE));
   for (double** p : {&c->L, &c->L2, &c->lp, &c->lp2, &c->lw, &c->lw_cur, &c->lp_s}) TRY(dalloc(c, p, (size_t)Pl));
   TRY(dalloc(c, &c->part, (size_t)c->max_chunks * Pl));
-  TRY(dalloc(c, &c->bpart, (size_t)c->nblk * c->W));
+  TRY(dalloc(c, &c->bpart, (size_t)c->nblk * std::max(c->W, c->Wt)));
   TRY(dalloc(c, &c->Sinv, (size_t)d * d));
   CU(c, cudaHostAlloc((void**)&c->hslot, 2 * sizeof(Ctl), cudaHostAllocMapped));
   CU(c, cudaHostGetDevicePointer((void**)&c->dslot, c->hslot, 0));
@@ -1027,6 +1048,11 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
     CU(c, cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(c, cudaFuncSetAttribute(k_mom_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(c, cudaFuncSetAttribute(k_accept_mom, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_accept_tile<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_accept_tile<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_accept_tile<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_accept_tile<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_accept_tile<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(c, cudaFuncSetAttribute(k_accept_mom_rb<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(c, cudaFuncSetAttribute(k_accept_mom_rb<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(c, cudaFuncSetAttribute(k_accept_mom_rb<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
@@ -1315,7 +1341,7 @@ sps_status sps_cphase(sps_ctx* c, int32_t t_target, double phi_target, int32_t* 
 static void trace_accumulate(sps_ctx* c) {
   cudaStreamSynchronize(c->stream);
   const unsigned long long* t = c->trace;
-  const int d = c->d, nb = (d * d + 31) / 32 + (c->Jl * d + 255) / 256 + 1;
+  const int d = c->d, nb = (d * (d + 1) / 2 + 31) / 32 + (c->Jl * d + 255) / 256 + 1;
   unsigned long long s0 = ~0ull, s1 = 0, e1 = 0, dmax = 0, dm = 0;
   for (int b = 0; b < nb; ++b) {
     s0 = std::min(s0, t[8 + b]);
