@@ -154,6 +154,27 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
+// Debug timeline (SPS_TIMELINE): per M step (row = *g_tl_steps, the step
+// index within the phase) and kernel slot k, [2k] = start of block (0,0),
+// [2k+1] = latest block end (atomicMax).  Null when disabled.
+constexpr int TL_W = 16, TL_ROWS = 4096;
+__device__ unsigned long long* g_tl = nullptr;
+__device__ const int* g_tl_steps = nullptr;
+__device__ __forceinline__ void tl_start(int k) {
+  unsigned long long* tl = g_tl;
+  if (tl && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+    const int r = *g_tl_steps;
+    if (r >= 0 && r < TL_ROWS) tl[r * TL_W + 2 * k] = gtimer();
+  }
+}
+__device__ __forceinline__ void tl_end(int k) {
+  unsigned long long* tl = g_tl;
+  if (tl && threadIdx.x == 0) {
+    const int r = *g_tl_steps;
+    if (r >= 0 && r < TL_ROWS) atomicMax(&tl[r * TL_W + 2 * k + 1], gtimer());
+  }
+}
+
 // ----------------------------------------------------------------- async copies
 // cp.async (LDGSTS) of 8 bytes global -> shared; all issued copies of a thread
 // are waited by cp_async_wait_all (one latency round for a whole staging phase).

@@ -406,6 +406,7 @@ __global__ void __launch_bounds__(128, MINB) k_loglik_bin_mma(LLArgs a) {
   constexpr int KP = 4 * KKD + (REM ? 4 : 0);  // X row stride (k padded to 4)
   extern __shared__ __align__(16) double smem[];
   if (a.stop && *a.stop) return;
+  tl_start(2);
   double* sT = smem;        // TAB
   double* sX = smem + 256;  // (chunk rounded up to 16) x KP
   const int c0 = a.t0 + blockIdx.y * a.chunk;
@@ -556,6 +557,7 @@ __global__ void __launch_bounds__(128, MINB) k_loglik_bin_mma(LLArgs a) {
         a.part[(int64_t)blockIdx.y * a.P + p] = -(m + (log(pp) + (double)ex * 0x1.62e42fefa39efp-1));
       }
     }
+  tl_end(2);
 }
 
 // Sum chunk partials in chunk order: out[p] = sum_c part[c][p].

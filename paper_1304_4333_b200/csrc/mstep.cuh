@@ -44,19 +44,24 @@ struct DrawArgs {
 __global__ void __launch_bounds__(256) k_normals(int64_t P, int64_t p0, int np, int ldz, uint64_t seed, uint32_t step,
                                                  uint32_t tag, uint32_t pass, double* __restrict__ Z,
                                                  double* __restrict__ logu, const Ctl* sctl, const int* stop) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= P * np) return;
+  // grid-stride over (particle, pair) tasks: the engine launches a small persistent grid so
+  // the side-stream normals share SMs with the critical path instead of filling them
   if (stop && *stop) return;
   if (sctl) step = sctl->step_cur + 1u;
-  const int64_t p = t / np;
-  const int pr = (int)(t - p * np);
-  double z0, z1;
-  normal_pair(seed, (uint32_t)pr, (uint32_t)(p0 + p), step, tag, pass, &z0, &z1);
-  reinterpret_cast<double2*>(Z + p * ldz)[pr] = make_double2(z0, z1);
-  if (logu && pr == 0) {
-    const u4 w = stream_block(seed, 0u, (uint32_t)(p0 + p), step, TAG_ACCEPT, pass);
-    logu[p] = plog(u01(w.x, w.y));
+  if (sctl) tl_start(1);
+  const int64_t ntask = P * np;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntask; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = t / np;
+    const int pr = (int)(t - p * np);
+    double z0, z1;
+    normal_pair(seed, (uint32_t)pr, (uint32_t)(p0 + p), step, tag, pass, &z0, &z1);
+    reinterpret_cast<double2*>(Z + p * ldz)[pr] = make_double2(z0, z1);
+    if (logu && pr == 0) {
+      const u4 w = stream_block(seed, 0u, (uint32_t)(p0 + p), step, TAG_ACCEPT, pass);
+      logu[p] = plog(u01(w.x, w.y));
+    }
   }
+  if (sctl) tl_end(1);
 }
 
 
@@ -172,6 +177,7 @@ __global__ void __launch_bounds__(256, 3) k_propose_rb(DrawArgs a) {
   extern __shared__ __align__(16) double sm[];
   if (a.stop && *a.stop) return;
   if (a.set_step && blockIdx.x == 0 && threadIdx.x == 0) a.ctl->step_cur = a.step0 + (uint32_t)a.ctl->steps_done;
+  if (a.set_step) tl_start(0);
   const int d = a.d, BS = round_up(PR_TILE * d, 2);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, ar = lane >> 2, ac = lane & 3;
   double* Zs0 = sm;                     // 2 x PR_TILE x KP: Z rows, then (theta* - mu) rows (per warp, in place)
@@ -272,6 +278,7 @@ __global__ void __launch_bounds__(256, 3) k_propose_rb(DrawArgs a) {
     }
   }
   if (threadIdx.x == 0) bulk_wait_all();
+  if (a.set_step) tl_end(0);
 }
 
 // ---------------------------------------------------------------- K9 + K6
@@ -289,6 +296,7 @@ struct AccArgs {
   const double* shift;
   const double* logu;  // plog of the ACCEPT uniforms of this step (precomputed), or nullptr
   double* bpart;
+  unsigned long long* trace;  // debug (SPS_TRACE): block-0 phase clocks [64..69], latest block end [70]
   Ctl* ctl;
   const int* stop;
   int64_t P, p0;
@@ -586,23 +594,24 @@ __global__ void __launch_bounds__(256) k_accept_tile(AccArgs a) {
   extern __shared__ __align__(16) double sm[];
   __shared__ __align__(8) uint64_t bar;
   __shared__ int red_i[32];
+  const bool tr = a.trace && blockIdx.x == 0 && threadIdx.x == 0;
+  if (tr) a.trace[64] = gtimer();
   if (a.stop && *a.stop) return;
+  if (a.decide) tl_start(3);
   const int d = a.d, tp = a.tp, lane = threadIdx.x & 31, w = threadIdx.x >> 5, ar = lane >> 2, ac = lane & 3;
   const int TD = tp * d;
   const bool dec = a.decide != 0;
-  const int treg = max(2 * TD, 8 * NTRI * 64);  // row tiles, later the warp partials
-  double* sTh = sm;                              // tp x d
-  double* sTs = sTh + TD;                        // tp x d (theta*)
-  double* sv = sm + treg;                        // [L | lp | lp* | log u] x tp
+  const int treg = max(TD, 8 * NTRI * 64);  // row tile (updated rows), later the warp partials
+  double* sTh = sm;                          // tp x d
+  double* sv = sm + treg;                    // [L | lp | lp* | log u] x tp
   unsigned char* acc = reinterpret_cast<unsigned char*>(sv + 4 * tp);
   const int64_t pbase = (int64_t)blockIdx.x * tp;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     const unsigned rb = (unsigned)TD * 8u, vb = (unsigned)tp * 8u;
-    mbar_arrive_expect_tx(&bar, rb + (dec ? rb + (a.logu ? 4u : 3u) * vb : 0u));
+    mbar_arrive_expect_tx(&bar, rb + (dec ? (a.logu ? 4u : 3u) * vb : 0u));
     bulk_g2s(sTh, a.theta + pbase * d, rb, &bar);
     if (dec) {
-      bulk_g2s(sTs, a.theta_s + pbase * d, rb, &bar);
       bulk_g2s(sv, a.L + pbase, vb, &bar);
       bulk_g2s(sv + tp, a.lp + pbase, vb, &bar);
       bulk_g2s(sv + 2 * tp, a.lp_s + pbase, vb, &bar);
@@ -624,6 +633,7 @@ __global__ void __launch_bounds__(256) k_accept_tile(AccArgs a) {
   }
   __syncthreads();  // barrier initialised
   mbar_wait(&bar, 0);
+  if (tr) a.trace[65] = gtimer();
   int nacc = 0;
   for (int q = q0; q < tp; q += blockDim.x) {
     unsigned char ok = 0;
@@ -652,13 +662,20 @@ __global__ void __launch_bounds__(256) k_accept_tile(AccArgs a) {
     acc[q] = ok;
   }
   nacc = block_sum(nacc, red_i);  // (barrier) acc visible
-  if (dec) {
+  if (tr) a.trace[66] = gtimer();
+  if (dec) {  // accepted rows only: theta* -> theta (global, L2-resident) and over the staged rows
+    const double* ts = a.theta_s + pbase * d;
     double* th = a.theta + pbase * d;
 #pragma unroll 4
     for (int e = threadIdx.x; e < TD; e += blockDim.x) {
       const int q = (int)(((uint64_t)e * a.dmagic) >> 32);
-      if (acc[q]) th[e] = sTs[e];
+      if (acc[q]) {
+        const double v = __ldcg(ts + e);
+        th[e] = v;
+        sTh[e] = v;
+      }
     }
+    __syncthreads();
   }
   // T'T, lower tiles; warp w takes k-steps k0 = 4 (w + 8 m)
   double cacc[NTRI][2];
@@ -667,7 +684,7 @@ __global__ void __launch_bounds__(256) k_accept_tile(AccArgs a) {
   for (int k0 = 4 * w; k0 < tp; k0 += 32) {
     const int q = k0 + ac;
     const bool valid = q < tp;
-    const double* row = (valid && acc[q] ? sTs : sTh) + (valid ? q : 0) * d;
+    const double* row = sTh + (valid ? q : 0) * d;
     double f[NT];
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
@@ -684,6 +701,7 @@ __global__ void __launch_bounds__(256) k_accept_tile(AccArgs a) {
       }
   }
   __syncthreads();  // row tiles consumed: the region holds the warp partials
+  if (tr) a.trace[67] = gtimer();
   double* wp = sm;  // 8 x NTRI x 64
 #pragma unroll
   for (int t = 0; t < NTRI; ++t) {
@@ -699,6 +717,12 @@ __global__ void __launch_bounds__(256) k_accept_tile(AccArgs a) {
     out[idx] = v;  // fragment index e = 2 lane + j = 8 r + c: row-major within the tile
   }
   if (threadIdx.x == 0) out[NTRI * 64] = (double)nacc;
+  if (a.trace && threadIdx.x == 0) {
+    const unsigned long long t = gtimer();
+    if (tr) a.trace[68] = t;
+    atomicMax(&a.trace[70], t);
+  }
+  if (a.decide) tl_end(3);
 }
 
 // 1/sqrt(x) without a slow-path call: MUFU approximation + 2 Newton steps
@@ -1062,6 +1086,7 @@ __global__ void __launch_bounds__(256) k_mom_reduce(RedArgs r, Ctl* ctl, double*
   __shared__ int s_last;
   if (f.trace && threadIdx.x == 0) f.trace[8 + blockIdx.x] = gtimer();
   if (stop && *stop) return;
+  if (f.mode == 1) tl_start(4);
   const int d = r.d, Jl = r.Jl, W = r.W, nblk = r.nblk, dd = d * d, nl = d * (d + 1) / 2;
   const int nm = (nl + 31) / 32, ng = (Jl * d + 255) / 256;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1121,12 +1146,20 @@ __global__ void __launch_bounds__(256) k_mom_reduce(RedArgs r, Ctl* ctl, double*
   __threadfence();  // this block's slice writes before its ticket
   __syncthreads();
   if (f.trace && threadIdx.x == 0) f.trace[8 + gridDim.x + blockIdx.x] = gtimer();
+  if (f.mode == 1) tl_end(4);
   if (threadIdx.x == 0) s_last = atomicAdd(f.ticket, 1u) == gridDim.x - 1;
   __syncthreads();
   if (!s_last) return;
   __threadfence();
   if (threadIdx.x == 0) *f.ticket = 0u;  // re-armed for the next launch (stream order)
+  unsigned long long* tl = g_tl;
+  int tlr = -1;
+  if (tl && threadIdx.x == 0 && f.mode == 1) {
+    tlr = *g_tl_steps;  // before finalize_body increments steps_done
+    if (tlr >= 0 && tlr < TL_ROWS) tl[tlr * TL_W + 10] = gtimer();
+  }
   finalize_body(f, fin_sm);
+  if (tlr >= 0 && tlr < TL_ROWS) tl[tlr * TL_W + 11] = gtimer();
 }
 
 // Finalize as its own launch (G > 1: after the all-gather of the slices; mode 0).

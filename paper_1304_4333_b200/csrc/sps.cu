@@ -146,6 +146,9 @@ struct sps_ctx {
   Ctl* dslot = nullptr;          // device view of hslot
   unsigned* ticket = nullptr;      // arrival counter of the fused reduce + finalize (k_mom_reduce)
   unsigned long long* trace = nullptr;  // debug (SPS_TRACE): finalize / reduce phase clocks (managed)
+  unsigned long long* tl = nullptr;     // debug (SPS_TIMELINE): per-step kernel start / end clocks
+  double tl_acc[16] = {};
+  int tl_rows = 0;
   double trace_acc[80] = {};
   int trace_n = 0;
   double* Zbuf[2] = {nullptr, nullptr};  // standard normals, one M step ahead (side stream)
@@ -159,6 +162,7 @@ struct sps_ctx {
   int64_t g_launches[2] = {0, 0}, g_k1[2] = {0, 0};
   double g_pairs[2] = {0, 0};
   int graph_updates = 0, graph_instantiations = 0;
+  bool capturing = false;  // inside build_mstep_graphs
   LLChoice_t llc{};
   int ll_regs = 0;
   struct Plan {
@@ -493,16 +497,34 @@ sps_status launch_loglik(sps_ctx* c, const double* theta, int64_t ldt, int64_t P
 // graph: inside an M-step capture -- forked from the main stream after the
 // proposal (ev_fork), step = ctl->step_cur + 1 on the device, joined back
 // through ev_join (graph replays are stream-ordered: no Zbuf events needed).
-sps_status launch_normals(sps_ctx* c, uint32_t tag, uint32_t step, int slot, bool graph = false) {
+sps_status launch_normals(sps_ctx* c, uint32_t tag, uint32_t step, int slot, bool graph = false, bool forked = false);
+sps_status launch_normals(sps_ctx* c, uint32_t tag, uint32_t step, int slot, bool graph, bool forked) {
   const int np = (c->d + 1) / 2;
   static const bool serial = getenv("SPS_SERIAL_NORMALS") != nullptr;  // debug: no overlap, own profile category
   cudaStream_t st = serial && !graph ? c->stream : c->aux;
-  CU(c, cudaStreamWaitEvent(st, graph ? c->ev_fork : c->ev_zfree[slot], 0));
+  if (!graph) CU(c, cudaStreamWaitEvent(st, c->ev_zfree[slot], 0));
+  if (forked) CU(c, cudaStreamWaitEvent(st, c->ev_fork, 0));
   const int64_t tasks = c->Pl * np;
   if (serial && !graph) PROF_BEGIN(c);
-  k_normals<<<(unsigned)((tasks + 255) / 256), 256, 0, st>>>(
-      c->Pl, c->p0, np, round_up(c->d, 4), c->cfg.seed, step, tag, (uint32_t)c->cfg.pass, c->Zbuf[slot],
-      tag == TAG_PROPOSAL ? c->LUbuf[slot] : nullptr, graph ? c->ctl : nullptr, graph ? &c->ctl->stop : nullptr);
+  {  // lowest scheduling priority as a launch attribute: it carries into captured graph nodes
+    cudaLaunchConfig_t lc = {};
+    // M steps: 2 blocks per SM (grid-stride); setup / first draws: full grid
+    const int64_t full = (tasks + 255) / 256;
+    lc.gridDim = dim3((unsigned)(forked ? std::min<int64_t>(full, 4 * (int64_t)num_sms()) : full));
+    lc.blockDim = dim3(256);
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    int lo = 0, hi = 0;
+    CU(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    at[0].id = cudaLaunchAttributePriority;
+    at[0].val.priority = lo;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    CU(c, cudaLaunchKernelEx(&lc, k_normals, (int64_t)c->Pl, (int64_t)c->p0, np, round_up(c->d, 4), (uint64_t)c->cfg.seed,
+                             step, tag, (uint32_t)c->cfg.pass, c->Zbuf[slot],
+                             tag == TAG_PROPOSAL ? c->LUbuf[slot] : (double*)nullptr, graph ? (const Ctl*)c->ctl : nullptr,
+                             graph ? (const int*)&c->ctl->stop : nullptr));
+  }
   CHECK_LAUNCH(c);
   if (serial && !graph) PROF_END(c, CAT_OTHER);
   CU(c, cudaEventRecord(graph ? c->ev_join : c->ev_zready[slot], st));
@@ -564,8 +586,13 @@ sps_status launch_draw(sps_ctx* c, int slot, const double* base, const double* L
 
 // K9 + K6 (decide = true) or K6 only, then the deterministic reduction into this
 // rank's stats slice and the gather across ranks -> `gath`.
+sps_status launch_normals(sps_ctx* c, uint32_t tag, uint32_t step, int slot, bool graph, bool forked);
+
+// fork_step != ~0u: after the accept kernel, fork the next step's normals (step fork_step + 1) onto
+// the side stream.
 sps_status accept_moments(sps_ctx* c, bool decide, int nchunks, double temper, uint32_t step, const int* stop,
-                          const double* logu = nullptr, const FinArgs* fin = nullptr, size_t fin_smem = 0) {
+                          const double* logu = nullptr, const FinArgs* fin = nullptr, size_t fin_smem = 0,
+                          uint32_t fork_step = ~0u) {
   AccArgs a{};
   a.theta = c->theta;
   a.L = c->L;
@@ -589,6 +616,7 @@ sps_status accept_moments(sps_ctx* c, bool decide, int nchunks, double temper, u
   a.step = step;
   a.pass = (uint32_t)c->cfg.pass;
   a.dmagic = ((1ull << 32) + (uint64_t)c->d - 1) / (uint64_t)c->d;
+  a.trace = decide ? c->trace : nullptr;
   PROF_BEGIN(c);
   if (c->acc_tnt > 0) {  // tile layout: bulk-staged rows, on-the-fly DMMA fragments, ones column
     switch (c->acc_tnt) {
@@ -618,6 +646,10 @@ sps_status accept_moments(sps_ctx* c, bool decide, int nchunks, double temper, u
   }
   CHECK_LAUNCH(c);
   PROF_END(c, CAT_ACCEPT);
+  if (fork_step != ~0u) {
+    CU(c, cudaEventRecord(c->ev_fork, c->stream));
+    TRY(launch_normals(c, TAG_PROPOSAL, fork_step + 1u, (int)((fork_step + 1u) & 1u), c->capturing, true));
+  }
   const int d = c->d;
   const int nm = (d * (d + 1) / 2 + 31) / 32, ng = (c->Jl * d + 255) / 256;
   RedArgs r{c->bpart, c->nblk, c->N / c->tp, c->Jl, d, c->acc_tnt > 0 ? c->Wt : c->W, c->acc_tnt, c->N, c->shift};
@@ -685,16 +717,18 @@ sps_status finalize(sps_ctx* c, int mode, bool allow_stop, const int* stop, int 
 
 // K9 + K6 -> reduce -> (gather) -> K7: fused into the reduce launch on one rank.
 sps_status moments_finalize(sps_ctx* c, bool decide, int nchunks, double temper, uint32_t step, const int* stop,
-                            const double* logu, int mode, bool allow_stop, int slot) {
+                            const double* logu, int mode, bool allow_stop, int slot, bool fork_normals = false) {
+  const bool graph = c->capturing;
   if (c->G > 1) {
-    TRY(accept_moments(c, decide, nchunks, temper, step, stop, logu));
+    TRY(accept_moments(c, decide, nchunks, temper, step, stop, logu, nullptr, 0, fork_normals ? step : ~0u));
     return finalize(c, mode, allow_stop, stop, slot);
   }
   FinArgs f;
   size_t smem = 0;
   TRY(make_fin(c, mode, allow_stop, stop, slot, &f, &smem));
   f.ticket = c->ticket;
-  return accept_moments(c, decide, nchunks, temper, step, stop, logu, &f, smem);
+  (void)graph;
+  return accept_moments(c, decide, nchunks, temper, step, stop, logu, &f, smem, fork_normals ? step : ~0u);
 }
 
 sps_status validate(const sps_config* cfg) {
@@ -742,6 +776,7 @@ void free_ctx(sps_ctx* c) {
   if (c->hslot) cudaFreeHost(c->hslot);
   if (c->ticket) cudaFree(c->ticket);
   if (c->trace) cudaFree(c->trace);
+  if (c->tl) cudaFree(c->tl);
   for (cudaEvent_t e : c->evs)
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : c->prof_pool) cudaEventDestroy(e);
@@ -870,7 +905,7 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
   c->W = d + d * d + 1;
   {  // tile-layout accept kernel when its bulk copies are 16-byte aligned and it fits in shared memory
     const int tnt = (d + 8) / 8, ntri = tnt * (tnt + 1) / 2, TD = c->tp * d;
-    const size_t sm = (size_t)(std::max(2 * TD, 8 * ntri * 64) + 4 * c->tp) * sizeof(double) + (size_t)c->tp + 16;
+    const size_t sm = (size_t)(std::max(TD, 8 * ntri * 64) + 4 * c->tp) * sizeof(double) + (size_t)c->tp + 16;
     static const bool no_tile = getenv("SPS_NO_ACC_TILE") != nullptr;
     if (d <= 32 && c->tp % 2 == 0 && sm <= 200 * 1024 && !no_tile) {
       c->acc_tnt = tnt;
@@ -885,7 +920,9 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
   if (cfg.stream) {
     c->stream = (cudaStream_t)cfg.stream;
   } else {
-    CU(c, cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    int lo = 0, hi = 0;
+    CU(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CU(c, cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, hi));  // the critical path
     c->own_stream = true;
   }
   if (c->G > 1 && cfg_in->nccl_id &&
@@ -941,7 +978,9 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
     TRY(dalloc(c, &c->LUbuf[1], (size_t)Pl));
     CU(c, cudaMemsetAsync(c->Zbuf[0], 0, zn * sizeof(double), c->stream));
     CU(c, cudaMemsetAsync(c->Zbuf[1], 0, zn * sizeof(double), c->stream));
-    CU(c, cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+    int lo = 0, hi = 0;
+    CU(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CU(c, cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, lo));  // side work fills idle SMs
     for (int q = 0; q < 2; ++q) {
       CU(c, cudaEventCreateWithFlags(&c->ev_zready[q], cudaEventDisableTiming));
       CU(c, cudaEventCreateWithFlags(&c->ev_zfree[q], cudaEventDisableTiming));
@@ -988,6 +1027,13 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
   if (c->G > 1) TRY(dalloc(c, &c->mx_gath, (size_t)c->G));
   else c->mx_gath = c->mx_slice;
   TRY(dalloc(c, &c->ctl, 1));
+  if (getenv("SPS_TIMELINE")) {
+    CU(c, cudaMalloc((void**)&c->tl, sizeof(unsigned long long) * TL_W * TL_ROWS));
+    CU(c, cudaMemsetAsync(c->tl, 0, sizeof(unsigned long long) * TL_W * TL_ROWS, c->stream));
+    const int* steps = &c->ctl->steps_done;
+    CU(c, cudaMemcpyToSymbolAsync(g_tl, &c->tl, sizeof(c->tl), 0, cudaMemcpyHostToDevice, c->stream));
+    CU(c, cudaMemcpyToSymbolAsync(g_tl_steps, &steps, sizeof(steps), 0, cudaMemcpyHostToDevice, c->stream));
+  }
   CU(c, cudaMallocHost((void**)&c->hctl, sizeof(Ctl)));
   std::memset(c->hctl, 0, sizeof(Ctl));
   c->hctl->h = cfg.h_init;
@@ -1045,6 +1091,11 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
     }
     CU(c, cudaFuncSetAttribute(k_propose<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(c, cudaFuncSetAttribute(k_propose<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    // the side-stream normals use no shared memory; with the default (L1-leaning) carveout the SMs
+    // they run on cannot take a 111 KB accept block until they drain and reconfigure (SPS_TIMELINE:
+    // accept started 18 us late), so they request the max-shared split like the M-step kernels
+    CU(c, cudaFuncSetAttribute(k_normals, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared));
     CU(c, cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(c, cudaFuncSetAttribute(k_mom_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(c, cudaFuncSetAttribute(k_accept_mom, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
@@ -1148,6 +1199,21 @@ sps_status sps_get_counters(const sps_ctx* cc, sps_counters* out) {
                                "host slot", "start skew", "longest block", "moment block"};
     fprintf(stderr, "SPS_TRACE mean ns over %d finalizes:", c->trace_n);
     for (int q = 0; q < 11; ++q) fprintf(stderr, " %s=%.0f", nm[q], c->trace_acc[q] / c->trace_n);
+    fprintf(stderr, "\n");
+    if (false) {}
+    if (c->trace_acc[17] > 0) {
+      static const char* an[] = {"load", "decide", "writeback+dmma", "combine", "kernel span", "gap->reduce"};
+      fprintf(stderr, "SPS_TRACE accept (block 0) mean ns over %.0f:", c->trace_acc[17]);
+      for (int q = 0; q < 6; ++q) fprintf(stderr, " %s=%.0f", an[q], c->trace_acc[11 + q] / c->trace_acc[17]);
+      fprintf(stderr, "\n");
+    }
+  }
+  if (c->tl && c->tl_rows) {
+    static const char* nm[] = {"propose", "normals", "K1", "accept", "reduce", "finalize", "gap K1<-propose",
+                               "gap accept<-K1", "gap reduce<-accept", "gap fin<-reduce", "normals start-propose end",
+                               "normals end-K1 end", "gap next propose<-fin", "step"};
+    fprintf(stderr, "SPS_TIMELINE mean us over %d steps:", c->tl_rows);
+    for (int q = 0; q < 14; ++q) fprintf(stderr, " %s=%.2f", nm[q], c->tl_acc[q] / c->tl_rows / 1e3);
     fprintf(stderr, "\n");
   }
   out->launches = c->launches;
@@ -1354,10 +1420,48 @@ static void trace_accumulate(sps_ctx* c) {
   c->trace_acc[9] += (double)dmax;       // longest block
   c->trace_acc[10] += (double)dm;        // a moment block
   if (t[0] < s0 || t[6] < t[0]) return;  // stopped step (no finalize)
+  if (t[68] > t[64] && t[70] >= t[68]) {  // accept kernel: block 0 phases, latest block end
+    c->trace_acc[11] += (double)(t[65] - t[64]);
+    c->trace_acc[12] += (double)(t[66] - t[65]);
+    c->trace_acc[13] += (double)(t[67] - t[66]);
+    c->trace_acc[14] += (double)(t[68] - t[67]);
+    c->trace_acc[15] += (double)(t[70] - t[64]);
+    c->trace_acc[16] += (double)(s0 - t[70]);  // last accept block end -> first reduce block start
+    c->trace_acc[17] += 1;
+  }
   c->trace_acc[0] += (double)(e1 - s0);      // reduce phase: first block start -> last block ticket
   c->trace_acc[1] += (double)(t[0] - e1);    // ticket -> finalize start
   for (int q = 1; q <= 6; ++q) c->trace_acc[1 + q] += (double)(t[q] - t[q - 1]);
   c->trace_n += 1;
+  c->trace[70] = 0;  // latest accept block end (atomicMax), re-armed (the stream is idle here)
+}
+
+// Debug (SPS_TIMELINE): mean kernel spans and gaps over the finished steps of a
+// phase (0 propose, 1 normals(next), 2 K1, 3 accept, 4 reduce, 5 finalize block).
+static sps_status timeline_accumulate(sps_ctx* c, int R) {
+  CU(c, cudaStreamSynchronize(c->stream));
+  CU(c, cudaStreamSynchronize(c->aux));
+  std::vector<unsigned long long> h((size_t)TL_W * TL_ROWS);
+  const int rows = std::min(R, TL_ROWS);
+  CU(c, cudaMemcpy(h.data(), c->tl, sizeof(unsigned long long) * TL_W * rows, cudaMemcpyDeviceToHost));
+  for (int r = 0; r < rows; ++r) {
+    const unsigned long long* t = &h[(size_t)r * TL_W];
+    bool ok = true;
+    for (int k = 0; k < 6; ++k) ok = ok && t[2 * k] && t[2 * k + 1] >= t[2 * k];
+    if (!ok) continue;
+    for (int k = 0; k < 6; ++k) c->tl_acc[k] += (double)(t[2 * k + 1] - t[2 * k]);  // spans
+    c->tl_acc[6] += (double)t[4] - (double)t[1];    // K1 start - propose end
+    c->tl_acc[7] += (double)t[6] - (double)t[5];    // accept start - K1 end
+    c->tl_acc[8] += (double)t[8] - (double)t[7];    // reduce start - accept end
+    c->tl_acc[9] += (double)t[10] - (double)t[9];   // finalize start - reduce end
+    c->tl_acc[10] += (double)t[2] - (double)t[1];   // normals start - propose end
+    c->tl_acc[11] += (double)t[3] - (double)t[5];   // normals end - K1 end
+    if (r + 1 < rows && h[(size_t)(r + 1) * TL_W]) c->tl_acc[12] += (double)h[(size_t)(r + 1) * TL_W] - (double)t[11];
+    c->tl_acc[13] += (double)t[11] - (double)t[0];  // step: propose start -> finalize end
+    c->tl_rows += 1;
+  }
+  CU(c, cudaMemsetAsync(c->tl, 0, sizeof(unsigned long long) * TL_W * TL_ROWS, c->stream));
+  return SPS_OK;
 }
 
 // One M step (Algorithm 2 step 2(c)), fully enqueued:
@@ -1375,17 +1479,39 @@ static sps_status launch_mstep(sps_ctx* c, uint32_t step, bool allow_stop, bool 
   const int* stop = &c->ctl->stop;
   const int zs = (int)(step & 1u);
   TRY(launch_draw(c, zs, c->theta, c->Lprop, c->theta_s, c->lp_s, stop, graph, true));
-  if (graph) CU(c, cudaEventRecord(c->ev_fork, c->stream));
-  TRY(launch_normals(c, TAG_PROPOSAL, step + 1u, zs ^ 1, graph));  // next step's normals, overlapped
   int nch = 1;
   TRY(launch_loglik(c, c->theta_s, c->d, c->Pl, 0, t1, c->part, c->max_chunks, &nch, stop));
-  TRY(moments_finalize(c, true, nch, temper, step, stop, c->LUbuf[zs], 1, allow_stop, zs));
+  // next step's normals on the low-priority side stream, forked after accept: they fill the SMs
+  // the reduce / one-block finalize tail leaves idle (SPS_TIMELINE: launched before K1 they held
+  // every SM while K1 waited 17.8 us; forked after K1 they stretched accept from 13 to 25 us)
+  TRY(moments_finalize(c, true, nch, temper, step, stop, c->LUbuf[zs], 1, allow_stop, zs, true));
   if (graph) {
     CU(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
     CU(c, cudaEventRecordWithFlags(c->evs[zs], c->stream, cudaEventRecordExternal));
   } else {
     CU(c, cudaEventRecord(c->ev_zfree[zs], c->stream));  // Zbuf / LUbuf[zs] consumed
     CU(c, cudaEventRecord(c->evs[zs], c->stream));
+  }
+  return SPS_OK;
+}
+
+// Kernel-node priorities of a captured M step: k_normals lowest, everything else highest.
+static sps_status set_node_priorities(sps_ctx* c, cudaGraph_t g) {
+  size_t n = 0;
+  CU(c, cudaGraphGetNodes(g, nullptr, &n));
+  std::vector<cudaGraphNode_t> nodes(n);
+  CU(c, cudaGraphGetNodes(g, nodes.data(), &n));
+  int lo = 0, hi = 0;
+  CU(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  for (cudaGraphNode_t nd : nodes) {
+    cudaGraphNodeType t;
+    CU(c, cudaGraphNodeGetType(nd, &t));
+    if (t != cudaGraphNodeTypeKernel) continue;
+    cudaKernelNodeParams kp{};
+    CU(c, cudaGraphKernelNodeGetParams(nd, &kp));
+    cudaKernelNodeAttrValue v{};
+    v.priority = kp.func == (void*)k_normals ? lo : hi;
+    CU(c, cudaGraphKernelNodeSetAttribute(nd, cudaKernelNodeAttributePriority, &v));
   }
   return SPS_OK;
 }
@@ -1398,8 +1524,10 @@ static sps_status build_mstep_graphs(sps_ctx* c, bool allow_stop) {
     const int64_t l0 = c->launches, k0 = c->k1_launches;
     const double p0 = c->k1_pairs;
     CU(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    c->capturing = true;
     const sps_status st = launch_mstep(c, c->phase_step0 + (uint32_t)((par ^ (int)(c->phase_step0 & 1u)) & 1), allow_stop,
                                        true);
+    c->capturing = false;
     cudaGraph_t g = nullptr;
     const cudaError_t ee = cudaStreamEndCapture(c->stream, &g);
     if (st != SPS_OK) {
@@ -1407,6 +1535,7 @@ static sps_status build_mstep_graphs(sps_ctx* c, bool allow_stop) {
       return st;
     }
     CU(c, ee);
+    TRY(set_node_priorities(c, g));
     c->g_launches[par] = c->launches - l0;
     c->g_k1[par] = c->k1_launches - k0;
     c->g_pairs[par] = c->k1_pairs - p0;
@@ -1423,7 +1552,9 @@ static sps_status build_mstep_graphs(sps_ctx* c, bool allow_stop) {
     if (!ok) {
       if (c->gexec[par]) cudaGraphExecDestroy(c->gexec[par]);
       c->gexec[par] = nullptr;
-      const cudaError_t ei = cudaGraphInstantiate(&c->gexec[par], g, 0);
+      // per-node priorities (side-stream normals lowest): without this flag a replay schedules the
+      // nodes with the launch stream's priority and the normals hold SMs the critical path needs
+      const cudaError_t ei = cudaGraphInstantiateWithFlags(&c->gexec[par], g, cudaGraphInstantiateFlagUseNodePriority);
       cudaGraphDestroy(g);
       CU(c, ei);
       c->graph_instantiations += 1;
@@ -1502,6 +1633,7 @@ sps_status sps_mphase(sps_ctx* c, int32_t R_fixed, int32_t* R_out, double* min_r
     r += 1;
   }
   c->mstep = step0 + (uint32_t)r;
+  if (c->tl) TRY(timeline_accumulate(c, r));
   *c->hctl = got;
   c->cphase_done = false;
   c->tr_R.push_back(r);
