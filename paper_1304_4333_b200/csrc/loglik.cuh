@@ -446,18 +446,31 @@ __global__ void __launch_bounds__(128, MINB) k_loglik_bin_mma(LLArgs a) {
       E[nt][e] = 0;
     }
   int nit = 0;
-  const int sub = a.sub > 0 ? a.sub : ntot;  // X sub-chunk resident in shared memory (multiple of 16)
-  for (int cs = 0; cs < ntot; cs += sub) {
-  const int nobs = min(sub, ntot - cs);
-  const int nobs16 = (nobs + 15) & ~15;
-  __syncthreads();  // previous sub-chunk consumed
-  {
-    const double2* src = reinterpret_cast<const double2*>(a.X + (int64_t)(c0 + cs) * KP);
-    double2* dst = reinterpret_cast<double2*>(sX);
-    const int nv = nobs * KP / 2, nv16 = nobs16 * KP / 2;
-    for (int i = threadIdx.x; i < nv16; i += blockDim.x) dst[i] = i < nv ? __ldg(src + i) : make_double2(0.0, 0.0);
+  // X sub-chunks (sub rows, a multiple of 16) stream through two shared-memory buffers by TMA bulk
+  // copies: the next one loads while this one computes.  Rows past a sub-chunk's end hold stale
+  // data; their products are masked out below (the per-thread load/store staging these copies
+  // replace was ~28% of the stall samples, ncu r01_pa2).
+  const int sub = a.sub > 0 ? a.sub : ntot;
+  const int SR = (sub + 15) & ~15;
+  __shared__ __align__(8) uint64_t xbar[2];
+  if (threadIdx.x == 0) {
+    mbar_init(&xbar[0], 1);
+    mbar_init(&xbar[1], 1);
   }
   __syncthreads();
+  auto issue = [&](int cs, int buf) {
+    const unsigned bytes = (unsigned)(min(sub, ntot - cs) * KP * 8);
+    mbar_arrive_expect_tx(&xbar[buf], bytes);
+    bulk_g2s(sX + buf * SR * KP, a.X + (int64_t)(c0 + cs) * KP, bytes, &xbar[buf]);
+  };
+  if (threadIdx.x == 0 && ntot > 0) issue(0, 0);
+  int it = 0;
+  for (int cs = 0; cs < ntot; cs += sub, ++it) {
+  const int nobs = min(sub, ntot - cs);
+  const int buf = it & 1;
+  if (threadIdx.x == 0 && cs + sub < ntot) issue(cs + sub, buf ^ 1);  // buf ^ 1 released by the barrier below
+  mbar_wait(&xbar[buf], (unsigned)(it >> 1) & 1u);
+  const double* sXb = sX + buf * SR * KP;
   for (int t0 = 0; t0 < nobs; t0 += 8 * H) {
     double acc[H][NTW][2];
 #pragma unroll
@@ -466,7 +479,7 @@ __global__ void __launch_bounds__(128, MINB) k_loglik_bin_mma(LLArgs a) {
       for (int nt = 0; nt < NTW; ++nt) acc[h][nt][0] = acc[h][nt][1] = 0.0;
 #pragma unroll
     for (int h = 0; h < H; ++h) {
-      const double* xr = sX + (t0 + 8 * h + ar) * KP;
+      const double* xr = sXb + (t0 + 8 * h + ar) * KP;
       if (KS == 2 && KKD >= 2) {
         double acc2[NTW][2];
 #pragma unroll
@@ -536,6 +549,7 @@ __global__ void __launch_bounds__(128, MINB) k_loglik_bin_mma(LLArgs a) {
       }
     }
   }
+  __syncthreads();  // every warp is done with buffer `buf` before it is refilled
   }  // sub-chunks
   // combine the 8 lanes (ar = 0..7) of each particle column: sums of M and E, product of P
 #pragma unroll

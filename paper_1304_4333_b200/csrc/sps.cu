@@ -442,7 +442,8 @@ sps_status launch_loglik(sps_ctx* c, const double* theta, int64_t ldt, int64_t P
     c->plan_next = (c->plan_next + 1) % 8;
     const int smem_budget = 100 * 1024;
     const int chunk_cap = std::max(1, (int)((smem_budget - 256 * 8 - 64) / row_bytes) - 16);
-    const int sub_cap = std::max(16, chunk_cap / 16 * 16);  // streaming kernels: sub-chunk in smem
+    // streaming (DMMA) kernels: two sub-chunk buffers (TMA double buffering) in the same budget
+    const int sub_cap = std::max(16, (chunk_cap / 2) / 16 * 16);
     const int S_min = ch.streams ? 1 : std::max(1, (range + chunk_cap - 1) / chunk_cap);
     const int S_hi = std::min(max_chunks, std::max(S_min, std::min(S_min + 24, range / 8)));
     const int warp_regs = ((c->ll_regs * 32 + 255) / 256) * 256;
@@ -455,7 +456,7 @@ sps_status launch_loglik(sps_ctx* c, const double* theta, int64_t ldt, int64_t P
       const int chunk = (range + S - 1) / S;
       const int Se = (range + chunk - 1) / chunk;
       const int rows = ch.streams ? std::min(chunk, sub_cap) : chunk;
-      const size_t smem = 256 * 8 + (size_t)(rows + 16) * row_bytes + 16;
+      const size_t smem = 256 * 8 + (size_t)(ch.streams ? 2 * ((rows + 15) / 16 * 16) : rows + 16) * row_bytes + 16;
       const int by_smem = (int)(233472 / (smem + 1024));
       const int occ = std::max(1, std::min(std::min(by_regs, by_smem), 16));
       const double slots = (double)num_sms() * occ;
@@ -474,7 +475,8 @@ sps_status launch_loglik(sps_ctx* c, const double* theta, int64_t ldt, int64_t P
     pl->S = (range + chunk - 1) / chunk;
     pl->sub = ch.streams ? std::min(((chunk + 15) / 16) * 16, sub_cap) : 0;
     const int rows = ch.streams ? pl->sub : chunk;
-    pl->smem = 256 * 8 + (size_t)(rows + 16) * c->ldx * 8 + (c->C > 2 ? (size_t)chunk * 4 : 0);
+    pl->smem = 256 * 8 + (size_t)(ch.streams ? 2 * ((rows + 15) / 16 * 16) : rows + 16) * c->ldx * 8 +
+               (c->C > 2 ? (size_t)chunk * 4 : 0);
     if (pl->S > max_chunks) return fail(c, SPS_E_CONFIG, "observation range too long for the chunk buffer");
   }
   LLArgs a{c->Xs, c->y, theta, part, ldt, P, t0, t1, pl->chunk};
