@@ -175,6 +175,14 @@ __device__ __forceinline__ void tl_end(int k) {
   }
 }
 
+// Programmatic dependent launch: a kernel launched with programmatic stream
+// serialization may start while its predecessor runs; griddep_wait() blocks
+// until the predecessor grid has completed and its writes are visible (a no-op
+// without the launch attribute); griddep_launch() lets the successor's CTAs be
+// scheduled once every CTA of this grid has called it or exited.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 // ----------------------------------------------------------------- async copies
 // cp.async (LDGSTS) of 8 bytes global -> shared; all issued copies of a thread
 // are waited by cp_async_wait_all (one latency round for a whole staging phase).

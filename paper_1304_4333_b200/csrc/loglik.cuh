@@ -195,6 +195,7 @@ __global__ void __launch_bounds__(LL_THREADS, 2) k_loglik_bin(LLArgs a) {
   constexpr int LDX = ldx_of<K>();
   extern __shared__ __align__(16) double smem[];
   if (a.stop && *a.stop) return;
+  griddep_wait();  // launched with PDL: theta (the proposal kernel's output) after this
   double* sT = smem;
   double* sX = smem + 64;
   const int c0 = a.t0 + blockIdx.y * a.chunk;
@@ -250,7 +251,8 @@ __global__ void __launch_bounds__(LL_THREADS, 2) k_loglik_bin(LLArgs a) {
     for (int j = 0; j < PPT; ++j) {
       M[j] += relu_bits(s0[j]) + relu_bits(s1[j]);
       const double e0 = exp_neg(abs_clamp708(s0[j]), sT), e1 = exp_neg(abs_clamp708(s1[j]), sT);
-      Pp[j] *= (1.0 + e0) * (1.0 + e1);
+      Pp[j] = fma(Pp[j], e0, Pp[j]);  // Pp (1 + e): one FP64 op instead of an add and a multiply
+      Pp[j] = fma(Pp[j], e1, Pp[j]);
     }
     if ((t & 63) == 62) {
 #pragma unroll
@@ -274,7 +276,8 @@ __global__ void __launch_bounds__(LL_THREADS, 2) k_loglik_bin(LLArgs a) {
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
       M[j] += relu_bits(s0[j]);
-      Pp[j] *= 1.0 + exp_neg(abs_clamp708(s0[j]), sT);
+      const double e0 = exp_neg(abs_clamp708(s0[j]), sT);
+      Pp[j] = fma(Pp[j], e0, Pp[j]);
     }
   }
 #pragma unroll
@@ -296,6 +299,7 @@ __global__ void __launch_bounds__(LL_THREADS, 2) k_loglik_mnl(LLArgs a) {
   constexpr int LDX = ldx_of<K>();
   extern __shared__ __align__(16) double smem[];
   if (a.stop && *a.stop) return;
+  griddep_wait();  // launched with PDL: theta (the proposal kernel's output) after this
   double* sT = smem;
   double* sX = smem + 64;
   const int c0 = a.t0 + blockIdx.y * a.chunk;
@@ -415,6 +419,21 @@ __global__ void __launch_bounds__(128, MINB) k_loglik_bin_mma(LLArgs a) {
   for (int i = threadIdx.x; i < TAB; i += blockDim.x) sT[i] = TAB == 256 ? c_exp2tab256[i] : c_exp2tab[i];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, ar = lane >> 2, ac = lane & 3;
   const int64_t pw = ((int64_t)blockIdx.x * 4 + w) * (NTW * 8);  // first particle of this warp
+  const int sub = a.sub > 0 ? a.sub : ntot;  // X sub-chunk rows per shared buffer
+  const int SR = (sub + 15) & ~15;
+  __shared__ __align__(8) uint64_t xbar[2];
+  if (threadIdx.x == 0) {
+    mbar_init(&xbar[0], 1);
+    mbar_init(&xbar[1], 1);
+  }
+  __syncthreads();
+  auto issue = [&](int cs, int buf) {
+    const unsigned bytes = (unsigned)(min(sub, ntot - cs) * KP * 8);
+    mbar_arrive_expect_tx(&xbar[buf], bytes);
+    bulk_g2s(sX + buf * SR * KP, a.X + (int64_t)(c0 + cs) * KP, bytes, &xbar[buf]);
+  };
+  if (threadIdx.x == 0 && ntot > 0) issue(0, 0);
+  griddep_wait();  // theta* (the proposal kernel's output) from here on
   double b[NTW][KKD > 0 ? KKD : 1];
   double tr[NTW][2][REM > 0 ? REM : 1];  // remainder covariates of this lane's 2 particles per n-tile
 #pragma unroll
@@ -450,20 +469,6 @@ __global__ void __launch_bounds__(128, MINB) k_loglik_bin_mma(LLArgs a) {
   // copies: the next one loads while this one computes.  Rows past a sub-chunk's end hold stale
   // data; their products are masked out below (the per-thread load/store staging these copies
   // replace was ~28% of the stall samples, ncu r01_pa2).
-  const int sub = a.sub > 0 ? a.sub : ntot;
-  const int SR = (sub + 15) & ~15;
-  __shared__ __align__(8) uint64_t xbar[2];
-  if (threadIdx.x == 0) {
-    mbar_init(&xbar[0], 1);
-    mbar_init(&xbar[1], 1);
-  }
-  __syncthreads();
-  auto issue = [&](int cs, int buf) {
-    const unsigned bytes = (unsigned)(min(sub, ntot - cs) * KP * 8);
-    mbar_arrive_expect_tx(&xbar[buf], bytes);
-    bulk_g2s(sX + buf * SR * KP, a.X + (int64_t)(c0 + cs) * KP, bytes, &xbar[buf]);
-  };
-  if (threadIdx.x == 0 && ntot > 0) issue(0, 0);
   int it = 0;
   for (int cs = 0; cs < ntot; cs += sub, ++it) {
   const int nobs = min(sub, ntot - cs);
@@ -526,7 +531,8 @@ __global__ void __launch_bounds__(128, MINB) k_loglik_bin_mma(LLArgs a) {
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             M[nt][e] += relu_bits(acc[0][nt][e]);
-            Pp[nt][e] *= 1.0 + exp_neg_tab<TAB>(abs_clamp708(acc[0][nt][e]), sT);
+            const double ex = exp_neg_tab<TAB>(abs_clamp708(acc[0][nt][e]), sT);
+            Pp[nt][e] = fma(Pp[nt][e], ex, Pp[nt][e]);  // Pp (1 + e) in one FP64 op (12 per pair)
           }
       }
     } else {
@@ -538,7 +544,8 @@ __global__ void __launch_bounds__(128, MINB) k_loglik_bin_mma(LLArgs a) {
           const double s0 = v0 ? acc[0][nt][e] : -1e300, s1 = v1 ? acc[H - 1][nt][e] : -1e300;
           M[nt][e] += relu_bits(s0) + relu_bits(s1);
           const double e0 = exp_neg_tab<TAB>(abs_clamp708(s0), sT), e1 = exp_neg_tab<TAB>(abs_clamp708(s1), sT);
-          Pp[nt][e] *= (1.0 + e0) * (1.0 + e1);
+          Pp[nt][e] = fma(Pp[nt][e], e0, Pp[nt][e]);
+          Pp[nt][e] = fma(Pp[nt][e], e1, Pp[nt][e]);
         }
     }
     if ((++nit & 31) == 0) {
@@ -571,6 +578,7 @@ __global__ void __launch_bounds__(128, MINB) k_loglik_bin_mma(LLArgs a) {
         a.part[(int64_t)blockIdx.y * a.P + p] = -(m + (log(pp) + (double)ex * 0x1.62e42fefa39efp-1));
       }
     }
+  griddep_launch();
   tl_end(2);
 }
 

@@ -178,6 +178,7 @@ __global__ void __launch_bounds__(256, 3) k_propose_rb(DrawArgs a) {
   if (a.stop && *a.stop) return;
   if (a.set_step && blockIdx.x == 0 && threadIdx.x == 0) a.ctl->step_cur = a.step0 + (uint32_t)a.ctl->steps_done;
   if (a.set_step) tl_start(0);
+  griddep_launch();  // persistent grid (all CTAs resident): K1's CTAs may start their prologue
   const int d = a.d, BS = round_up(PR_TILE * d, 2);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, ar = lane >> 2, ac = lane & 3;
   double* Zs0 = sm;                     // 2 x PR_TILE x KP: Z rows, then (theta* - mu) rows (per warp, in place)
@@ -626,6 +627,8 @@ __global__ void __launch_bounds__(256) k_accept_tile(AccArgs a) {
   }
   double Ls = 0.0;  // K1 chunk partials of this thread's particle (sum in chunk order)
   const int q0 = threadIdx.x;
+  griddep_wait();    // K1's chunk partials from here on (the bulk copies above read older data)
+  griddep_launch();  // one wave: the reduce may start its launch
   if (dec && q0 < tp) {
     const int64_t p = pbase + q0;
     Ls = a.part[p];
@@ -1087,6 +1090,7 @@ __global__ void __launch_bounds__(256) k_mom_reduce(RedArgs r, Ctl* ctl, double*
   if (f.trace && threadIdx.x == 0) f.trace[8 + blockIdx.x] = gtimer();
   if (stop && *stop) return;
   if (f.mode == 1) tl_start(4);
+  griddep_wait();  // the accept kernel's block partials
   const int d = r.d, Jl = r.Jl, W = r.W, nblk = r.nblk, dd = d * d, nl = d * (d + 1) / 2;
   const int nm = (nl + 31) / 32, ng = (Jl * d + 255) / 256;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;

@@ -245,6 +245,24 @@ sps_status prof_end(sps_ctx* c, int cat);
     if (s_ != SPS_OK) return s_;       \
   } while (0)
 
+// Launch with programmatic stream serialization (PDL): the kernel may start
+// while its stream predecessor runs and synchronizes with griddep_wait().
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  static const bool off = getenv("SPS_NO_PDL") != nullptr;
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = grid;
+  lc.blockDim = block;
+  lc.dynamicSmemBytes = smem;
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = off ? 0 : 1;
+  return cudaLaunchKernelEx(&lc, kern, args...);
+}
+
 template <typename T>
 sps_status dalloc(sps_ctx* c, T** p, size_t count) {
   CU(c, cudaMalloc((void**)p, std::max<size_t>(count, 1) * sizeof(T)));
@@ -485,7 +503,7 @@ sps_status launch_loglik(sps_ctx* c, const double* theta, int64_t ldt, int64_t P
   a.sub = pl->sub;
   dim3 grid((unsigned)tiles, (unsigned)pl->S);
   PROF_BEGIN(c);
-  ch.fn<<<grid, LL_THREADS, pl->smem, c->stream>>>(a);
+  CU(c, launch_pdl(ch.fn, grid, dim3(LL_THREADS), pl->smem, c->stream, a));
   CHECK_LAUNCH(c);
   c->k1_launches += 1;
   c->k1_pairs += (double)P * range;
@@ -622,11 +640,11 @@ sps_status accept_moments(sps_ctx* c, bool decide, int nchunks, double temper, u
   PROF_BEGIN(c);
   if (c->acc_tnt > 0) {  // tile layout: bulk-staged rows, on-the-fly DMMA fragments, ones column
     switch (c->acc_tnt) {
-      case 1: k_accept_tile<1><<<c->nblk, 256, c->acc_smem, c->stream>>>(a); break;
-      case 2: k_accept_tile<2><<<c->nblk, 256, c->acc_smem, c->stream>>>(a); break;
-      case 3: k_accept_tile<3><<<c->nblk, 256, c->acc_smem, c->stream>>>(a); break;
-      case 4: k_accept_tile<4><<<c->nblk, 256, c->acc_smem, c->stream>>>(a); break;
-      default: k_accept_tile<5><<<c->nblk, 256, c->acc_smem, c->stream>>>(a); break;
+      case 1: CU(c, launch_pdl(k_accept_tile<1>, dim3(c->nblk), dim3(256), c->acc_smem, c->stream, a)); break;
+      case 2: CU(c, launch_pdl(k_accept_tile<2>, dim3(c->nblk), dim3(256), c->acc_smem, c->stream, a)); break;
+      case 3: CU(c, launch_pdl(k_accept_tile<3>, dim3(c->nblk), dim3(256), c->acc_smem, c->stream, a)); break;
+      case 4: CU(c, launch_pdl(k_accept_tile<4>, dim3(c->nblk), dim3(256), c->acc_smem, c->stream, a)); break;
+      default: CU(c, launch_pdl(k_accept_tile<5>, dim3(c->nblk), dim3(256), c->acc_smem, c->stream, a)); break;
     }
   } else if (c->d <= 32) {  // register-blocked T'T on DMMA
     const int NTr = (c->d + 7) / 8;
@@ -657,7 +675,8 @@ sps_status accept_moments(sps_ctx* c, bool decide, int nchunks, double temper, u
   RedArgs r{c->bpart, c->nblk, c->N / c->tp, c->Jl, d, c->acc_tnt > 0 ? c->Wt : c->W, c->acc_tnt, c->N, c->shift};
   FinArgs none{};
   PROF_BEGIN(c);
-  k_mom_reduce<<<nm + ng + 1, 256, fin ? fin_smem : 0, c->stream>>>(r, c->ctl, c->slice, stop, fin ? *fin : none);
+  CU(c, launch_pdl(k_mom_reduce, dim3(nm + ng + 1), dim3(256), fin ? fin_smem : 0, c->stream, r, c->ctl, c->slice, stop,
+                    fin ? *fin : none));
   CHECK_LAUNCH(c);
   PROF_END(c, fin ? CAT_FINALIZE : CAT_REDUCE);
   if (fin) return SPS_OK;  // one rank: the slice is the gathered stats, finalized by the last block
