@@ -123,6 +123,8 @@ struct LLArgs {
   int32_t k;           // covariates; theta block stride (K template >= k, zero padded)
   const int* stop;     // speculative M-step launches: return if set
   int32_t sub;         // DMMA kernel: observations per shared-memory sub-chunk (0: whole chunk)
+  int32_t tiles;       // DMMA kernel: particle tiles; items = tiles x chunks, item = tile + tiles * chunk
+  int32_t nitems;      //   (grid tiles x chunks: one item per block; a persistent grid loops over items)
 };
 
 // max(s, 0) and min(|s|, 708) with integer ops on the ALU pipe (sm_100a has no
@@ -412,28 +414,38 @@ __global__ void __launch_bounds__(128, MINB) k_loglik_bin_mma(LLArgs a) {
   if (a.stop && *a.stop) return;
   tl_start(2);
   double* sT = smem;        // TAB
-  double* sX = smem + 256;  // (chunk rounded up to 16) x KP
-  const int c0 = a.t0 + blockIdx.y * a.chunk;
-  const int c1 = min(c0 + a.chunk, a.t1);
-  const int ntot = max(c1 - c0, 0);
+  double* sX = smem + 256;  // 2 x (sub rounded up to 16) x KP
   for (int i = threadIdx.x; i < TAB; i += blockDim.x) sT[i] = TAB == 256 ? c_exp2tab256[i] : c_exp2tab[i];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, ar = lane >> 2, ac = lane & 3;
-  const int64_t pw = ((int64_t)blockIdx.x * 4 + w) * (NTW * 8);  // first particle of this warp
-  const int sub = a.sub > 0 ? a.sub : ntot;  // X sub-chunk rows per shared buffer
-  const int SR = (sub + 15) & ~15;
+  const int sub0 = a.sub;  // X sub-chunk rows per shared buffer (0: the whole chunk)
   __shared__ __align__(8) uint64_t xbar[2];
   if (threadIdx.x == 0) {
     mbar_init(&xbar[0], 1);
     mbar_init(&xbar[1], 1);
   }
   __syncthreads();
+  griddep_wait();  // theta* (the proposal kernel's output) from here on
+  int it = 0;            // sub-chunk loads issued so far (mbarrier phases)
+  int held_chunk = -1;   // chunk whose single sub-chunk is resident in buffer held_buf
+  int held_buf = 0;
+  const int stride = gridDim.x * gridDim.y;
+  for (int item = blockIdx.x + gridDim.x * blockIdx.y; item < a.nitems; item += stride) {
+  const int tile = item % a.tiles, cy = item / a.tiles;
+  const int c0 = a.t0 + cy * a.chunk;
+  const int c1 = min(c0 + a.chunk, a.t1);
+  const int ntot = max(c1 - c0, 0);
+  const int sub = sub0 > 0 ? sub0 : ntot;
+  const int SR = (sub + 15) & ~15;
+  const int64_t pw = ((int64_t)tile * 4 + w) * (NTW * 8);  // first particle of this warp
   auto issue = [&](int cs, int buf) {
     const unsigned bytes = (unsigned)(min(sub, ntot - cs) * KP * 8);
     mbar_arrive_expect_tx(&xbar[buf], bytes);
     bulk_g2s(sX + buf * SR * KP, a.X + (int64_t)(c0 + cs) * KP, bytes, &xbar[buf]);
   };
-  if (threadIdx.x == 0 && ntot > 0) issue(0, 0);
-  griddep_wait();  // theta* (the proposal kernel's output) from here on
+  // one sub-chunk: reuse it while consecutive items share the chunk (persistent grid)
+  const bool single = ntot <= sub;
+  const bool reuse = single && cy == held_chunk;
+  if (!reuse && threadIdx.x == 0 && ntot > 0) issue(0, it & 1);
   double b[NTW][KKD > 0 ? KKD : 1];
   double tr[NTW][2][REM > 0 ? REM : 1];  // remainder covariates of this lane's 2 particles per n-tile
 #pragma unroll
@@ -469,12 +481,19 @@ __global__ void __launch_bounds__(128, MINB) k_loglik_bin_mma(LLArgs a) {
   // copies: the next one loads while this one computes.  Rows past a sub-chunk's end hold stale
   // data; their products are masked out below (the per-thread load/store staging these copies
   // replace was ~28% of the stall samples, ncu r01_pa2).
-  int it = 0;
-  for (int cs = 0; cs < ntot; cs += sub, ++it) {
+  for (int cs = 0; cs < ntot; cs += sub) {
   const int nobs = min(sub, ntot - cs);
-  const int buf = it & 1;
-  if (threadIdx.x == 0 && cs + sub < ntot) issue(cs + sub, buf ^ 1);  // buf ^ 1 released by the barrier below
-  mbar_wait(&xbar[buf], (unsigned)(it >> 1) & 1u);
+  int buf;
+  if (reuse) {
+    buf = held_buf;
+  } else {
+    buf = it & 1;
+    if (threadIdx.x == 0 && cs + sub < ntot) issue(cs + sub, buf ^ 1);  // buf ^ 1 released by the barrier below
+    mbar_wait(&xbar[buf], (unsigned)(it >> 1) & 1u);
+    ++it;
+    held_chunk = single ? cy : -1;
+    held_buf = buf;
+  }
   const double* sXb = sX + buf * SR * KP;
   for (int t0 = 0; t0 < nobs; t0 += 8 * H) {
     double acc[H][NTW][2];
@@ -575,9 +594,10 @@ __global__ void __launch_bounds__(128, MINB) k_loglik_bin_mma(LLArgs a) {
       const int64_t p = pw + nt * 8 + 2 * ac + e;
       if (ar == 0 && p < a.P) {
         renorm(pp, ex);
-        a.part[(int64_t)blockIdx.y * a.P + p] = -(m + (log(pp) + (double)ex * 0x1.62e42fefa39efp-1));
+        a.part[(int64_t)cy * a.P + p] = -(m + (log(pp) + (double)ex * 0x1.62e42fefa39efp-1));
       }
     }
+  }  // items
   griddep_launch();
   tl_end(2);
 }

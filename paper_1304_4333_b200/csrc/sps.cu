@@ -167,7 +167,7 @@ struct sps_ctx {
   int ll_regs = 0;
   struct Plan {
     int64_t P = -1;
-    int range = -1, max_chunks = -1, S = 1, chunk = 0, sub = 0;
+    int range = -1, max_chunks = -1, S = 1, chunk = 0, sub = 0, occ = 1;
     size_t smem = 0;
   } plans[8];
   int plan_next = 0;
@@ -463,12 +463,14 @@ sps_status launch_loglik(sps_ctx* c, const double* theta, int64_t ldt, int64_t P
     // streaming (DMMA) kernels: two sub-chunk buffers (TMA double buffering) in the same budget
     const int sub_cap = std::max(16, (chunk_cap / 2) / 16 * 16);
     const int S_min = ch.streams ? 1 : std::max(1, (range + chunk_cap - 1) / chunk_cap);
-    const int S_hi = std::min(max_chunks, std::max(S_min, std::min(S_min + 24, range / 8)));
+    static const int s_cap = getenv("SPS_K1_SMAX") ? std::max(1, atoi(getenv("SPS_K1_SMAX"))) : 1 << 20;  // tuning
+    static const double ovh = getenv("SPS_K1_OVH") ? atof(getenv("SPS_K1_OVH")) : 24.0;
+    const int S_hi = std::min(std::min(max_chunks, s_cap), std::max(S_min, std::min(S_min + 24, range / 8)));
     const int warp_regs = ((c->ll_regs * 32 + 255) / 256) * 256;
     const int by_regs = 65536 / ((LL_THREADS / 32) * warp_regs);
     // cost ~ waves x (chunk + per-block overhead), overhead ~ 24 observation-equivalents
     // (theta load, X staging, final logs): fills whole waves without shredding the range
-    int best = S_min;
+    int best = S_min, best_occ = 1;
     double best_cost = 1e300;
     for (int S = S_min; S <= S_hi; ++S) {
       const int chunk = (range + S - 1) / S;
@@ -479,10 +481,11 @@ sps_status launch_loglik(sps_ctx* c, const double* theta, int64_t ldt, int64_t P
       const int occ = std::max(1, std::min(std::min(by_regs, by_smem), 16));
       const double slots = (double)num_sms() * occ;
       const double waves = std::ceil((double)tiles * Se / slots);
-      const double cost = waves * (chunk + 24.0);
+      const double cost = waves * (chunk + ovh);
       if (cost < best_cost * 0.995) {
         best_cost = cost;
         best = S;
+        best_occ = occ;
       }
     }
     int chunk = (range + best - 1) / best;
@@ -490,6 +493,7 @@ sps_status launch_loglik(sps_ctx* c, const double* theta, int64_t ldt, int64_t P
     pl->range = range;
     pl->max_chunks = max_chunks;
     pl->chunk = chunk;
+    pl->occ = best_occ;
     pl->S = (range + chunk - 1) / chunk;
     pl->sub = ch.streams ? std::min(((chunk + 15) / 16) * 16, sub_cap) : 0;
     const int rows = ch.streams ? pl->sub : chunk;
@@ -501,7 +505,12 @@ sps_status launch_loglik(sps_ctx* c, const double* theta, int64_t ldt, int64_t P
   a.k = c->k;
   a.stop = stop;
   a.sub = pl->sub;
+  a.tiles = (int32_t)tiles;
+  a.nitems = (int32_t)(tiles * pl->S);
   dim3 grid((unsigned)tiles, (unsigned)pl->S);
+  static const bool persist = getenv("SPS_K1_PERSIST") != nullptr;
+  if (persist && ch.streams)  // persistent: one wave of resident blocks loops over the items
+    grid = dim3((unsigned)std::min<int64_t>(tiles * pl->S, (int64_t)num_sms() * pl->occ), 1);
   PROF_BEGIN(c);
   CU(c, launch_pdl(ch.fn, grid, dim3(LL_THREADS), pl->smem, c->stream, a));
   CHECK_LAUNCH(c);
@@ -530,7 +539,8 @@ sps_status launch_normals(sps_ctx* c, uint32_t tag, uint32_t step, int slot, boo
     cudaLaunchConfig_t lc = {};
     // M steps: 2 blocks per SM (grid-stride); setup / first draws: full grid
     const int64_t full = (tasks + 255) / 256;
-    lc.gridDim = dim3((unsigned)(forked ? std::min<int64_t>(full, 4 * (int64_t)num_sms()) : full));
+    static const int nb_per_sm = getenv("SPS_NORMALS_BPS") ? atoi(getenv("SPS_NORMALS_BPS")) : 8;
+    lc.gridDim = dim3((unsigned)(forked && nb_per_sm > 0 ? std::min<int64_t>(full, nb_per_sm * (int64_t)num_sms()) : full));
     lc.blockDim = dim3(256);
     lc.stream = st;
     cudaLaunchAttribute at[1];
