@@ -265,7 +265,9 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 
 template <typename T>
 sps_status dalloc(sps_ctx* c, T** p, size_t count) {
-  CU(c, cudaMalloc((void**)p, std::max<size_t>(count, 1) * sizeof(T)));
+  // stream-ordered allocation from the device's default pool (release threshold raised once per
+  // device): a new context reuses memory cached by earlier ones instead of driver allocations
+  CU(c, cudaMallocAsync((void**)p, std::max<size_t>(count, 1) * sizeof(T), c->stream));
   return SPS_OK;
 }
 
@@ -779,35 +781,53 @@ sps_status validate(const sps_config* cfg) {
 
 void free_ctx(sps_ctx* c) {
   if (!c) return;
+  static const bool dbg = getenv("SPS_DEBUG_CLOSE") != nullptr;
+  auto T0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!dbg) return;
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "free_ctx %-10s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(t - T0).count());
+    T0 = t;
+  };
   if (c->G == 1) {  // aliases of the local slices
     c->gath = c->essgath = c->grp_ms_gath = c->Lj_gath = c->pw_gath = c->mx_gath = nullptr;
   }
   if (c->aux) cudaStreamSynchronize(c->aux);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  lap("sync");
+  cudaStream_t fs = c->stream ? c->stream : 0;
   for (double* z : c->Zbuf)
-    if (z) cudaFree(z);
+    if (z) cudaFreeAsync(z, fs);
   for (double* z : c->LUbuf)
-    if (z) cudaFree(z);
-  for (int q = 0; q < 2; ++q) {
+    if (z) cudaFreeAsync(z, fs);
+  lap("zbuf");
+  for (int q = 0; q < 2; ++q)
     if (c->gexec[q]) cudaGraphExecDestroy(c->gexec[q]);
+  lap("gexec");
+  for (int q = 0; q < 2; ++q) {
     if (c->ev_zready[q]) cudaEventDestroy(c->ev_zready[q]);
     if (c->ev_zfree[q]) cudaEventDestroy(c->ev_zfree[q]);
   }
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  lap("events");
   if (c->aux) cudaStreamDestroy(c->aux);
+  lap("graphs/ev");
   void* ptrs[] = {c->X, c->Xs, c->mu, c->Lprior, c->xbar, c->mon, c->y, c->theta, c->theta2, c->L, c->L2, c->lp,
                   c->lp2, c->lw, c->lw_cur, c->theta_s, c->lp_s, c->part, c->gpart, c->mpart, c->slice, c->gath,
                   c->shift, c->Lprop, c->V, c->rne, c->lwbuf, c->essparts, c->essslice, c->essgath, c->grp_ms,
                   c->grp_ms_gath, c->Lj, c->Lj_gath, c->scal, c->pw_parts, c->pw_slice, c->pw_gath, c->mx_parts,
                   c->mx_slice, c->mx_gath, c->fn_A, c->fn_out, c->ll_scratch, c->Sinv, c->LpriorP, c->SinvP, c->Rp, c->RpP, c->bpart, c->ctl};
   for (void* p : ptrs)
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, fs);
+  lap("cudaFree");
   if (c->hctl) cudaFreeHost(c->hctl);
   if (c->hslot) cudaFreeHost(c->hslot);
-  if (c->ticket) cudaFree(c->ticket);
-  if (c->trace) cudaFree(c->trace);
-  if (c->tl) cudaFree(c->tl);
+  lap("freeHost");
+  if (c->ticket) cudaFreeAsync(c->ticket, fs);
+  if (c->trace) cudaFree(c->trace);  // managed
+  if (c->tl) cudaFreeAsync(c->tl, fs);
+  cudaStreamSynchronize(fs);
   for (cudaEvent_t e : c->evs)
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : c->prof_pool) cudaEventDestroy(e);
@@ -815,6 +835,7 @@ void free_ctx(sps_ctx* c) {
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->comm) g_nccl.CommDestroy(c->comm);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  lap("rest");
 }
 
 constexpr int ESS_TILE = 2048;
@@ -948,6 +969,18 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
   c->max_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(64, ((int64_t)1 << 26) / std::max<int64_t>(c->Pl, 1)));
   c->Bmax = (int)std::max<int64_t>(8, std::min<int64_t>(256, ((int64_t)1 << 23) / std::max<int64_t>(c->Pl, 1)));
 
+  {  // keep freed device memory in the default pool across contexts (once per device)
+    static std::mutex mu;
+    static bool done[64] = {};
+    std::lock_guard<std::mutex> lk(mu);
+    if (cfg.device >= 0 && cfg.device < 64 && !done[cfg.device]) {
+      cudaMemPool_t pool;
+      CU(c, cudaDeviceGetDefaultMemPool(&pool, cfg.device));
+      uint64_t thr = ~0ull;
+      CU(c, cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+      done[cfg.device] = true;
+    }
+  }
   if (cfg.stream) {
     c->stream = (cudaStream_t)cfg.stream;
   } else {
@@ -990,7 +1023,7 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
   TRY(dalloc(c, &c->Sinv, (size_t)d * d));
   CU(c, cudaHostAlloc((void**)&c->hslot, 2 * sizeof(Ctl), cudaHostAllocMapped));
   CU(c, cudaHostGetDevicePointer((void**)&c->dslot, c->hslot, 0));
-  CU(c, cudaMalloc((void**)&c->ticket, sizeof(unsigned)));
+  TRY(dalloc(c, &c->ticket, 1));
   if (getenv("SPS_TRACE")) CU(c, cudaMallocManaged((void**)&c->trace, 128 * sizeof(unsigned long long)));
   CU(c, cudaMemsetAsync(c->ticket, 0, sizeof(unsigned), c->stream));
   CU(c, cudaEventCreateWithFlags(&c->evs[0], cudaEventDisableTiming));
@@ -1059,7 +1092,7 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
   else c->mx_gath = c->mx_slice;
   TRY(dalloc(c, &c->ctl, 1));
   if (getenv("SPS_TIMELINE")) {
-    CU(c, cudaMalloc((void**)&c->tl, sizeof(unsigned long long) * TL_W * TL_ROWS));
+    TRY(dalloc(c, &c->tl, (size_t)TL_W * TL_ROWS));
     CU(c, cudaMemsetAsync(c->tl, 0, sizeof(unsigned long long) * TL_W * TL_ROWS, c->stream));
     const int* steps = &c->ctl->steps_done;
     CU(c, cudaMemcpyToSymbolAsync(g_tl, &c->tl, sizeof(c->tl), 0, cudaMemcpyHostToDevice, c->stream));
@@ -1283,7 +1316,7 @@ sps_status sps_loglik(sps_ctx* c, const double* theta_dev, int64_t P, int32_t ld
   const int max_chunks = 64;
   const size_t need = (size_t)max_chunks * (size_t)P;
   if (need > c->ll_scratch_cap) {
-    if (c->ll_scratch) cudaFree(c->ll_scratch);
+    if (c->ll_scratch) cudaFreeAsync(c->ll_scratch, c->stream);
     c->ll_scratch = nullptr;
     c->ll_scratch_cap = 0;
     TRY(dalloc(c, &c->ll_scratch, need));
@@ -1696,8 +1729,8 @@ sps_status sps_moments(sps_ctx* c, int32_t m, const double* A, double* mean, dou
   if (m == 0) return SPS_OK;
   CU(c, cudaSetDevice(c->cfg.device));
   if (m > c->fn_cap) {
-    if (c->fn_A) cudaFree(c->fn_A);
-    if (c->fn_out) cudaFree(c->fn_out);
+    if (c->fn_A) cudaFreeAsync(c->fn_A, c->stream);
+    if (c->fn_out) cudaFreeAsync(c->fn_out, c->stream);
     c->fn_A = c->fn_out = nullptr;
     TRY(dalloc(c, &c->fn_A, (size_t)m * c->d));
     TRY(dalloc(c, &c->fn_out, (size_t)m * 4));
