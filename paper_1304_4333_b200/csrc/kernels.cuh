@@ -615,13 +615,14 @@ __global__ void __launch_bounds__(1024) k_resample(const double* __restrict__ lw
 }
 
 // Pooled log-ML increment from all groups' (m_j, s_j) in group order (R10).
-__global__ void k_logml_pooled(const double* __restrict__ gath_ms, int J, double P, Ctl* ctl) {
+__global__ void k_logml_pooled(const double* __restrict__ gath_ms, int J, double P, Ctl* ctl, double* inc_out) {
   if (threadIdx.x != 0) return;
   double M = -INFINITY;
   for (int j = 0; j < J; ++j) M = fmax(M, gath_ms[j * 2]);
   double S = 0.0;
   for (int j = 0; j < J; ++j) S += gath_ms[j * 2 + 1] * exp(gath_ms[j * 2] - M);
   ctl->logml_inc = M + log(S / P);
+  if (inc_out) *inc_out = ctl->logml_inc;  // per-cycle record, read by the host when needed
 }
 
 // NSE of log ML across groups (R10) from the gathered per-group L_j.

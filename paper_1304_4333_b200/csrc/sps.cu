@@ -186,6 +186,11 @@ struct sps_ctx {
   double logml = 0.0, pairs = 0.0;
   std::vector<int> tr_t, tr_R, tr_h;
   std::vector<double> tr_phi, tr_inc, tr_rne;
+  // log-ML increments are recorded on the device (inc_dev, cycles inc_base..ell-1) and pulled to the
+  // host (tr_inc, logml, in cycle order) only when needed: no host round trip per C phase
+  double* inc_dev = nullptr;
+  int inc_cap = 1024, inc_base = 0;
+  int last_adv = 0;  // observations absorbed by the last data-tempering C phase (first galloping chunk)
   // counters (sps_get_counters)
   int64_t launches = 0, k1_launches = 0, syncs = 0;
   double k1_pairs = 0.0, k1_ms = 0.0;
@@ -817,7 +822,7 @@ void free_ctx(sps_ctx* c) {
                   c->lp2, c->lw, c->lw_cur, c->theta_s, c->lp_s, c->part, c->gpart, c->mpart, c->slice, c->gath,
                   c->shift, c->Lprop, c->V, c->rne, c->lwbuf, c->essparts, c->essslice, c->essgath, c->grp_ms,
                   c->grp_ms_gath, c->Lj, c->Lj_gath, c->scal, c->pw_parts, c->pw_slice, c->pw_gath, c->mx_parts,
-                  c->mx_slice, c->mx_gath, c->fn_A, c->fn_out, c->ll_scratch, c->Sinv, c->LpriorP, c->SinvP, c->Rp, c->RpP, c->bpart, c->ctl};
+                  c->mx_slice, c->mx_gath, c->fn_A, c->fn_out, c->ll_scratch, c->Sinv, c->LpriorP, c->SinvP, c->Rp, c->RpP, c->bpart, c->ctl, c->inc_dev};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, fs);
   lap("cudaFree");
@@ -1071,6 +1076,7 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
   TRY(dalloc(c, &c->essparts, (size_t)c->Bmax * ntiles * 3));
   TRY(dalloc(c, &c->essslice, (size_t)c->Bmax * 3));
   TRY(dalloc(c, &c->grp_ms, (size_t)c->Jl * 2));
+  TRY(dalloc(c, &c->inc_dev, (size_t)c->inc_cap));
   TRY(dalloc(c, &c->Lj, (size_t)c->Jl));
   if (c->G > 1) {
     TRY(dalloc(c, &c->essgath, (size_t)c->Bmax * 3 * c->G));
@@ -1214,6 +1220,8 @@ sps_status sps_reset(sps_ctx* c, uint64_t seed, int32_t pass) {
   c->tr_phi.clear();
   c->tr_inc.clear();
   c->tr_rne.clear();
+  c->inc_base = 0;
+  c->last_adv = 0;
   c->launches = c->k1_launches = c->syncs = 0;
   c->k1_pairs = c->k1_ms = 0.0;
   c->host_launch_us = c->host_wait_us = c->host_graph_us = 0.0;
@@ -1339,6 +1347,21 @@ sps_status sps_sync(sps_ctx* c) {
 }
 
 // One C phase + S phase.
+// Pull the device-recorded log-ML increments of cycles inc_base..ell-1 (cycle order).
+static sps_status sync_incs(sps_ctx* c) {
+  const int pending = c->ell - c->inc_base;
+  if (pending <= 0) return SPS_OK;
+  std::vector<double> h((size_t)pending);
+  CU(c, cudaMemcpyAsync(h.data(), c->inc_dev, sizeof(double) * pending, cudaMemcpyDeviceToHost, c->stream));
+  CU(c, cudaStreamSynchronize(c->stream));
+  for (double inc : h) {
+    c->logml += inc;
+    c->tr_inc.push_back(inc);
+  }
+  c->inc_base = c->ell;
+  return SPS_OK;
+}
+
 sps_status sps_cphase(sps_ctx* c, int32_t t_target, double phi_target, int32_t* t_new, double* phi_new,
                       double* logml_inc) {
   if (!c) return SPS_E_CONFIG;
@@ -1355,7 +1378,8 @@ sps_status sps_cphase(sps_ctx* c, int32_t t_target, double phi_target, int32_t* 
       return fail(c, SPS_E_CONFIG, "t_target out of range");
     CU(c, cudaMemsetAsync(c->lw_cur, 0, sizeof(double) * Pl, c->stream));
     int s = c->t;
-    int B = 8;
+    int B = 8;  // first galloping chunk: twice the last cycle's advance (usually one chunk, one sync)
+    while (B < 2 * c->last_adv && B < c->Bmax) B *= 2;
     const int ntiles = (int)((Pl + ESS_TILE - 1) / ESS_TILE);
     const size_t scan_smem = sizeof(double) * c->d * 128;
     CU(c, cudaFuncSetAttribute(k_cphase_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem + 1024));
@@ -1384,6 +1408,7 @@ sps_status sps_cphase(sps_ctx* c, int32_t t_target, double phi_target, int32_t* 
       if (sstar > 0) {
         k_take_lw<<<pgrid, 256, 0, c->stream>>>(c->lwbuf, sstar - s - 1, Pl, c->lw, c->L);
         CHECK_LAUNCH(c);
+        c->last_adv = sstar - c->t;
         c->t = sstar;
         break;
       }
@@ -1448,21 +1473,22 @@ sps_status sps_cphase(sps_ctx* c, int32_t t_target, double phi_target, int32_t* 
     std::swap(c->L, c->L2);
     std::swap(c->lp, c->lp2);
     TRY(gather(c, c->grp_ms, c->grp_ms_gath, (size_t)c->Jl * 2));
-    k_logml_pooled<<<1, 32, 0, c->stream>>>(c->grp_ms_gath, c->J, P, c->ctl);
+    if (c->ell - 1 - c->inc_base >= c->inc_cap) TRY(sync_incs(c));  // (ell was incremented above)
+    k_logml_pooled<<<1, 32, 0, c->stream>>>(c->grp_ms_gath, c->J, P, c->ctl, c->inc_dev + (c->ell - 1 - c->inc_base));
     CHECK_LAUNCH(c);
   }
   PROF_END(c, CAT_RESAMPLE);
-  TRY(read_ctl(c));
-  const double inc = c->hctl->logml_inc;
-  c->logml += inc;
   c->need_pre_moments = true;
   c->cphase_done = true;
   c->tr_t.push_back(c->t);
   c->tr_phi.push_back(c->phi);
-  c->tr_inc.push_back(inc);
   if (t_new) *t_new = c->t;
   if (phi_new) *phi_new = c->phi;
-  if (logml_inc) *logml_inc = inc;
+  if (logml_inc) {  // the caller wants it now: one round trip (sps_run does not ask)
+    TRY(sync_incs(c));
+    TRY(read_ctl(c));
+    *logml_inc = c->tr_inc.back();
+  }
   return SPS_OK;
 }
 
@@ -1713,6 +1739,7 @@ sps_status sps_mphase(sps_ctx* c, int32_t R_fixed, int32_t* R_out, double* min_r
 sps_status sps_logml(sps_ctx* c, double* logml, double* nse) {
   if (!c) return SPS_E_CONFIG;
   CU(c, cudaSetDevice(c->cfg.device));
+  TRY(sync_incs(c));
   if (logml) *logml = c->logml;
   if (nse) {
     TRY(gather(c, c->Lj, c->Lj_gath, (size_t)c->Jl));
@@ -1769,6 +1796,7 @@ sps_status sps_run(sps_ctx* c, sps_report* rep) {
   for (int r : c->tr_R) rep->total_m_steps += r;
   rep->h_final = c->hctl->h;
   rep->pairs = c->pairs;
+  if (sync_incs(c) != SPS_OK && st == SPS_OK) st = SPS_E_CUDA;
   const int L = (int)c->tr_t.size();
   for (int l = 0; l < std::min(L, rep->cap_cycles); ++l) {
     if (rep->t_cycle) rep->t_cycle[l] = c->tr_t[l];
