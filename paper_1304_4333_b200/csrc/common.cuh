@@ -167,6 +167,13 @@ __device__ __forceinline__ void tl_start(int k) {
     if (r >= 0 && r < TL_ROWS) tl[r * TL_W + 2 * k] = gtimer();
   }
 }
+__device__ __forceinline__ void tl_mark(int slot) {  // block (0,0) thread 0: a phase clock in slot 12..15
+  unsigned long long* tl = g_tl;
+  if (tl && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+    const int r = *g_tl_steps;
+    if (r >= 0 && r < TL_ROWS) tl[r * TL_W + slot] = gtimer();
+  }
+}
 __device__ __forceinline__ void tl_end(int k) {
   unsigned long long* tl = g_tl;
   if (tl && threadIdx.x == 0) {

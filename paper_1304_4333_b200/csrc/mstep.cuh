@@ -637,6 +637,7 @@ __global__ void __launch_bounds__(256) k_accept_tile(AccArgs a) {
   __syncthreads();  // barrier initialised
   mbar_wait(&bar, 0);
   if (tr) a.trace[65] = gtimer();
+  if (dec) tl_mark(12);
   int nacc = 0;
   for (int q = q0; q < tp; q += blockDim.x) {
     unsigned char ok = 0;
@@ -666,19 +667,22 @@ __global__ void __launch_bounds__(256) k_accept_tile(AccArgs a) {
   }
   nacc = block_sum(nacc, red_i);  // (barrier) acc visible
   if (tr) a.trace[66] = gtimer();
-  if (dec) {  // accepted rows only: theta* -> theta (global, L2-resident) and over the staged rows
+  if (dec) tl_mark(13);
+  if (dec) {  // accepted rows only: theta* over the staged rows (one cp.async round), then back to theta
     const double* ts = a.theta_s + pbase * d;
     double* th = a.theta + pbase * d;
-#pragma unroll 4
+#pragma unroll 5
     for (int e = threadIdx.x; e < TD; e += blockDim.x) {
       const int q = (int)(((uint64_t)e * a.dmagic) >> 32);
-      if (acc[q]) {
-        const double v = __ldcg(ts + e);
-        th[e] = v;
-        sTh[e] = v;
-      }
+      if (acc[q]) cp_async8(sTh + e, ts + e);
     }
+    cp_async_wait_all();
     __syncthreads();
+#pragma unroll 5
+    for (int e = threadIdx.x; e < TD; e += blockDim.x) {
+      const int q = (int)(((uint64_t)e * a.dmagic) >> 32);
+      if (acc[q]) th[e] = sTh[e];
+    }
   }
   // T'T, lower tiles; warp w takes k-steps k0 = 4 (w + 8 m)
   double cacc[NTRI][2];
@@ -705,6 +709,7 @@ __global__ void __launch_bounds__(256) k_accept_tile(AccArgs a) {
   }
   __syncthreads();  // row tiles consumed: the region holds the warp partials
   if (tr) a.trace[67] = gtimer();
+  if (dec) tl_mark(14);
   double* wp = sm;  // 8 x NTRI x 64
 #pragma unroll
   for (int t = 0; t < NTRI; ++t) {

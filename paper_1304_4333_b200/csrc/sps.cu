@@ -147,7 +147,7 @@ struct sps_ctx {
   unsigned* ticket = nullptr;      // arrival counter of the fused reduce + finalize (k_mom_reduce)
   unsigned long long* trace = nullptr;  // debug (SPS_TRACE): finalize / reduce phase clocks (managed)
   unsigned long long* tl = nullptr;     // debug (SPS_TIMELINE): per-step kernel start / end clocks
-  double tl_acc[16] = {};
+  double tl_acc[20] = {};
   int tl_rows = 0;
   double trace_acc[80] = {};
   int trace_n = 0;
@@ -1283,9 +1283,10 @@ sps_status sps_get_counters(const sps_ctx* cc, sps_counters* out) {
   if (c->tl && c->tl_rows) {
     static const char* nm[] = {"propose", "normals", "K1", "accept", "reduce", "finalize", "gap K1<-propose",
                                "gap accept<-K1", "gap reduce<-accept", "gap fin<-reduce", "normals start-propose end",
-                               "normals end-K1 end", "gap next propose<-fin", "step"};
+                               "normals end-K1 end", "gap next propose<-fin", "step", "acc0 load", "acc0 decide",
+                               "acc0 wb+dmma", "acc0 combine..end(all)"};
     fprintf(stderr, "SPS_TIMELINE mean us over %d steps:", c->tl_rows);
-    for (int q = 0; q < 14; ++q) fprintf(stderr, " %s=%.2f", nm[q], c->tl_acc[q] / c->tl_rows / 1e3);
+    for (int q = 0; q < 18; ++q) fprintf(stderr, " %s=%.2f", nm[q], c->tl_acc[q] / c->tl_rows / 1e3);
     fprintf(stderr, "\n");
   }
   out->launches = c->launches;
@@ -1548,6 +1549,12 @@ static sps_status timeline_accumulate(sps_ctx* c, int R) {
     c->tl_acc[11] += (double)t[3] - (double)t[5];   // normals end - K1 end
     if (r + 1 < rows && h[(size_t)(r + 1) * TL_W]) c->tl_acc[12] += (double)h[(size_t)(r + 1) * TL_W] - (double)t[11];
     c->tl_acc[13] += (double)t[11] - (double)t[0];  // step: propose start -> finalize end
+    if (t[12] && t[13] && t[14]) {  // accept block 0: load / decide+writeback / dmma phases
+      c->tl_acc[14] += (double)t[12] - (double)t[6];
+      c->tl_acc[15] += (double)t[13] - (double)t[12];
+      c->tl_acc[16] += (double)t[14] - (double)t[13];
+      c->tl_acc[17] += (double)t[7] - (double)t[14];
+    }
     c->tl_rows += 1;
   }
   CU(c, cudaMemsetAsync(c->tl, 0, sizeof(unsigned long long) * TL_W * TL_ROWS, c->stream));
