@@ -31,6 +31,7 @@ struct DrawArgs {
   int d;
   uint32_t step0;  // set_step: ctl->step_cur = step0 + ctl->steps_done (device-resident step of a graph replay)
   int set_step;
+  const double* Zalt;  // device-side loop: Z of odd steps (Z: even steps), chosen by the parity of step_cur
 };
 
 // Standard normals of the streams (id = p0 + p, step, tag) for every local
@@ -41,14 +42,20 @@ struct DrawArgs {
 // particle (R16), so the accept test on the critical path is one comparison.
 // With `sctl` (M steps replayed from a CUDA graph) the step is device-resident:
 // step = sctl->step_cur + 1, written by the proposal kernel of the running step.
+// Zalt / logualt (device-side loop): the outputs of odd steps (Z / logu: even steps).
 __global__ void __launch_bounds__(256) k_normals(int64_t P, int64_t p0, int np, int ldz, uint64_t seed, uint32_t step,
                                                  uint32_t tag, uint32_t pass, double* __restrict__ Z,
-                                                 double* __restrict__ logu, const Ctl* sctl, const int* stop) {
+                                                 double* __restrict__ logu, const Ctl* sctl, const int* stop,
+                                                 double* Zalt, double* logualt) {
   // grid-stride over (particle, pair) tasks: the engine launches a small persistent grid so
   // the side-stream normals share SMs with the critical path instead of filling them
   if (stop && *stop) return;
   if (sctl) step = sctl->step_cur + 1u;
   if (sctl) tl_start(1);
+  if (Zalt && (step & 1u)) {
+    Z = Zalt;
+    if (logu) logu = logualt;
+  }
   const int64_t ntask = P * np;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntask; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t p = t / np;
@@ -76,6 +83,8 @@ __global__ void __launch_bounds__(256) k_propose(DrawArgs a) {
   extern __shared__ double sm[];
   if (a.stop && *a.stop) return;
   if (a.set_step && blockIdx.x == 0 && threadIdx.x == 0) a.ctl->step_cur = a.step0 + (uint32_t)a.ctl->steps_done;
+  const double* Zsrc = a.Z;
+  if (a.Zalt && ((a.step0 + (uint32_t)a.ctl->steps_done) & 1u)) Zsrc = a.Zalt;
   const int d = a.d, np = (d + 1) / 2, d2 = 2 * np, KP = round_up(d, 4), NP = round_up(d, 8), NT = NP / 8;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   double* Zs = sm;                  // PR_TILE x KP
@@ -105,7 +114,7 @@ __global__ void __launch_bounds__(256) k_propose(DrawArgs a) {
       const unsigned bb = a.base ? (unsigned)(round_up(cnt * d, 2) * 8) : 0u;
       const unsigned mb = (STAGE && phase == 0) ? (unsigned)(NP * KP * 8) : 0u;
       mbar_arrive_expect_tx(&bar, zb + bb + 2 * mb);
-      bulk_g2s(Zs, a.Z + pb * KP, zb, &bar);
+      bulk_g2s(Zs, Zsrc + pb * KP, zb, &bar);
       if (a.base) bulk_g2s(Bs, a.base + pb * d, bb, &bar);
       if (mb) {
         bulk_g2s(sL, a.Lz, mb, &bar);
@@ -179,6 +188,8 @@ __global__ void __launch_bounds__(256, 3) k_propose_rb(DrawArgs a) {
   if (a.set_step && blockIdx.x == 0 && threadIdx.x == 0) a.ctl->step_cur = a.step0 + (uint32_t)a.ctl->steps_done;
   if (a.set_step) tl_start(0);
   griddep_launch();  // persistent grid (all CTAs resident): K1's CTAs may start their prologue
+  const double* Zsrc = a.Z;
+  if (a.Zalt && ((a.step0 + (uint32_t)a.ctl->steps_done) & 1u)) Zsrc = a.Zalt;
   const int d = a.d, BS = round_up(PR_TILE * d, 2);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, ar = lane >> 2, ac = lane & 3;
   double* Zs0 = sm;                     // 2 x PR_TILE x KP: Z rows, then (theta* - mu) rows (per warp, in place)
@@ -202,7 +213,7 @@ __global__ void __launch_bounds__(256, 3) k_propose_rb(DrawArgs a) {
     const unsigned bb = a.base ? (unsigned)(round_up(cnt * d, 2) * 8) : 0u;
     const unsigned mb = first ? (unsigned)(NP * KP * 8) : 0u;
     mbar_arrive_expect_tx(&bar[buf], zb + bb + 2 * mb);
-    bulk_g2s(Zs0 + buf * PR_TILE * KP, a.Z + pb * KP, zb, &bar[buf]);
+    bulk_g2s(Zs0 + buf * PR_TILE * KP, Zsrc + pb * KP, zb, &bar[buf]);
     if (a.base) bulk_g2s(Bs0 + buf * BS, a.base + pb * d, bb, &bar[buf]);
     if (mb) {
       bulk_g2s(sL, a.Lz, mb, &bar[buf]);
@@ -306,6 +317,8 @@ struct AccArgs {
   int nchunks, d, tp, decide;
   uint32_t step, pass;
   uint64_t dmagic, pmagic;  // ceil(2^32 / d), ceil(2^32 / (LT - d)): e / m = (e * magic) >> 32 for e < 2^16
+  const double* logualt;    // device-side loop: log u of odd steps (step = step0 + ctl->steps_done)
+  uint32_t step0;
 };
 
 // Block = tp (<= 256, divides N) particles of one group, 256 threads.
@@ -334,7 +347,7 @@ __global__ void __launch_bounds__(256) k_accept_mom(AccArgs a) {
       const double delta = a.temper * (Ls - Lc) + (lps - lpc);
       double lu;
       if (a.logu) {
-        lu = a.logu[p];
+        lu = (a.logualt && ((a.step0 + (uint32_t)a.ctl->steps_done) & 1u)) ? a.logualt[p] : a.logu[p];
       } else {
         const u4 wv = stream_block(a.seed, 0u, (uint32_t)(a.p0 + p), a.step, TAG_ACCEPT, a.pass);
         lu = plog(u01(wv.x, wv.y));
@@ -471,7 +484,7 @@ __global__ void __launch_bounds__(256) k_accept_mom_rb(AccArgs a) {
       const double delta = a.temper * (Ls - Lc) + (lps - lpc);
       double lu;
       if (a.logu) {
-        lu = a.logu[p];
+        lu = (a.logualt && ((a.step0 + (uint32_t)a.ctl->steps_done) & 1u)) ? a.logualt[p] : a.logu[p];
       } else {
         const u4 wv = stream_block(a.seed, 0u, (uint32_t)(a.p0 + p), a.step, TAG_ACCEPT, a.pass);
         lu = plog(u01(wv.x, wv.y));
@@ -607,6 +620,8 @@ __global__ void __launch_bounds__(256) k_accept_tile(AccArgs a) {
   double* sv = sm + treg;                    // [L | lp | lp* | log u] x tp
   unsigned char* acc = reinterpret_cast<unsigned char*>(sv + 4 * tp);
   const int64_t pbase = (int64_t)blockIdx.x * tp;
+  const double* logu = a.logu;
+  if (a.logualt && ((a.step0 + (uint32_t)a.ctl->steps_done) & 1u)) logu = a.logualt;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     const unsigned rb = (unsigned)TD * 8u, vb = (unsigned)tp * 8u;
@@ -616,7 +631,7 @@ __global__ void __launch_bounds__(256) k_accept_tile(AccArgs a) {
       bulk_g2s(sv, a.L + pbase, vb, &bar);
       bulk_g2s(sv + tp, a.lp + pbase, vb, &bar);
       bulk_g2s(sv + 2 * tp, a.lp_s + pbase, vb, &bar);
-      if (a.logu) bulk_g2s(sv + 3 * tp, a.logu + pbase, vb, &bar);
+      if (logu) bulk_g2s(sv + 3 * tp, logu + pbase, vb, &bar);
     }
   }
   double shv[NT];  // c_i of this lane's fragment columns
@@ -1052,8 +1067,13 @@ __device__ void finalize_body(const FinArgs& f, double* sm) {
       minrne = fmin(minrne, rne);
     }
     f.ctl->minrne = minrne;
-    f.ctl->stop = (f.K > 0.0 && minrne >= f.K) ? 1 : 0;
-    f.ctl->steps_done += 1;
+    const int done = f.ctl->steps_done + 1;
+    // stop: 1 = min RNE >= K; 2 = the device-side loop reached its step cap
+    const int stop = (f.K > 0.0 && minrne >= f.K) ? 1 : ((f.loop && done >= f.rmax) ? 2 : 0);
+    f.ctl->stop = stop;
+    f.ctl->steps_done = done;
+    // device-side M phase (a WHILE graph node, two steps per body): continue unless stopped
+    if (f.loop) cudaGraphSetConditional(f.cond, stop == 0 ? 1u : 0u);
   }
 #pragma unroll 1
   for (int idx = threadIdx.x; idx < dd; idx += blockDim.x) f.V[idx] = sV[idx];

@@ -162,7 +162,14 @@ struct sps_ctx {
   int64_t g_launches[2] = {0, 0}, g_k1[2] = {0, 0};
   double g_pairs[2] = {0, 0};
   int graph_updates = 0, graph_instantiations = 0;
-  bool capturing = false;  // inside build_mstep_graphs
+  bool capturing = false;  // inside build_mstep_graphs / build_mstep_loop
+  // device-side M phase: one WHILE graph node whose body is one M step (one rank)
+  bool capturing_loop = false;
+  cudaGraphExec_t gloop = nullptr;
+  cudaGraphConditionalHandle loop_cond = 0;
+  int loop_rmax = 0;
+  int64_t gl_launches = 0, gl_k1 = 0;
+  double gl_pairs = 0;
   LLChoice_t llc{};
   int ll_regs = 0;
   struct Plan {
@@ -558,9 +565,11 @@ sps_status launch_normals(sps_ctx* c, uint32_t tag, uint32_t step, int slot, boo
     lc.attrs = at;
     lc.numAttrs = 1;
     CU(c, cudaLaunchKernelEx(&lc, k_normals, (int64_t)c->Pl, (int64_t)c->p0, np, round_up(c->d, 4), (uint64_t)c->cfg.seed,
-                             step, tag, (uint32_t)c->cfg.pass, c->Zbuf[slot],
-                             tag == TAG_PROPOSAL ? c->LUbuf[slot] : (double*)nullptr, graph ? (const Ctl*)c->ctl : nullptr,
-                             graph ? (const int*)&c->ctl->stop : nullptr));
+                             step, tag, (uint32_t)c->cfg.pass, c->capturing_loop ? c->Zbuf[0] : c->Zbuf[slot],
+                             tag == TAG_PROPOSAL ? (c->capturing_loop ? c->LUbuf[0] : c->LUbuf[slot]) : (double*)nullptr,
+                             graph ? (const Ctl*)c->ctl : nullptr, graph ? (const int*)&c->ctl->stop : nullptr,
+                             c->capturing_loop ? c->Zbuf[1] : (double*)nullptr,
+                             c->capturing_loop ? c->LUbuf[1] : (double*)nullptr));
   }
   CHECK_LAUNCH(c);
   if (serial && !graph) PROF_END(c, CAT_OTHER);
@@ -591,6 +600,10 @@ sps_status launch_draw(sps_ctx* c, int slot, const double* base, const double* L
   a.d = d;
   a.step0 = c->phase_step0;
   a.set_step = set_step ? 1 : 0;
+  if (c->capturing_loop) {  // device-side loop: the parity of the device step picks the buffer
+    a.Z = c->Zbuf[0];
+    a.Zalt = c->Zbuf[1];
+  }
   if (!graph) CU(c, cudaStreamWaitEvent(c->stream, c->ev_zready[slot], 0));
   const int64_t ntl = (c->Pl + PR_TILE - 1) / PR_TILE;
   PROF_BEGIN(c);
@@ -654,6 +667,11 @@ sps_status accept_moments(sps_ctx* c, bool decide, int nchunks, double temper, u
   a.pass = (uint32_t)c->cfg.pass;
   a.dmagic = ((1ull << 32) + (uint64_t)c->d - 1) / (uint64_t)c->d;
   a.trace = decide ? c->trace : nullptr;
+  if (c->capturing_loop && logu) {
+    a.logu = c->LUbuf[0];
+    a.logualt = c->LUbuf[1];
+    a.step0 = c->phase_step0;
+  }
   PROF_BEGIN(c);
   if (c->acc_tnt > 0) {  // tile layout: bulk-staged rows, on-the-fly DMMA fragments, ones column
     switch (c->acc_tnt) {
@@ -733,6 +751,12 @@ sps_status make_fin(sps_ctx* c, int mode, bool allow_stop, const int* stop, int 
   f.stop_in = stop;
   f.rne_out = c->rne;
   f.trace = c->trace;
+  if (c->capturing_loop && mode == 1) {
+    f.loop = 1;
+    f.cond = c->loop_cond;
+    f.rmax = c->loop_rmax;
+    f.host_out = c->dslot;
+  }
   f.stage_S = fin_smem_doubles(c->d, c->J, c->nmon, true) * 8 <= 200 * 1024 ? 1 : 0;
   const size_t smem = (size_t)fin_smem_doubles(c->d, c->J, c->nmon, f.stage_S != 0) * sizeof(double);
   if (smem > 200 * 1024) return fail(c, SPS_E_CONFIG, "d = %d too large for the finalize kernel", c->d);
@@ -808,6 +832,7 @@ void free_ctx(sps_ctx* c) {
   lap("zbuf");
   for (int q = 0; q < 2; ++q)
     if (c->gexec[q]) cudaGraphExecDestroy(c->gexec[q]);
+  if (c->gloop) cudaGraphExecDestroy(c->gloop);
   lap("gexec");
   for (int q = 0; q < 2; ++q) {
     if (c->ev_zready[q]) cudaEventDestroy(c->ev_zready[q]);
@@ -1584,7 +1609,7 @@ static sps_status launch_mstep(sps_ctx* c, uint32_t step, bool allow_stop, bool 
   TRY(moments_finalize(c, true, nch, temper, step, stop, c->LUbuf[zs], 1, allow_stop, zs, true));
   if (graph) {
     CU(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
-    CU(c, cudaEventRecordWithFlags(c->evs[zs], c->stream, cudaEventRecordExternal));
+    if (!c->capturing_loop) CU(c, cudaEventRecordWithFlags(c->evs[zs], c->stream, cudaEventRecordExternal));
   } else {
     CU(c, cudaEventRecord(c->ev_zfree[zs], c->stream));  // Zbuf / LUbuf[zs] consumed
     CU(c, cudaEventRecord(c->evs[zs], c->stream));
@@ -1662,6 +1687,67 @@ static sps_status build_mstep_graphs(sps_ctx* c, bool allow_stop) {
   return SPS_OK;
 }
 
+// Device-side M phase: a graph with one WHILE node whose body (captured from one M step) runs until
+// the finalize kernel clears the condition (min RNE >= K, or the step cap).  Captured per phase and
+// applied to the previous executable graph with cudaGraphExecUpdate when possible.
+static sps_status build_mstep_loop(sps_ctx* c, bool allow_stop, int rmax) {
+  cudaGraph_t g = nullptr;
+  CU(c, cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  CU(c, cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams np = {};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = h;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  cudaGraphNode_t cn;
+  CU(c, cudaGraphAddNode(&cn, g, nullptr, 0, &np));
+  cudaGraph_t body = np.conditional.phGraph_out[0];
+  const int64_t l0 = c->launches, k0 = c->k1_launches;
+  const double p0 = c->k1_pairs;
+  c->loop_cond = h;
+  c->loop_rmax = rmax;
+  CU(c, cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  c->capturing = c->capturing_loop = true;
+  // two M steps per body: half the loop-iteration boundaries (~4.8 us each vs ~1.5 between kernels);
+  // after a stop the second step's kernels return at once
+  sps_status st = launch_mstep(c, c->phase_step0, allow_stop, true);
+  if (st == SPS_OK) st = launch_mstep(c, c->phase_step0 + 1u, allow_stop, true);
+  c->capturing = c->capturing_loop = false;
+  cudaGraph_t captured = nullptr;
+  const cudaError_t ee = cudaStreamEndCapture(c->stream, &captured);
+  if (st != SPS_OK || ee != cudaSuccess) {
+    cudaGraphDestroy(g);
+    if (st != SPS_OK) return st;
+    CU(c, ee);
+  }
+  TRY(set_node_priorities(c, body));
+  c->gl_launches = c->launches - l0;
+  c->gl_k1 = c->k1_launches - k0;
+  c->gl_pairs = c->k1_pairs - p0;
+  c->launches = l0;
+  c->k1_launches = k0;
+  c->k1_pairs = p0;
+  bool ok = false;
+  if (c->gloop) {
+    cudaGraphExecUpdateResultInfo info;
+    ok = cudaGraphExecUpdate(c->gloop, g, &info) == cudaSuccess;
+    if (ok) c->graph_updates += 1;
+    cudaGetLastError();
+  }
+  if (!ok) {
+    if (c->gloop) cudaGraphExecDestroy(c->gloop);
+    c->gloop = nullptr;
+    const cudaError_t ei = cudaGraphInstantiateWithFlags(&c->gloop, g, cudaGraphInstantiateFlagUseNodePriority);
+    cudaGraphDestroy(g);
+    CU(c, ei);
+    c->graph_instantiations += 1;
+  } else {
+    cudaGraphDestroy(g);
+  }
+  return SPS_OK;
+}
+
 static sps_status replay_mstep(sps_ctx* c, uint32_t step) {
   const int par = (int)(step & 1u);
   CU(c, cudaGraphLaunch(c->gexec[par], c->stream));
@@ -1689,10 +1775,51 @@ sps_status sps_mphase(sps_ctx* c, int32_t R_fixed, int32_t* R_out, double* min_r
   const uint32_t step0 = c->mstep;
   c->phase_step0 = step0;
   static const bool no_graph = getenv("SPS_NO_GRAPH") != nullptr;
+  static const bool no_loop = getenv("SPS_NO_LOOP") != nullptr;
   const bool graph = c->G == 1 && !c->profiling && !no_graph;
+  const bool loop = graph && !no_loop;
   // the first step's normals after all earlier work of the main stream (graph replays record no Zbuf events)
   CU(c, cudaEventRecord(c->ev_zfree[step0 & 1u], c->stream));
   TRY(launch_normals(c, TAG_PROPOSAL, step0, (int)(step0 & 1u)));
+  if (loop) {  // the whole adaptive M phase on the device: one graph launch, one host sync
+    const auto g0 = std::chrono::steady_clock::now();
+    TRY(build_mstep_loop(c, adaptive, Rmax));
+    c->host_graph_us +=
+        std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - g0).count();
+    CU(c, cudaStreamWaitEvent(c->stream, c->ev_zready[step0 & 1u], 0));
+    const auto h0 = std::chrono::steady_clock::now();
+    CU(c, cudaGraphLaunch(c->gloop, c->stream));
+    CU(c, cudaEventRecord(c->evs[0], c->stream));
+    const auto h1 = std::chrono::steady_clock::now();
+    CU(c, cudaEventSynchronize(c->evs[0]));
+    const auto h2 = std::chrono::steady_clock::now();
+    c->host_launch_us += std::chrono::duration<double, std::micro>(h1 - h0).count();
+    c->host_wait_us += std::chrono::duration<double, std::micro>(h2 - h1).count();
+    c->syncs += 1;
+    const Ctl got = c->hslot[0];
+    const int r = got.steps_done;
+    c->launches += c->gl_launches / 2 * r;  // (the body holds two steps)
+    c->k1_launches += c->gl_k1 / 2 * r;
+    c->k1_pairs += c->gl_pairs / 2 * r;
+    c->pairs += (double)c->P * t1 * r;
+    if (got.err == ERR_NUMERIC)
+      return fail(c, SPS_E_NUMERIC, "numerical failure in the M phase (non-finite loglik or Cholesky failure "
+                                    "after ridge; cf. PAPER.md:1024-1030)");
+    if (adaptive && got.stop != 1)
+      return fail(c, SPS_E_MIXING, "M phase did not reach RNE >= K in %d steps", c->cfg.max_m_steps);
+    c->mstep = step0 + (uint32_t)r;
+    if (c->tl) TRY(timeline_accumulate(c, r));
+    *c->hctl = got;
+    c->cphase_done = false;
+    c->tr_R.push_back(r);
+    c->tr_rne.push_back(got.minrne);
+    c->tr_h.push_back(got.h);
+    if (final_cycle(c)) c->finished = true;
+    if (R_out) *R_out = r;
+    if (min_rne) *min_rne = got.minrne;
+    if (h_out) *h_out = got.h;
+    return SPS_OK;
+  }
   if (graph) {
     const auto g0 = std::chrono::steady_clock::now();
     TRY(build_mstep_graphs(c, adaptive));
