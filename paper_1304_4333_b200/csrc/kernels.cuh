@@ -165,7 +165,7 @@ struct FinArgs {
   int J, Jl, N, d;
   double* shift;       // in: c used by the moments; out: new c = theta-bar
   double* Lprop;       // out: chol((h/100) V)
-  double* V;           // out: pooled covariance (d x d)
+  double* V;           // out: pooled covariance (d x d), or null
   const double* mon;   // monitors (nmon x d)
   int nmon;
   int mode;            // 0: moments of resampled particles (no h / RNE); 1: after an M step

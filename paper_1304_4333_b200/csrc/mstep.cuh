@@ -1072,15 +1072,19 @@ __device__ void finalize_body(const FinArgs& f, double* sm) {
     const int stop = (f.K > 0.0 && minrne >= f.K) ? 1 : ((f.loop && done >= f.rmax) ? 2 : 0);
     f.ctl->stop = stop;
     f.ctl->steps_done = done;
-    // device-side M phase (a WHILE graph node, two steps per body): continue unless stopped
-    if (f.loop) cudaGraphSetConditional(f.cond, stop == 0 ? 1u : 0u);
+    // device-side M phase (a WHILE graph node, two steps per body): the condition is 1 from the
+    // launch on and is cleared once, on the stopping step (a device-side set costs ~2 us)
+    if (f.loop && stop != 0) cudaGraphSetConditional(f.cond, 0u);
   }
+  if (f.V)
 #pragma unroll 1
-  for (int idx = threadIdx.x; idx < dd; idx += blockDim.x) f.V[idx] = sV[idx];
+    for (int idx = threadIdx.x; idx < dd; idx += blockDim.x) f.V[idx] = sV[idx];
   for (int i = threadIdx.x; i < d; i += blockDim.x) f.shift[i] = sbar[i];
   __syncthreads();
   if (f.trace && threadIdx.x == 0) f.trace[5] = gtimer();
-  if (f.host_out && threadIdx.x == 0) *f.host_out = *f.ctl;  // into mapped pinned host memory (visible at kernel end)
+  // into mapped pinned host memory (visible at kernel end); in the device-side loop the host reads
+  // it after the phase: written on the stopping step only
+  if (f.host_out && threadIdx.x == 0 && (!f.loop || f.ctl->stop != 0)) *f.host_out = *f.ctl;
   if (f.trace && threadIdx.x == 0) f.trace[6] = gtimer();
 }
 

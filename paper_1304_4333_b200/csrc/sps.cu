@@ -738,7 +738,7 @@ sps_status make_fin(sps_ctx* c, int mode, bool allow_stop, const int* stop, int 
   f.d = c->d;
   f.shift = c->shift;
   f.Lprop = c->Lprop;
-  f.V = c->V;
+  f.V = nullptr;  // (the pooled V is not read back on the hot path)
   f.mon = c->mon;
   f.nmon = c->nmon;
   f.mode = mode;
