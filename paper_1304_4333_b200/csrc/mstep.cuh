@@ -180,8 +180,8 @@ __global__ void __launch_bounds__(256) k_propose(DrawArgs a) {
 // the TMA loads of the block's next tile (Z rows, base rows) are in flight
 // while the current tile computes; theta* is assembled in shared memory over
 // the base rows and leaves as one TMA bulk store (contiguous rows).
-template <int KK>
-__global__ void __launch_bounds__(256, 3) k_propose_rb(DrawArgs a) {
+template <int KK, int TILE>  // TILE particles per tile = TILE / 8 warps of 8 rows (blockDim = 4 TILE)
+__global__ void __launch_bounds__(4 * TILE, TILE == 32 ? 5 : 3) k_propose_rb(DrawArgs a) {
   constexpr int KP = 4 * KK, NT = (KP + 7) / 8, NP = 8 * NT;
   extern __shared__ __align__(16) double sm[];
   if (a.stop && *a.stop) return;
@@ -190,15 +190,15 @@ __global__ void __launch_bounds__(256, 3) k_propose_rb(DrawArgs a) {
   griddep_launch();  // persistent grid (all CTAs resident): K1's CTAs may start their prologue
   const double* Zsrc = a.Z;
   if (a.Zalt && ((a.step0 + (uint32_t)a.ctl->steps_done) & 1u)) Zsrc = a.Zalt;
-  const int d = a.d, BS = round_up(PR_TILE * d, 2);
+  const int d = a.d, BS = round_up(TILE * d, 2);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, ar = lane >> 2, ac = lane & 3;
-  double* Zs0 = sm;                     // 2 x PR_TILE x KP: Z rows, then (theta* - mu) rows (per warp, in place)
-  double* Bs0 = Zs0 + 2 * PR_TILE * KP;  // 2 x BS: base rows, overwritten with theta*
+  double* Zs0 = sm;                     // 2 x TILE x KP: Z rows, then (theta* - mu) rows (per warp, in place)
+  double* Bs0 = Zs0 + 2 * TILE * KP;  // 2 x BS: base rows, overwritten with theta*
   double* smu = Bs0 + 2 * BS;           // KP
   double* sL = smu + KP;                // NP x KP
   double* sS = sL + NP * KP;            // NP x KP (Rp)
   __shared__ __align__(8) uint64_t bar[2];
-  const int64_t ntl = (a.P + PR_TILE - 1) / PR_TILE;
+  const int64_t ntl = (a.P + TILE - 1) / TILE;
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -207,13 +207,13 @@ __global__ void __launch_bounds__(256, 3) k_propose_rb(DrawArgs a) {
   __syncthreads();
   // thread 0: TMA loads of `tile` into buffer `buf` (+ Lz, Sinv with the first)
   auto issue = [&](int64_t tile, int buf, bool first) {
-    const int64_t pb = tile * PR_TILE;
-    const int cnt = (int)min((int64_t)PR_TILE, a.P - pb);
-    const unsigned zb = (unsigned)(PR_TILE * KP * 8);
+    const int64_t pb = tile * TILE;
+    const int cnt = (int)min((int64_t)TILE, a.P - pb);
+    const unsigned zb = (unsigned)(TILE * KP * 8);
     const unsigned bb = a.base ? (unsigned)(round_up(cnt * d, 2) * 8) : 0u;
     const unsigned mb = first ? (unsigned)(NP * KP * 8) : 0u;
     mbar_arrive_expect_tx(&bar[buf], zb + bb + 2 * mb);
-    bulk_g2s(Zs0 + buf * PR_TILE * KP, Zsrc + pb * KP, zb, &bar[buf]);
+    bulk_g2s(Zs0 + buf * TILE * KP, Zsrc + pb * KP, zb, &bar[buf]);
     if (a.base) bulk_g2s(Bs0 + buf * BS, a.base + pb * d, bb, &bar[buf]);
     if (mb) {
       bulk_g2s(sL, a.Lz, mb, &bar[buf]);
@@ -224,14 +224,14 @@ __global__ void __launch_bounds__(256, 3) k_propose_rb(DrawArgs a) {
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < ntl; tile += gridDim.x, ++it) {
     const int buf = it & 1;
-    const int64_t pb = tile * PR_TILE;
-    const int cnt = (int)min((int64_t)PR_TILE, a.P - pb);
+    const int64_t pb = tile * TILE;
+    const int cnt = (int)min((int64_t)TILE, a.P - pb);
     if (threadIdx.x == 0 && tile + gridDim.x < ntl) {
       bulk_wait_read();  // the bulk store of iteration it-1 has read buffer buf^1
       issue(tile + gridDim.x, buf ^ 1, false);
     }
     mbar_wait(&bar[buf], (unsigned)(it >> 1) & 1u);
-    double* Zs = Zs0 + buf * PR_TILE * KP;
+    double* Zs = Zs0 + buf * TILE * KP;
     double* Ds = Zs;  // a warp's Z rows are dead once its first product is done
     double* Bs = Bs0 + buf * BS;
     const int p = w * 8 + ar;  // this lane's particle row (A / C fragments)

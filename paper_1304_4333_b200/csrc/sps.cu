@@ -607,21 +607,28 @@ sps_status launch_draw(sps_ctx* c, int slot, const double* base, const double* L
   if (!graph) CU(c, cudaStreamWaitEvent(c->stream, c->ev_zready[slot], 0));
   const int64_t ntl = (c->Pl + PR_TILE - 1) / PR_TILE;
   PROF_BEGIN(c);
-  if (d <= 32) {  // register-blocked DMMA proposal
+  if (d <= 32) {  // register-blocked DMMA proposal, persistent, double-buffered
+    // 32-particle tiles (4 warps, ~42 KB smem -> 5 blocks / SM): a finer tile grain than 64 (3 / SM,
+    // ceil(1024 / 444) = 3 rounds of 64 at P = 65536) for the persistent loop's last round
+    static const int tile = getenv("SPS_PROPOSE_TILE") ? atoi(getenv("SPS_PROPOSE_TILE")) : 32;
+    const int T = tile == 64 ? 64 : 32;
     const int KK = (d + 3) / 4, KPr = 4 * KK, NPr = 8 * ((KPr + 7) / 8);
-    const size_t sm =
-        (size_t)(2 * PR_TILE * KPr + 2 * round_up(PR_TILE * d, 2) + KPr + 2 * NPr * KPr) * sizeof(double);
-    const unsigned grid = (unsigned)std::min<int64_t>(ntl, 3 * (int64_t)num_sms());  // persistent, 3 per SM
+    const size_t sm = (size_t)(2 * T * KPr + 2 * round_up(T * d, 2) + KPr + 2 * NPr * KPr) * sizeof(double);
+    const int64_t ntlT = (c->Pl + T - 1) / T;
+    const unsigned grid = (unsigned)std::min<int64_t>(ntlT, (T == 32 ? 5 : 3) * (int64_t)num_sms());
+    const unsigned thr = (unsigned)(4 * T);
+#define PRB(KK_)                                                                      \
+  case KK_:                                                                           \
+    if (T == 32)                                                                      \
+      k_propose_rb<KK_, 32><<<grid, thr, sm, c->stream>>>(a);                         \
+    else                                                                              \
+      k_propose_rb<KK_, 64><<<grid, thr, sm, c->stream>>>(a);                         \
+    break;
     switch (KK) {
-      case 1: k_propose_rb<1><<<grid, 256, sm, c->stream>>>(a); break;
-      case 2: k_propose_rb<2><<<grid, 256, sm, c->stream>>>(a); break;
-      case 3: k_propose_rb<3><<<grid, 256, sm, c->stream>>>(a); break;
-      case 4: k_propose_rb<4><<<grid, 256, sm, c->stream>>>(a); break;
-      case 5: k_propose_rb<5><<<grid, 256, sm, c->stream>>>(a); break;
-      case 6: k_propose_rb<6><<<grid, 256, sm, c->stream>>>(a); break;
-      case 7: k_propose_rb<7><<<grid, 256, sm, c->stream>>>(a); break;
-      default: k_propose_rb<8><<<grid, 256, sm, c->stream>>>(a); break;
+      PRB(1) PRB(2) PRB(3) PRB(4) PRB(5) PRB(6) PRB(7)
+      default: PRB(8)
     }
+#undef PRB
   } else {
     const unsigned grid = (unsigned)ntl;
     if (stage)
@@ -1170,20 +1177,6 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
                             cudaMemcpyDeviceToDevice, c->stream));
     // one-time kernel attributes (dynamic shared memory above 48 KB)
     const int big = 200 * 1024;
-    // every kernel of the M step runs with the same (max shared) carveout, so consecutive
-    // launches never reconfigure the SM's L1/shared split
-    if (getenv("SPS_MAX_CARVEOUT")) {
-      const void* fns[] = {(const void*)c->llc.fn, (const void*)k_propose_rb<1>, (const void*)k_propose_rb<2>,
-                           (const void*)k_propose_rb<3>, (const void*)k_propose_rb<4>, (const void*)k_propose_rb<5>,
-                           (const void*)k_propose_rb<6>, (const void*)k_propose_rb<7>, (const void*)k_propose_rb<8>,
-                           (const void*)k_propose<true>, (const void*)k_propose<false>, (const void*)k_accept_mom,
-                           (const void*)k_accept_mom_rb<1>, (const void*)k_accept_mom_rb<2>,
-                           (const void*)k_accept_mom_rb<3>, (const void*)k_accept_mom_rb<4>, (const void*)k_mom_reduce,
-                           (const void*)k_finalize,
-                           (const void*)k_normals};
-      for (const void* fn : fns)
-        CU(c, cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
-    }
     CU(c, cudaFuncSetAttribute(k_propose<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(c, cudaFuncSetAttribute(k_propose<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     // the side-stream normals use no shared memory; with the default (L1-leaning) carveout the SMs
@@ -1203,14 +1196,11 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
     CU(c, cudaFuncSetAttribute(k_accept_mom_rb<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(c, cudaFuncSetAttribute(k_accept_mom_rb<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(c, cudaFuncSetAttribute(k_accept_mom_rb<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    CU(c, cudaFuncSetAttribute(k_propose_rb<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    CU(c, cudaFuncSetAttribute(k_propose_rb<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    CU(c, cudaFuncSetAttribute(k_propose_rb<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    CU(c, cudaFuncSetAttribute(k_propose_rb<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    CU(c, cudaFuncSetAttribute(k_propose_rb<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    CU(c, cudaFuncSetAttribute(k_propose_rb<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    CU(c, cudaFuncSetAttribute(k_propose_rb<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    CU(c, cudaFuncSetAttribute(k_propose_rb<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+#define PRB_ATTR(KK_)                                                                                    \
+  CU(c, cudaFuncSetAttribute(k_propose_rb<KK_, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, big)); \
+  CU(c, cudaFuncSetAttribute(k_propose_rb<KK_, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    PRB_ATTR(1) PRB_ATTR(2) PRB_ATTR(3) PRB_ATTR(4) PRB_ATTR(5) PRB_ATTR(6) PRB_ATTR(7) PRB_ATTR(8)
+#undef PRB_ATTR
     CU(c, cudaFuncSetAttribute(k_functional_stats, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(c, cudaFuncSetAttribute(k_resample, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(c, cudaFuncSetAttribute(k_cphase_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
