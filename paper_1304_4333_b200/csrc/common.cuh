@@ -157,7 +157,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // Debug timeline (SPS_TIMELINE): per M step (row = *g_tl_steps, the step
 // index within the phase) and kernel slot k, [2k] = start of block (0,0),
 // [2k+1] = latest block end (atomicMax).  Null when disabled.
-constexpr int TL_W = 16, TL_ROWS = 4096;
+constexpr int TL_W = 24, TL_ROWS = 4096;
 __device__ unsigned long long* g_tl = nullptr;
 __device__ const int* g_tl_steps = nullptr;
 __device__ __forceinline__ void tl_start(int k) {
@@ -167,7 +167,14 @@ __device__ __forceinline__ void tl_start(int k) {
     if (r >= 0 && r < TL_ROWS) tl[r * TL_W + 2 * k] = gtimer();
   }
 }
-__device__ __forceinline__ void tl_mark(int slot) {  // block (0,0) thread 0: a phase clock in slot 12..15
+__device__ __forceinline__ void tl_mark_any(int slot) {  // calling thread: a phase clock in slot 12..23
+  unsigned long long* tl = g_tl;
+  if (tl) {
+    const int r = *g_tl_steps;
+    if (r >= 0 && r < TL_ROWS) tl[r * TL_W + slot] = gtimer();
+  }
+}
+__device__ __forceinline__ void tl_mark(int slot) {  // block (0,0) thread 0: a phase clock in slot 12..23
   unsigned long long* tl = g_tl;
   if (tl && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
     const int r = *g_tl_steps;

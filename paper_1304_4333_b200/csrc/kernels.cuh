@@ -178,6 +178,7 @@ struct FinArgs {
   Ctl* host_out;       // mapped pinned host slot for the control block (may be null)
   unsigned* ticket;    // k_mom_reduce: arrival counter; the last block runs the finalize (null: separate launch)
   unsigned long long* trace;  // debug (SPS_TRACE): %globaltimer at phase boundaries, or null
+  int preloaded;                // cluster reduce: group sums, second moment, accepts, error already in shared memory
   int loop;                     // inside a device-side WHILE node: set its condition after the step
   int rmax;                     // step cap of the M phase (adaptive: max_m_steps; fixed: R)
   cudaGraphConditionalHandle cond;

@@ -4,6 +4,8 @@
 // a fixed tree/order (deterministic), and kernels of a speculatively launched
 // step return immediately once the device stop flag is set.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "loglik.cuh"
@@ -885,7 +887,7 @@ __device__ void stage3(double* d0, const double* s0, int n0, double* d1, const d
 __host__ __device__ inline int64_t fin_smem_doubles(int d, int J, int nmon, bool stage_S) {
   const int D = (d + 3) / 4 * 4;
   return (int64_t)2 * d * d + (d > 32 ? 0 : (int64_t)D * D) + 2 * d + (int64_t)nmon * d + (int64_t)nmon * J + nmon +
-         (stage_S ? (int64_t)J * d : 0);
+         4 + (stage_S ? (int64_t)J * d : 0);
 }
 
 // ---------------------------------------------------------------- K7
@@ -910,11 +912,15 @@ __device__ void finalize_body(const FinArgs& f, double* sm) {
   double* sshift = sbar + d;                      // d
   double* smon = sshift + d;                      // nmon x d
   double* sg = smon + f.nmon * d;                 // nmon x J group means, then nmon RNEs
+  double* sxtra = sg + f.nmon * J + f.nmon;       // [accepts, error, h] (preloaded by the cluster reduce)
   __shared__ int s_h, s_flag;
   __shared__ double s_part[8][32];
   if (f.trace && threadIdx.x == 0) f.trace[0] = gtimer();
   // ---- stage: one round of independent L2 loads
-  if (f.G == 1) {
+  if (f.preloaded) {
+    // S, M, accepts, error (other CTAs, DSMEM) and shift, monitors, h (this CTA, prefetched at its
+    // start) are already in shared memory
+  } else if (f.G == 1) {
     if (f.stage_S)
       stage3(sS, f.gath, gs_len + dd, sshift, f.shift, d, smon, f.mon, f.nmon * d);
     else
@@ -933,13 +939,18 @@ __device__ void finalize_body(const FinArgs& f, double* sm) {
     }
   }
   if (threadIdx.x == 0) {  // h update from the pooled acceptance (R6)
-    int h = f.ctl->h;
+    int h = f.preloaded ? (int)sxtra[2] : f.ctl->h;
     if (f.mode == 1) {
       double acc = 0.0, err = 0.0;
+      if (f.preloaded) {
+        acc = sxtra[0];
+        err = sxtra[1];
+      } else {
 #pragma unroll 1
-      for (int r = 0; r < f.G; ++r) {
-        acc += __ldcg(f.gath + (int64_t)r * f.slice_len + gs_len + dd);
-        err = fmax(err, __ldcg(f.gath + (int64_t)r * f.slice_len + gs_len + dd + 1));
+        for (int r = 0; r < f.G; ++r) {
+          acc += __ldcg(f.gath + (int64_t)r * f.slice_len + gs_len + dd);
+          err = fmax(err, __ldcg(f.gath + (int64_t)r * f.slice_len + gs_len + dd + 1));
+        }
       }
       h = (acc > f.accept_target * P) ? min(h + f.h_step, f.h_max) : max(h - f.h_step, f.h_min);
       if (err > 0.0) f.ctl->err = (int)err;
@@ -950,6 +961,7 @@ __device__ void finalize_body(const FinArgs& f, double* sm) {
   }
   __syncthreads();
   if (f.trace && threadIdx.x == 0) f.trace[1] = gtimer();
+  if (f.mode == 1 && threadIdx.x == 0) tl_mark_any(16);
   auto S = [&](int j, int i) -> double { return f.stage_S ? sS[j * d + i] : group_sum_global(f, j, i); };
   // ---- theta-bar: lane = coordinate, warp = group subset, fixed-order combine
 #pragma unroll 1
@@ -976,6 +988,7 @@ __device__ void finalize_body(const FinArgs& f, double* sm) {
     __syncthreads();
   }
   if (f.trace && threadIdx.x == 0) f.trace[2] = gtimer();
+  if (f.mode == 1 && threadIdx.x == 0) tl_mark_any(17);
   // ---- V (R11) and the factorization input (h/100) V, identity-padded to D x D
   const double hd = (double)s_h / 100.0;
   const int DA = d > 32 ? d : D;
@@ -996,6 +1009,7 @@ __device__ void finalize_body(const FinArgs& f, double* sm) {
   }
   __syncthreads();
   if (f.trace && threadIdx.x == 0) f.trace[3] = gtimer();
+  if (f.mode == 1 && threadIdx.x == 0) tl_mark_any(18);
   const int ldp = round_up(d, 4);  // padded (DMMA) layout of the factor
   if (w == 0 && d <= 32) {         // chol((h/100) V), one ridge retry (R13)
     bool ok = warp_cholesky_d(sA, f.Lprop, ldp, d);
@@ -1055,6 +1069,7 @@ __device__ void finalize_body(const FinArgs& f, double* sm) {
   }
   __syncthreads();
   if (f.trace && threadIdx.x == 0) f.trace[4] = gtimer();
+  if (f.mode == 1 && threadIdx.x == 0) tl_mark_any(19);
   if (d > 32) {  // block Cholesky (larger d)
     block_factor(f, sA, sV, hd, ldp, &s_flag);
   }
@@ -1082,6 +1097,7 @@ __device__ void finalize_body(const FinArgs& f, double* sm) {
   for (int i = threadIdx.x; i < d; i += blockDim.x) f.shift[i] = sbar[i];
   __syncthreads();
   if (f.trace && threadIdx.x == 0) f.trace[5] = gtimer();
+  if (f.mode == 1 && threadIdx.x == 0) tl_mark_any(20);
   // into mapped pinned host memory (visible at kernel end); in the device-side loop the host reads
   // it after the phase: written on the stopping step only
   if (f.host_out && threadIdx.x == 0 && (!f.loop || f.ctl->stop != 0)) *f.host_out = *f.ctl;
@@ -1189,6 +1205,97 @@ __global__ void __launch_bounds__(256) k_mom_reduce(RedArgs r, Ctl* ctl, double*
   int tlr = -1;
   if (tl && threadIdx.x == 0 && f.mode == 1) {
     tlr = *g_tl_steps;  // before finalize_body increments steps_done
+    if (tlr >= 0 && tlr < TL_ROWS) tl[tlr * TL_W + 10] = gtimer();
+  }
+  finalize_body(f, fin_sm);
+  if (tlr >= 0 && tlr < TL_ROWS) tl[tlr * TL_W + 11] = gtimer();
+}
+
+// Reduce + finalize as ONE thread-block cluster (one rank): CTA r reduces moment groups r, r + ncta,
+// ... (32 lower-triangle entries, 8 warps over the block partial rows) and a share of the group sums,
+// writing the results straight into CTA 0's finalize shared memory (DSMEM); after one cluster
+// barrier CTA 0 runs finalize_body on them -- no global stats slice, no ticket, no staging round.
+__global__ void __launch_bounds__(256) k_mom_reduce_cl(RedArgs r, Ctl* ctl, const int* __restrict__ stop, FinArgs f) {
+  namespace cg = cooperative_groups;
+  extern __shared__ double fin_sm[];
+  __shared__ double part[8][33];
+  __shared__ double red[32];
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank(), ncta = (int)cl.num_blocks();
+  if (stop && *stop) return;  // uniform over the cluster
+  if (f.mode == 1 && rank == 0) tl_start(4);
+  griddep_wait();  // the accept kernel's block partials
+  const int d = r.d, Jl = r.Jl, W = r.W, nblk = r.nblk, nl = d * (d + 1) / 2, nm = (nl + 31) / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double* sS0 = cl.map_shared_rank(fin_sm, 0);  // CTA 0's finalize layout: [S (J x d) | M (d x d) | ...]
+  double* sM0 = sS0 + (int64_t)f.J * d;
+  double* sx0 = sM0 + fin_smem_doubles(d, f.J, f.nmon, true) - (int64_t)f.J * d - 4;  // [accepts, error, h]
+  if (rank == 0) {  // prefetch the finalize inputs that do not depend on this step's partials
+    const int D = round_up(d, 4);
+    double* sshift = sM0 + 2 * d * d + (d > 32 ? 0 : D * D) + d;  // (layout of finalize_body)
+    double* smon = sshift + d;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) sshift[i] = f.shift[i];
+    for (int i = threadIdx.x; i < f.nmon * d; i += blockDim.x) smon[i] = f.mon[i];
+    if (threadIdx.x == 0) fin_sm[sx0 - sS0 + 2] = (double)f.ctl->h;
+  }
+  for (int g = rank; g < nm; g += ncta) {
+    const int e = g * 32 + lane;
+    int i = 0, l = 0;
+    if (e < nl) {
+      i = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+      while (i * (i + 1) / 2 > e) --i;
+      while ((i + 1) * (i + 2) / 2 <= e) ++i;
+      l = e - i * (i + 1) / 2;
+    }
+    const int col = red_col(r, i, l);
+    double acc8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (e < nl) {
+#pragma unroll 1
+      for (int b0 = w; b0 < nblk; b0 += 256) {
+        double v[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+          const int b = b0 + 8 * u;
+          v[u] = b < nblk ? r.bpart[(int64_t)b * W + col] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 32; ++u) acc8[u & 7] += v[u];
+      }
+    }
+    part[w][lane] = ((acc8[0] + acc8[1]) + (acc8[2] + acc8[3])) + ((acc8[4] + acc8[5]) + (acc8[6] + acc8[7]));
+    __syncthreads();
+    if (w == 0 && e < nl) {
+      double t = part[0][lane];
+      for (int q = 1; q < 8; ++q) t += part[q][lane];
+      sM0[i * d + l] = t;
+      sM0[l * d + i] = t;
+    }
+    __syncthreads();
+  }
+  for (int idx = rank * 256 + threadIdx.x; idx < Jl * d; idx += ncta * 256) {  // group sums
+    const int j = idx / d, c = idx % d;
+    const int col = r.tnt ? red_col(r, d, c) : c;
+    double s = 0.0;
+    for (int b = 0; b < r.bpg; ++b) s += r.bpart[(int64_t)(j * r.bpg + b) * W + col];
+    if (r.tnt) s += (double)r.N * r.shift[c];
+    sS0[idx] = s;
+  }
+  if (rank == ncta - 1) {  // accepts
+    double s = 0.0;
+    for (int b = threadIdx.x; b < nblk; b += 256) s += r.bpart[(int64_t)b * W + W - 1];
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) {
+      sx0[0] = s;
+      sx0[1] = (double)ctl->err;
+    }
+  }
+  cl.sync();  // every DSMEM write into CTA 0 is visible
+  if (f.mode == 1 && rank == 0) tl_end(4);
+  if (rank != 0) return;
+  unsigned long long* tl = g_tl;
+  int tlr = -1;
+  if (tl && threadIdx.x == 0 && f.mode == 1) {
+    tlr = *g_tl_steps;
     if (tlr >= 0 && tlr < TL_ROWS) tl[tlr * TL_W + 10] = gtimer();
   }
   finalize_body(f, fin_sm);

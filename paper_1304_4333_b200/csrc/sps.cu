@@ -141,13 +141,14 @@ struct sps_ctx {
   double* bpart = nullptr;       // accept+moments block partials
   int tp = 0, QE = 1, W = 0, nblk = 0;
   int acc_tnt = 0, Wt = 0;  // tile-layout accept kernel: tiles per side (0: full-layout kernels), partial row width
+  int red_cluster = 0;      // cluster size of the DSMEM reduce + finalize (0: ticket path)
   size_t acc_smem = 0;
   Ctl* hslot = nullptr;          // 2 mapped pinned Ctl slots (pipelined M steps), written by finalize_body
   Ctl* dslot = nullptr;          // device view of hslot
   unsigned* ticket = nullptr;      // arrival counter of the fused reduce + finalize (k_mom_reduce)
   unsigned long long* trace = nullptr;  // debug (SPS_TRACE): finalize / reduce phase clocks (managed)
   unsigned long long* tl = nullptr;     // debug (SPS_TIMELINE): per-step kernel start / end clocks
-  double tl_acc[20] = {};
+  double tl_acc[24] = {};
   int tl_rows = 0;
   double trace_acc[80] = {};
   int trace_n = 0;
@@ -272,6 +273,28 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   at[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at;
   lc.numAttrs = off ? 0 : 1;
+  return cudaLaunchKernelEx(&lc, kern, args...);
+}
+
+// Cluster launch (cluster of `cl` CTAs along x) with programmatic stream serialization.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_cluster_pdl(void (*kern)(KArgs...), int cl, dim3 block, size_t smem, cudaStream_t st,
+                               Args... args) {
+  static const bool off = getenv("SPS_NO_PDL") != nullptr;
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)cl);
+  lc.blockDim = block;
+  lc.dynamicSmemBytes = smem;
+  lc.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)cl;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = off ? 1 : 2;
   return cudaLaunchKernelEx(&lc, kern, args...);
 }
 
@@ -716,6 +739,16 @@ sps_status accept_moments(sps_ctx* c, bool decide, int nchunks, double temper, u
   const int nm = (d * (d + 1) / 2 + 31) / 32, ng = (c->Jl * d + 255) / 256;
   RedArgs r{c->bpart, c->nblk, c->N / c->tp, c->Jl, d, c->acc_tnt > 0 ? c->Wt : c->W, c->acc_tnt, c->N, c->shift};
   FinArgs none{};
+  if (fin && fin->stage_S && c->red_cluster > 0) {  // one rank: reduce + finalize as one cluster (DSMEM)
+    FinArgs f = *fin;
+    f.preloaded = 1;
+    f.ticket = nullptr;
+    PROF_BEGIN(c);
+    CU(c, launch_cluster_pdl(k_mom_reduce_cl, c->red_cluster, dim3(256), fin_smem, c->stream, r, c->ctl, stop, f));
+    CHECK_LAUNCH(c);
+    PROF_END(c, CAT_FINALIZE);
+    return SPS_OK;
+  }
   PROF_BEGIN(c);
   CU(c, launch_pdl(k_mom_reduce, dim3(nm + ng + 1), dim3(256), fin ? fin_smem : 0, c->stream, r, c->ctl, c->slice, stop,
                     fin ? *fin : none));
@@ -1186,6 +1219,31 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
                                cudaSharedmemCarveoutMaxShared));
     CU(c, cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(c, cudaFuncSetAttribute(k_mom_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_mom_reduce_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(c, cudaFuncSetAttribute(k_mom_reduce_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    {  // largest of 16 / 8 CTAs per cluster the device can co-schedule with the finalize smem
+      static const bool no_cl = getenv("SPS_NO_CLUSTER_REDUCE") != nullptr;
+      const size_t fsm = (size_t)fin_smem_doubles(d, c->J, c->nmon, true) * sizeof(double);
+      for (int cl : {16, 8}) {
+        if (no_cl || c->G != 1 || fsm > 200 * 1024) break;
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3((unsigned)cl);
+        lc.blockDim = dim3(256);
+        lc.dynamicSmemBytes = fsm;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)cl;
+        at[0].val.clusterDim.y = at[0].val.clusterDim.z = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        int nclusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&nclusters, (void*)k_mom_reduce_cl, &lc) == cudaSuccess && nclusters > 0) {
+          c->red_cluster = cl;
+          break;
+        }
+        cudaGetLastError();
+      }
+    }
     CU(c, cudaFuncSetAttribute(k_accept_mom, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(c, cudaFuncSetAttribute(k_accept_tile<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(c, cudaFuncSetAttribute(k_accept_tile<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
@@ -1299,9 +1357,10 @@ sps_status sps_get_counters(const sps_ctx* cc, sps_counters* out) {
     static const char* nm[] = {"propose", "normals", "K1", "accept", "reduce", "finalize", "gap K1<-propose",
                                "gap accept<-K1", "gap reduce<-accept", "gap fin<-reduce", "normals start-propose end",
                                "normals end-K1 end", "gap next propose<-fin", "step", "acc0 load", "acc0 decide",
-                               "acc0 wb+dmma", "acc0 combine..end(all)"};
+                               "acc0 wb+dmma", "acc0 combine..end(all)", "fin stage", "fin theta-bar", "fin V",
+                               "fin chol|RNE", "fin stats", "fin tail"};
     fprintf(stderr, "SPS_TIMELINE mean us over %d steps:", c->tl_rows);
-    for (int q = 0; q < 18; ++q) fprintf(stderr, " %s=%.2f", nm[q], c->tl_acc[q] / c->tl_rows / 1e3);
+    for (int q = 0; q < 24; ++q) fprintf(stderr, " %s=%.2f", nm[q], c->tl_acc[q] / c->tl_rows / 1e3);
     fprintf(stderr, "\n");
   }
   out->launches = c->launches;
@@ -1564,6 +1623,14 @@ static sps_status timeline_accumulate(sps_ctx* c, int R) {
     c->tl_acc[11] += (double)t[3] - (double)t[5];   // normals end - K1 end
     if (r + 1 < rows && h[(size_t)(r + 1) * TL_W]) c->tl_acc[12] += (double)h[(size_t)(r + 1) * TL_W] - (double)t[11];
     c->tl_acc[13] += (double)t[11] - (double)t[0];  // step: propose start -> finalize end
+    if (t[16] && t[17] && t[18] && t[19] && t[20]) {  // finalize phases: stage / theta-bar / V / chol|RNE / tail
+      c->tl_acc[18] += (double)t[16] - (double)t[10];
+      c->tl_acc[19] += (double)t[17] - (double)t[16];
+      c->tl_acc[20] += (double)t[18] - (double)t[17];
+      c->tl_acc[21] += (double)t[19] - (double)t[18];
+      c->tl_acc[22] += (double)t[20] - (double)t[19];
+      c->tl_acc[23] += (double)t[11] - (double)t[20];
+    }
     if (t[12] && t[13] && t[14]) {  // accept block 0: load / decide+writeback / dmma phases
       c->tl_acc[14] += (double)t[12] - (double)t[6];
       c->tl_acc[15] += (double)t[13] - (double)t[12];
