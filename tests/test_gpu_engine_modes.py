@@ -1,0 +1,72 @@
+"""The M-step scheduling modes of the engine give bit-identical results.
+
+The default path runs each adaptive M phase as one CUDA graph with a device-side
+WHILE node (two M steps per body), reduces the moments and finalizes in one
+16-CTA cluster over DSMEM, and launches K1 / accept / reduce with programmatic
+dependent launch.  The alternatives -- per-step graph replays (SPS_NO_LOOP),
+plain stream launches (SPS_NO_GRAPH), the ticket-based reduce + finalize
+(SPS_NO_CLUSTER_REDUCE), no PDL (SPS_NO_PDL) -- enqueue the same kernels with the
+same arithmetic, so every result must agree to the bit.  The switches are read
+once per process, hence one subprocess per mode.
+"""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, {root!r})
+import paper_1304_4333_b200 as sps, sps_synth
+out = {{}}
+# full adaptive run, cfg1 (data tempering) and a German-credit-shaped subset
+for name, kw in (("cfg1", dict(J=4, N=128)), ("cfg2s", dict(J=8, N=256))):
+    X, y = sps_synth.config_data("cfg1" if name == "cfg1" else "cfg2")
+    if name == "cfg2s":
+        X, y = X[:300], y[:300]
+    k = X.shape[1]
+    ctx = sps.Sps(X, y, np.zeros(k), sps.g_prior(X, 2, 0.25), seed=7, **kw)
+    rep = ctx.run()
+    th, L, lp = ctx.particles()
+    out[name] = dict(logml=rep["logml"], nse=rep["logml_nse"], R=[int(r) for r in rep["R_cycle"]],
+                     t=[int(t) for t in rep["t_cycle"]], h=[int(h) for h in rep["h_cycle"]],
+                     mean=list(rep["mean"]), theta=th.tobytes().hex(), L=L.tobytes().hex(), lp=lp.tobytes().hex())
+    ctx.close()
+# fixed schedule replay (Algorithm 3 style): C phase to t = 20, then exactly R = 3 M steps (odd: the
+# device loop's second half-step must stop at the cap), then R = 2
+X, y = sps_synth.config_data("cfg1")
+ctx = sps.Sps(X, y, np.zeros(4), sps.g_prior(X, 2, 0.25), J=4, N=128, seed=3)
+ctx.cphase(t_target=20)
+R1, rne1, h1 = ctx.mphase(R_fixed=3)
+ctx.cphase(t_target=35)
+R2, rne2, h2 = ctx.mphase(R_fixed=2)
+th, L, lp = ctx.particles()
+out["fixed"] = dict(R=[R1, R2], h=[h1, h2], rne=[rne1, rne2], theta=th.tobytes().hex(), L=L.tobytes().hex())
+ctx.close()
+print("RESULT" + json.dumps(out))
+"""
+
+
+def _run(env_extra):
+    env = dict(os.environ)
+    env.update(env_extra)
+    p = subprocess.run([sys.executable, "-c", CHILD.format(root=ROOT)], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    line = [ln for ln in p.stdout.splitlines() if ln.startswith("RESULT")][-1]
+    return json.loads(line[len("RESULT"):])
+
+
+@pytest.mark.gpu
+def test_scheduling_modes_bit_identical():
+    base = _run({})
+    assert base["fixed"]["R"] == [3, 2]
+    for extra in ({"SPS_NO_LOOP": "1"}, {"SPS_NO_GRAPH": "1"}, {"SPS_NO_CLUSTER_REDUCE": "1"},
+                  {"SPS_NO_PDL": "1"}):
+        other = _run(extra)
+        assert other == base, f"results differ under {extra}"
