@@ -64,6 +64,12 @@ class Report(C.Structure):
 _lib = None
 
 
+class Schedule(C.Structure):
+    """or_schedule: the fixed design of Algorithm 3 pass 2."""
+    _fields_ = [("L", C.c_int32), ("t_cycle", C.POINTER(C.c_int32)), ("phi_cycle", C.POINTER(C.c_double)),
+                ("R_cycle", C.POINTER(C.c_int32)), ("sigma", C.POINTER(C.c_double))]
+
+
 def lib() -> C.CDLL:
     global _lib
     if _lib is None:
@@ -105,6 +111,9 @@ def lib() -> C.CDLL:
         L.or_power_search.restype = C.c_int32
         L.or_run.argtypes = [C.POINTER(Config), dp, ip, dp, dp, dp, dp, C.POINTER(Report), dp]
         L.or_run.restype = C.c_int32
+        L.or_run2.argtypes = [C.POINTER(Config), dp, ip, dp, dp, dp, dp, C.POINTER(Schedule), dp, C.c_int64,
+                              C.POINTER(Report), dp]
+        L.or_run2.restype = C.c_int32
         _lib = L
     return _lib
 
@@ -282,7 +291,10 @@ def default_report(X, C_):
 
 
 def run(X, y, C_, J, N, seed, prior_mean, prior_cov, monitors=None, report_fns=None, max_cycles=None,
-        return_theta=False, **kw):
+        return_theta=False, replay=None, record_sigma=False, **kw):
+    """Algorithm 2 (one pass).  replay: dict(t_cycle, phi_cycle, R_cycle, sigma) of a pass-1 run ->
+    Algorithm 3 step 2 with that fixed design (pass tag kw `pass_`); record_sigma: return the
+    proposal variances Sigma_lr actually used (out["sigma"], M steps x d x d)."""
     X, Xp = _d(X)
     y, yp = _i(y)
     n, k = X.shape
@@ -310,7 +322,22 @@ def run(X, y, C_, J, N, seed, prior_mean, prior_cov, monitors=None, report_fns=N
     rf, rfp = _d(report_fns)
     theta = np.zeros((J * N, d)) if return_theta else None
     thp = theta.ctypes.data_as(C.POINTER(C.c_double)) if return_theta else None
-    lib().or_run(C.byref(cfg), Xp, yp, mup, covp, monp, rfp, C.byref(rep), thp)
+    sched, keep = None, []
+    if replay is not None:
+        tc, tcp = _i(replay["t_cycle"])
+        pc, pcp = _d(replay["phi_cycle"])
+        rc, rcp = _i(replay["R_cycle"])
+        sg, sgp = _d(replay["sigma"])
+        keep += [tc, pc, rc, sg]
+        sched = Schedule(L=len(rc), t_cycle=tcp, phi_cycle=pcp, R_cycle=rcp, sigma=sgp)
+    sigma = None
+    cap = 0
+    if record_sigma:
+        cap = min(200000, max(1, (1 << 28) // (8 * d * d)))
+        sigma = np.zeros((cap, d, d))
+    sgo = sigma.ctypes.data_as(C.POINTER(C.c_double)) if record_sigma else None
+    lib().or_run2(C.byref(cfg), Xp, yp, mup, covp, monp, rfp, C.byref(sched) if sched is not None else None, sgo,
+                  cap, C.byref(rep), thp)
     L = rep.L
     out = dict(status=rep.status, L=L, total_m_steps=rep.total_m_steps, h_final=rep.h_final,
                logml=rep.logml, logml_nse=rep.logml_nse, pairs=rep.pairs,
@@ -320,4 +347,18 @@ def run(X, y, C_, J, N, seed, prior_mean, prior_cov, monitors=None, report_fns=N
                mean=arrs["mean"], sd=arrs["sd"], nse=arrs["nse"], rne=arrs["rne"])
     if return_theta:
         out["theta"] = theta
+    if record_sigma:
+        out["sigma"] = sigma[: rep.total_m_steps].copy()
     return out
+
+
+def two_pass(X, y, C_, J, N, seed1, seed2, prior_mean, prior_cov, **kw):
+    """Algorithm 3: an adaptive pass (seed1, pass tag 0) records L, t_l / phi_l, R_l and
+    Sigma_lr; pass 2 (seed2, pass tag 1) runs Algorithm 2 with that design fixed."""
+    p1 = run(X, y, C_, J, N, seed1, prior_mean, prior_cov, record_sigma=True, **kw)
+    if p1["status"] != 0:
+        return p1, None
+    kw2 = dict(kw)
+    kw2["pass_"] = 1
+    p2 = run(X, y, C_, J, N, seed2, prior_mean, prior_cov, replay=p1, **kw2)
+    return p1, p2

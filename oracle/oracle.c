@@ -506,6 +506,13 @@ static int nthreads_of(const or_config* cfg) {
 int32_t or_run(const or_config* cfg, const double* X, const int32_t* y, const double* prior_mean,
                const double* prior_cov, const double* monitors, const double* report_fns,
                or_report* rep, double* theta_out) {
+  return or_run2(cfg, X, y, prior_mean, prior_cov, monitors, report_fns, NULL, NULL, 0, rep, theta_out);
+}
+
+int32_t or_run2(const or_config* cfg, const double* X, const int32_t* y, const double* prior_mean,
+                const double* prior_cov, const double* monitors, const double* report_fns,
+                const or_schedule* replay, double* sigma_out, int64_t sigma_cap, or_report* rep,
+                double* theta_out) {
   const int32_t n = cfg->n, k = cfg->k, C = cfg->C, J = cfg->J, N = cfg->N;
   if (n < 1 || k < 1 || C < 2 || C > 64 || J < 2 || N < 2 || N > 16384 || k * (C - 1) > 512 ||
       cfg->n_monitors < 1 || cfg->max_cycles < 1 || cfg->h_min > cfg->h_init || cfg->h_init > cfg->h_max)
@@ -604,16 +611,22 @@ int32_t or_run(const or_config* cfg, const double* X, const int32_t* y, const do
           s1 += w;
           s2 += w * w;
         }
-        if (s1 * s1 < cfg->ess_frac * (double)P * s2 || s == n) break;
+        if (replay ? s == replay->t_cycle[ell - 1]
+                   : (s1 * s1 < cfg->ess_frac * (double)P * s2 || s == n))
+          break;
       }
       t = s;
       for (int64_t p = 0; p < P; ++p) Lk[p] += lw[p];
     } else {
       double rem = 1.0 - phi;
       double dphi;
-      or_power_search(Lk, P, rem, cfg->ess_frac, &dphi);
+      if (replay) {
+        dphi = replay->phi_cycle[ell - 1] - phi;
+      } else {
+        or_power_search(Lk, P, rem, cfg->ess_frac, &dphi);
+      }
       for (int64_t p = 0; p < P; ++p) lw[p] = dphi * Lk[p];
-      phi = (dphi == rem) ? 1.0 : phi + dphi;
+      phi = replay ? replay->phi_cycle[ell - 1] : ((dphi == rem) ? 1.0 : phi + dphi);
     }
     /* log marginal likelihood increment (R10):
      * log[(JN)^-1 sum_jn w_jn] pooled and log[N^-1 sum_n w_jn] per group. */
@@ -652,7 +665,7 @@ int32_t or_run(const or_config* cfg, const double* X, const int32_t* y, const do
     { double* tmp = lp; lp = lp2; lp2 = tmp; }
 
     /* ---------------- M phase ------------------------ */
-    const int final_cycle = power ? (phi == 1.0) : (t == n);
+    const int final_cycle = replay ? (ell == replay->L) : (power ? (phi == 1.0) : (t == n));
     const double K = final_cycle ? cfg->K_final : cfg->K_inter;   /* PAPER.md:418-424, R14 */
     const int32_t r_t1 = power ? n : t;
     const double temper = power ? phi : 1.0;
@@ -664,7 +677,13 @@ int32_t or_run(const or_config* cfg, const double* X, const int32_t* y, const do
         st = OR_E_MIXING;
         goto out;
       }
-      /* i. sample variance V_lr of all JN particles (R11) */
+      /* i. sample variance V_lr of all JN particles (R11) -- pass 2 of
+       * Algorithm 3 takes Sigma_lr from the pass-1 record instead */
+      double hd = (double)h / 100.0;
+      if (replay) {
+        memcpy(Sig, replay->sigma + (int64_t)mstep * d * d, sizeof(double) * d * d);
+        for (int32_t i = 0; i < d * d; ++i) V[i] = Sig[i] / hd;  /* (only the ridge retry reads V) */
+      } else {
       for (int32_t i = 0; i < d; ++i) {
         double s = 0.0;
         for (int64_t p = 0; p < P; ++p) s += theta[p * d + i];
@@ -677,8 +696,9 @@ int32_t or_run(const or_config* cfg, const double* X, const int32_t* y, const do
           V[i * d + j] = V[j * d + i] = s / (double)(P - 1);
         }
       /* Sigma_lr = h_lr V_lr, Cholesky with one ridge retry (R13) */
-      double hd = (double)h / 100.0;
       for (int32_t i = 0; i < d * d; ++i) Sig[i] = hd * V[i];
+      }
+      if (sigma_out && (int64_t)mstep < sigma_cap) memcpy(sigma_out + (int64_t)mstep * d * d, Sig, sizeof(double) * d * d);
       if (or_cholesky(d, Sig, Lprop) != OR_OK) {
         double tr = 0.0;
         for (int32_t i = 0; i < d; ++i) tr += V[i * d + i];
@@ -741,7 +761,7 @@ int32_t or_run(const or_config* cfg, const double* X, const int32_t* y, const do
         or_group_stats(g, J, N, NULL, NULL, NULL, &rne);
         if (rne < minrne) minrne = rne;
       }
-      if (minrne >= K) break;
+      if (replay ? r == replay->R_cycle[ell - 1] : minrne >= K) break;
     }
     rep->L = ell;
     rep->total_m_steps += r;

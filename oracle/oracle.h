@@ -107,6 +107,28 @@ int32_t or_run(const or_config* cfg, const double* X, const int32_t* y, const do
                const double* prior_cov, const double* monitors, const double* report_fns,
                or_report* rep, double* theta_out);
 
+/* ---- Algorithm 3 (two pass) ---------------------------
+ * A fixed design for pass 2: L cycles, their break points t_l (data tempering)
+ * or phi_l (power tempering), M steps R_l, and the proposal variance matrices
+ * Sigma_lr (d x d, row-major, one per M step in execution order). */
+typedef struct {
+  int32_t L;
+  const int32_t* t_cycle;
+  const double* phi_cycle;
+  const int32_t* R_cycle;
+  const double* sigma;
+} or_schedule;
+
+/* or_run with (a) replay != NULL: Algorithm 2 with the cycle break points, M
+ * step counts and proposal variances fixed by `replay` (Algorithm 3 step 2 --
+ * no ESS rule, no h / V adaptation, no RNE stopping); (b) sigma_out != NULL:
+ * the Sigma_lr actually used are recorded (capacity sigma_cap steps; Algorithm
+ * 3 step 1).  Everything else as or_run. */
+int32_t or_run2(const or_config* cfg, const double* X, const int32_t* y, const double* prior_mean,
+                const double* prior_cov, const double* monitors, const double* report_fns,
+                const or_schedule* replay, double* sigma_out, int64_t sigma_cap, or_report* rep,
+                double* theta_out);
+
 #ifdef __cplusplus
 }
 #endif

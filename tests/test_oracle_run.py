@@ -107,3 +107,43 @@ def test_resampling_schemes_agree(orc):
         r = orc.run(X, y, 2, 10, 400, seed=4, prior_mean=np.zeros(2), prior_cov=cov, resampling=scheme)
         assert r["status"] == 0
         assert abs(r["mean"][0] - qmean[0]) <= 4 * r["nse"][0]
+
+
+@pytest.mark.parametrize("mode", ["data", "power"])
+def test_two_pass_quadrature_and_agreement(orc, mode):
+    """Algorithm 3: pass 2 replays pass 1's design exactly (same L, t_l / phi_l, R_l)
+    with fresh random numbers; its posterior mean and logML are within 3 NSE of the quadrature values in
+    >= 8 of 10 seeds (the fixed-design SMC the CLT covers), and pass 1 and pass 2 agree within 3 combined
+    NSE in >= 8 of 10 (the paper's Table 2 property)."""
+    X, y = _tiny_binary()
+    cov = orc.g_prior(X, 2, 0.25)
+    fn = X.mean(axis=0)[None, :]
+    qml, qmean = quadrature.posterior(X, y, 2, np.zeros(2), cov, fn)
+    ok_m = ok_l = ok_a = 0
+    tmp = orc.DATA if mode == "data" else orc.POWER
+    for seed in range(1, 11):
+        p1, p2 = orc.two_pass(X, y, 2, 10, 400, seed, 5000 + seed, np.zeros(2), cov, tempering=tmp)
+        assert p1["status"] == 0 and p2 is not None and p2["status"] == 0
+        assert p2["L"] == p1["L"] and list(p2["R_cycle"]) == list(p1["R_cycle"])
+        if mode == "data":
+            assert list(p2["t_cycle"]) == list(p1["t_cycle"])
+        else:
+            assert list(p2["phi_cycle"]) == list(p1["phi_cycle"])
+        assert p1["sigma"].shape == (p1["total_m_steps"], 2, 2)
+        ok_m += abs(p2["mean"][0] - qmean[0]) <= 3 * p2["nse"][0]
+        ok_l += abs(p2["logml"] - qml) <= 3 * p2["logml_nse"]
+        ok_a += abs(p1["logml"] - p2["logml"]) <= 3 * math.hypot(p1["logml_nse"], p2["logml_nse"])
+    assert ok_m >= 8 and ok_l >= 8 and ok_a >= 8, (ok_m, ok_l, ok_a)
+
+
+def test_two_pass_sigma_is_the_pass1_proposal(orc):
+    """The recorded Sigma_lr are the matrices pass 1 factored: symmetric positive definite, and replaying
+    them with pass 1's own seed and pass tag reproduces pass 1 exactly (same particles, same logML)."""
+    X, y = _tiny_binary()
+    cov = orc.g_prior(X, 2, 0.25)
+    p1 = orc.run(X, y, 2, 4, 128, seed=3, prior_mean=np.zeros(2), prior_cov=cov, record_sigma=True,
+                 return_theta=True)
+    for S in p1["sigma"]:
+        assert np.allclose(S, S.T) and np.all(np.linalg.eigvalsh(S) > 0)
+    again = orc.run(X, y, 2, 4, 128, seed=3, prior_mean=np.zeros(2), prior_cov=cov, replay=p1, return_theta=True)
+    assert again["logml"] == p1["logml"] and np.array_equal(again["theta"], p1["theta"])
