@@ -160,6 +160,37 @@ sps_status sps_get_particles(sps_ctx* ctx, double* theta_host, double* L_host, d
  * without re-uploading data.  Collective. */
 sps_status sps_reset(sps_ctx* ctx, uint64_t seed, int32_t pass);
 
+/* ---- Algorithm 3: two passes --------------------------
+ * Pass 1 runs Algorithm 2 and records its design: the cycle break points t_l
+ * (data tempering) or phi_l (power tempering), the M steps R_l per cycle
+ * (sps_run's report) and the proposal variance Sigma_lr = (h_lr/100) V_lr of
+ * every M step.  Pass 2 restarts with an independent
+ * seed and pass tag 1 (sps_reset) and reruns Algorithm 1 with that design
+ * fixed: no ESS rule, no RNE stopping rule, Sigma_lr taken
+ * from the record (h is still adapted and reported, and the ridge retry R13
+ * uses V = Sigma_lr / (h/100)). */
+
+/* Record Sigma_lr of every M step run from now on (on != 0) into a device
+ * buffer indexed by the global M-step number (0-based, counted over the run
+ * since sps_create / sps_reset; the record survives sps_reset and is
+ * overwritten from step 0 by the next run).  Errors: SPS_E_CUDA. */
+sps_status sps_record_sigma(sps_ctx* ctx, int32_t on);
+
+/* Copy recorded Sigma_lr of global M steps [first, first + count) to `out`
+ * (host, count x d x d row-major, caller-owned).  Errors: SPS_E_STATE (not
+ * recording or steps not yet run), SPS_E_CONFIG. */
+sps_status sps_get_sigma(sps_ctx* ctx, int64_t first, int64_t count, double* out);
+
+/* Fix the design of the next sps_run (Algorithm 3 step 2): L cycles with
+ * t_cycle[l] (data) or phi_cycle[l] (power; strictly increasing, ending at T /
+ * 1 for a run to the posterior), R_cycle[l] >= 1 M steps, and sigma: the
+ * sum_l R_l proposal variances d x d row-major in execution order (host; all
+ * arrays copied, caller may free on return).  The design stays set across
+ * sps_reset; L = 0 clears it (adaptive runs again).  Errors: SPS_E_CONFIG
+ * (missing arrays, non-increasing schedule, L > max_cycles), SPS_E_CUDA. */
+sps_status sps_set_design(sps_ctx* ctx, int32_t L, const int32_t* t_cycle, const double* phi_cycle,
+                          const int32_t* R_cycle, const double* sigma);
+
 typedef struct sps_counters {
   int64_t launches;     /* kernel launches by the library since the last create/reset */
   int64_t k1_launches;  /* log-likelihood (K1) launches                                 */

@@ -68,6 +68,7 @@ EXPORTED = [
     "sps_moments", "sps_get_particles", "sps_shard", "sps_destroy", "sps_last_error", "sps_nccl_unique_id",
     "sps_g_prior", "sps_test_philox", "sps_test_normals", "sps_test_portable", "sps_test_resample_int",
     "sps_test_resample_group", "sps_test_accept", "sps_reset", "sps_set_profiling", "sps_get_counters", "sps_sync", "sps_loopback_unique_id",
+    "sps_record_sigma", "sps_get_sigma", "sps_set_design",
 ]
 
 
@@ -134,6 +135,9 @@ def _declare(L):
         "sps_sync": ([vp], st),
         "sps_set_profiling": ([vp, C.c_int32], st),
         "sps_get_counters": ([vp, C.POINTER(Counters)], st),
+        "sps_record_sigma": ([vp, C.c_int32], st),
+        "sps_get_sigma": ([vp, C.c_int64, C.c_int64, dp], st),
+        "sps_set_design": ([vp, C.c_int32, ip, dp, ip, dp], st),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

@@ -147,6 +147,48 @@ class Sps:
         """sps_reset: new seed on the resident data (fresh initial particles)."""
         _check(lib().sps_reset(self.ctx, int(seed), int(pass_)), self.ctx)
 
+    # ---------------------------------------------- Algorithm 3 (PAPER.md:544-607)
+    def record_sigma(self, on=True):
+        """sps_record_sigma: record Sigma_lr of every M step (pass 1)."""
+        _check(lib().sps_record_sigma(self.ctx, 1 if on else 0), self.ctx)
+
+    def sigma(self, first, count):
+        """sps_get_sigma: recorded Sigma_lr of global M steps [first, first + count) -> (count, d, d)."""
+        out = np.zeros((int(count), self.d, self.d))
+        _check(lib().sps_get_sigma(self.ctx, int(first), int(count), _dptr(out)), self.ctx)
+        return out
+
+    def set_design(self, design=None):
+        """sps_set_design: fix t_l / phi_l, R_l and Sigma_lr for the next run (None clears)."""
+        if design is None:
+            _check(lib().sps_set_design(self.ctx, 0, None, None, None, None), self.ctx)
+            return
+        R = np.ascontiguousarray(design["R_cycle"], dtype=np.int32)
+        t = np.ascontiguousarray(design.get("t_cycle", np.zeros(R.size)), dtype=np.int32)
+        phi = np.ascontiguousarray(design.get("phi_cycle", np.zeros(R.size)), dtype=np.float64)
+        sig = np.ascontiguousarray(design["sigma"], dtype=np.float64)
+        assert sig.shape == (int(R.sum()), self.d, self.d), sig.shape
+        P32 = C.POINTER(C.c_int32)
+        _check(lib().sps_set_design(self.ctx, R.size, t.ctypes.data_as(P32), _dptr(phi), R.ctypes.data_as(P32),
+                                    _dptr(sig)), self.ctx)
+
+    def two_pass(self, seed1, seed2, **run_kw):
+        """Algorithm 3: pass 1 (adaptive, seed1, pass tag 0) records the design; pass 2 (seed2, pass
+        tag 1) reruns Algorithm 1 with it fixed.  Returns (pass-1 report + "sigma", pass-2 report)."""
+        self.set_design(None)
+        self.reset(seed1, 0)
+        self.record_sigma(True)
+        p1 = self.run(**run_kw)
+        p1["sigma"] = self.sigma(0, p1["total_m_steps"])
+        self.record_sigma(False)
+        self.reset(seed2, 1)
+        self.set_design(p1)
+        try:
+            p2 = self.run(**run_kw)
+        finally:
+            self.set_design(None)
+        return p1, p2
+
     def set_profiling(self, on=True):
         _check(lib().sps_set_profiling(self.ctx, 1 if on else 0), self.ctx)
 

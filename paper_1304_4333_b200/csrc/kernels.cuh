@@ -183,6 +183,14 @@ struct FinArgs {
   int rmax;                     // step cap of the M phase (adaptive: max_m_steps; fixed: R)
   cudaGraphConditionalHandle cond;
   int stage_S;         // group sums staged in shared memory (else read from gath)
+  // Algorithm 3: the proposal variance Sigma_lr of global M step s (computed here
+  // for the step that follows: s = sig_step if >= 0, else ctl->step_cur + 1) is recorded into
+  // sig_rec[s] (pass 1) or taken from sig_in[s] instead of (h/100) V (pass 2, fixed design)
+  double* sig_rec;     // d x d per step, capacity sig_rec_cap steps (null: not recording)
+  int64_t sig_rec_cap;
+  const double* sig_in;  // d x d per step, sig_in_n steps (null: adaptive Sigma = (h/100) V)
+  int64_t sig_in_n;
+  int64_t sig_step;
 };
 
 // Reported functional moments (K11) from the gathered

@@ -839,16 +839,24 @@ __device__ __noinline__ double group_sum_global(const FinArgs& f, int j, int i) 
 
 // chol((h/100) V) by the whole block for d > 32 (sA: d x d, (h/100) V), one
 // ridge retry (R13); factor -> f.Lprop (row stride ldp).
-__device__ __noinline__ void block_factor(const FinArgs& f, double* sA, const double* sV, double hd, int ldp, int* s_flag) {
+// The ridge base V: the pooled covariance, or Sigma_lr / (h/100) when Sigma_lr comes from a fixed
+// design (Algorithm 3 pass 2; the oracle's reading of R13 there).
+__device__ __forceinline__ double ridge_base(const double* sV, const double* sig, double hd, int idx) {
+  return sig ? __ldcg(sig + idx) / hd : sV[idx];
+}
+
+__device__ __noinline__ void block_factor(const FinArgs& f, double* sA, const double* sV, double hd, int ldp, int* s_flag,
+                                          const double* sig) {
   const int d = f.d, lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   bool ok = block_cholesky(sA, d, s_flag);
   if (threadIdx.x == 0) f.ctl->chol_ridge = ok ? 0 : 1;
   if (!ok) {
     double tr = 0.0;
-    for (int i = 0; i < d; ++i) tr += sV[i * d + i];
+    for (int i = 0; i < d; ++i) tr += ridge_base(sV, sig, hd, i * d + i);
     const double ridge = 1e-8 * tr / (double)d;
     for (int i = w; i < d; i += nw)
-      for (int l = lane; l < d; l += 32) sA[i * d + l] = hd * (sV[i * d + l] + (i == l ? ridge : 0.0));
+      for (int l = lane; l < d; l += 32)
+        sA[i * d + l] = hd * (ridge_base(sV, sig, hd, i * d + l) + (i == l ? ridge : 0.0));
     __syncthreads();
     ok = block_cholesky(sA, d, s_flag);
     if (!ok) {
@@ -992,6 +1000,10 @@ __device__ void finalize_body(const FinArgs& f, double* sm) {
   // ---- V (R11) and the factorization input (h/100) V, identity-padded to D x D
   const double hd = (double)s_h / 100.0;
   const int DA = d > 32 ? d : D;
+  // Algorithm 3: Sigma of the step this factor serves, from / into the design record
+  const int64_t sstep = f.sig_step >= 0 ? f.sig_step : (int64_t)__ldcg(&f.ctl->step_cur) + 1;
+  const double* sig = (f.sig_in && sstep < f.sig_in_n) ? f.sig_in + sstep * dd : nullptr;
+  double* srec = (f.sig_rec && sstep < f.sig_rec_cap) ? f.sig_rec + sstep * dd : nullptr;
 #pragma unroll 2
   for (int i = w; i < DA; i += nw) {
     const double ci = i < d ? sbar[i] - sshift[i] : 0.0;
@@ -1001,7 +1013,9 @@ __device__ void finalize_body(const FinArgs& f, double* sm) {
         const double cl = sbar[l] - sshift[l];
         const double v = (sM[i * d + l] - P * ci * cl) / (P - 1.0);
         sV[i * d + l] = v;
-        sA[i * ldc + l] = hd * v;
+        const double a = sig ? __ldcg(sig + i * d + l) : hd * v;  // Sigma_lr = (h/100) V_lr
+        sA[i * ldc + l] = a;
+        if (srec) srec[i * d + l] = a;
       } else {
         sA[i * ldc + l] = i == l ? 1.0 : 0.0;
       }
@@ -1017,11 +1031,12 @@ __device__ void finalize_body(const FinArgs& f, double* sm) {
     if (!ok) {
       double tr = 0.0;
 #pragma unroll 1
-      for (int i = 0; i < d; ++i) tr += sV[i * d + i];
+      for (int i = 0; i < d; ++i) tr += ridge_base(sV, sig, hd, i * d + i);
       const double ridge = 1e-8 * tr / (double)d;
       if (lane < d)
 #pragma unroll 1
-        for (int l = 0; l < d; ++l) sA[lane * ldc + l] = hd * (sV[lane * d + l] + (lane == l ? ridge : 0.0));
+        for (int l = 0; l < d; ++l)
+          sA[lane * ldc + l] = hd * (ridge_base(sV, sig, hd, lane * d + l) + (lane == l ? ridge : 0.0));
       __syncwarp();
       ok = warp_cholesky_d(sA, f.Lprop, ldp, d);
       ridge_used = 1;
@@ -1071,7 +1086,7 @@ __device__ void finalize_body(const FinArgs& f, double* sm) {
   if (f.trace && threadIdx.x == 0) f.trace[4] = gtimer();
   if (f.mode == 1 && threadIdx.x == 0) tl_mark_any(19);
   if (d > 32) {  // block Cholesky (larger d)
-    block_factor(f, sA, sV, hd, ldp, &s_flag);
+    block_factor(f, sA, sV, hd, ldp, &s_flag, sig);
   }
   if (f.mode == 1 && threadIdx.x == 0) {
     double minrne = INFINITY;

@@ -199,6 +199,14 @@ struct sps_ctx {
   double* inc_dev = nullptr;
   int inc_cap = 1024, inc_base = 0;
   int last_adv = 0;  // observations absorbed by the last data-tempering C phase (first galloping chunk)
+  // Algorithm 3: Sigma_lr record of pass 1, fixed design of pass 2
+  bool recording = false;
+  double* sig_rec = nullptr;     // d x d per global M step
+  int64_t sig_rec_cap = 0;
+  double* sig_in = nullptr;      // fixed design: d x d per global M step
+  int64_t sig_in_n = 0;
+  std::vector<int> des_t, des_R;
+  std::vector<double> des_phi;
   // counters (sps_get_counters)
   int64_t launches = 0, k1_launches = 0, syncs = 0;
   double k1_pairs = 0.0, k1_ms = 0.0;
@@ -797,6 +805,11 @@ sps_status make_fin(sps_ctx* c, int mode, bool allow_stop, const int* stop, int 
     f.rmax = c->loop_rmax;
     f.host_out = c->dslot;
   }
+  f.sig_rec = c->recording ? c->sig_rec : nullptr;
+  f.sig_rec_cap = c->recording ? c->sig_rec_cap : 0;
+  f.sig_in = c->sig_in;
+  f.sig_in_n = c->sig_in_n;
+  f.sig_step = mode == 0 ? (int64_t)c->mstep : -1;  // mode 1: the device step (ctl->step_cur) + 1
   f.stage_S = fin_smem_doubles(c->d, c->J, c->nmon, true) * 8 <= 200 * 1024 ? 1 : 0;
   const size_t smem = (size_t)fin_smem_doubles(c->d, c->J, c->nmon, f.stage_S != 0) * sizeof(double);
   if (smem > 200 * 1024) return fail(c, SPS_E_CONFIG, "d = %d too large for the finalize kernel", c->d);
@@ -887,7 +900,8 @@ void free_ctx(sps_ctx* c) {
                   c->lp2, c->lw, c->lw_cur, c->theta_s, c->lp_s, c->part, c->gpart, c->mpart, c->slice, c->gath,
                   c->shift, c->Lprop, c->V, c->rne, c->lwbuf, c->essparts, c->essslice, c->essgath, c->grp_ms,
                   c->grp_ms_gath, c->Lj, c->Lj_gath, c->scal, c->pw_parts, c->pw_slice, c->pw_gath, c->mx_parts,
-                  c->mx_slice, c->mx_gath, c->fn_A, c->fn_out, c->ll_scratch, c->Sinv, c->LpriorP, c->SinvP, c->Rp, c->RpP, c->bpart, c->ctl, c->inc_dev};
+                  c->mx_slice, c->mx_gath, c->fn_A, c->fn_out, c->ll_scratch, c->Sinv, c->LpriorP, c->SinvP, c->Rp, c->RpP, c->bpart, c->ctl, c->inc_dev,
+                  c->sig_rec, c->sig_in};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, fs);
   lap("cudaFree");
@@ -1531,7 +1545,8 @@ sps_status sps_cphase(sps_ctx* c, int32_t t_target, double phi_target, int32_t* 
     }
     k_power_apply<<<pgrid, 256, 0, c->stream>>>(c->L, Pl, dphi, c->lw);
     CHECK_LAUNCH(c);
-    c->phi = (dphi == rem) ? 1.0 : c->phi + dphi;
+    // a fixed schedule (Algorithm 3 pass 2) lands exactly on the recorded phi_l
+    c->phi = phi_target >= 0 ? phi_target : ((dphi == rem) ? 1.0 : c->phi + dphi);
   }
   PROF_END(c, CAT_CPHASE);
   // ---- S phase + log-ML increments (R10) ----
@@ -1814,6 +1829,21 @@ static sps_status replay_mstep(sps_ctx* c, uint32_t step) {
   return SPS_OK;
 }
 
+// Sigma_lr record (Algorithm 3 step 1): room for global M steps [0, need), contents kept.
+static sps_status reserve_sigma(sps_ctx* c, int64_t need) {
+  if (need <= c->sig_rec_cap) return SPS_OK;
+  const int64_t cap = std::max<int64_t>(need, 2 * c->sig_rec_cap), dd = (int64_t)c->d * c->d;
+  double* nb = nullptr;
+  TRY(dalloc(c, &nb, (size_t)(cap * dd)));
+  if (c->sig_rec) {
+    CU(c, cudaMemcpyAsync(nb, c->sig_rec, sizeof(double) * c->sig_rec_cap * dd, cudaMemcpyDeviceToDevice, c->stream));
+    CU(c, cudaFreeAsync(c->sig_rec, c->stream));
+  }
+  c->sig_rec = nb;
+  c->sig_rec_cap = cap;
+  return SPS_OK;
+}
+
 sps_status sps_mphase(sps_ctx* c, int32_t R_fixed, int32_t* R_out, double* min_rne, int32_t* h_out) {
   if (!c) return SPS_E_CONFIG;
   CU(c, cudaSetDevice(c->cfg.device));
@@ -1825,6 +1855,7 @@ sps_status sps_mphase(sps_ctx* c, int32_t R_fixed, int32_t* R_out, double* min_r
   // reset stop / step counter; moments + chol(h V) of the resampled particles
   CU(c, cudaMemsetAsync(&c->ctl->stop, 0, sizeof(int), c->stream));
   CU(c, cudaMemsetAsync(&c->ctl->steps_done, 0, sizeof(int), c->stream));
+  if (c->recording) TRY(reserve_sigma(c, (int64_t)c->mstep + Rmax + 2));
   if (c->need_pre_moments) {
     TRY(moments_finalize(c, false, 1, 1.0, 0u, nullptr, nullptr, 0, false, -1));
     c->need_pre_moments = false;
@@ -1975,10 +2006,15 @@ sps_status sps_moments(sps_ctx* c, int32_t m, const double* A, double* mean, dou
 sps_status sps_run(sps_ctx* c, sps_report* rep) {
   if (!c || !rep) return SPS_E_CONFIG;
   sps_status st = SPS_OK;
+  const bool fixed = !c->des_R.empty();  // Algorithm 3 pass 2: the recorded design (sps_set_design)
+  const bool power = c->cfg.tempering == SPS_POWER_TEMPERING;
   while (!c->finished) {
-    st = sps_cphase(c, -1, -1.0, nullptr, nullptr, nullptr);
+    const int l = c->ell;
+    if (fixed && l >= (int)c->des_R.size()) break;
+    st = sps_cphase(c, fixed && !power ? c->des_t[l] : -1, fixed && power ? c->des_phi[l] : -1.0, nullptr, nullptr,
+                    nullptr);
     if (st != SPS_OK) break;
-    st = sps_mphase(c, 0, nullptr, nullptr, nullptr);
+    st = sps_mphase(c, fixed ? c->des_R[l] : 0, nullptr, nullptr, nullptr);
     if (st != SPS_OK) break;
   }
   rep->status = st;
@@ -2016,6 +2052,63 @@ sps_status sps_run(sps_ctx* c, sps_report* rep) {
     }
     TRY(sps_moments(c, rep->n_report, fns, rep->mean, rep->sd, rep->nse, rep->rne));
   }
+  return SPS_OK;
+}
+
+sps_status sps_record_sigma(sps_ctx* c, int32_t on) {
+  if (!c) return SPS_E_CONFIG;
+  CU(c, cudaSetDevice(c->cfg.device));
+  c->recording = on != 0;
+  if (c->recording) TRY(reserve_sigma(c, (int64_t)c->mstep + 2));
+  return SPS_OK;
+}
+
+sps_status sps_get_sigma(sps_ctx* c, int64_t first, int64_t count, double* out) {
+  if (!c || first < 0 || count < 0 || (count > 0 && !out)) return SPS_E_CONFIG;
+  if (count == 0) return SPS_OK;
+  CU(c, cudaSetDevice(c->cfg.device));
+  if (!c->recording || first + count > (int64_t)c->mstep || first + count > c->sig_rec_cap)
+    return fail(c, SPS_E_STATE, "sps_get_sigma: steps [%lld, %lld) not recorded (recording %d, %u steps run)",
+                (long long)first, (long long)(first + count), (int)c->recording, c->mstep);
+  const int64_t dd = (int64_t)c->d * c->d;
+  CU(c, cudaMemcpyAsync(out, c->sig_rec + first * dd, sizeof(double) * count * dd, cudaMemcpyDeviceToHost, c->stream));
+  CU(c, cudaStreamSynchronize(c->stream));
+  return SPS_OK;
+}
+
+sps_status sps_set_design(sps_ctx* c, int32_t L, const int32_t* t_cycle, const double* phi_cycle,
+                          const int32_t* R_cycle, const double* sigma) {
+  if (!c || L < 0) return SPS_E_CONFIG;
+  CU(c, cudaSetDevice(c->cfg.device));
+  CU(c, cudaStreamSynchronize(c->stream));
+  if (c->sig_in) CU(c, cudaFreeAsync(c->sig_in, c->stream));
+  c->sig_in = nullptr;
+  c->sig_in_n = 0;
+  c->des_t.clear();
+  c->des_R.clear();
+  c->des_phi.clear();
+  if (L == 0) return SPS_OK;
+  const bool power = c->cfg.tempering == SPS_POWER_TEMPERING;
+  if (!R_cycle || !sigma || (power ? !phi_cycle : !t_cycle) || L > c->cfg.max_cycles)
+    return fail(c, SPS_E_CONFIG, "sps_set_design: missing arrays or L > max_cycles");
+  int64_t steps = 0;
+  for (int l = 0; l < L; ++l) {
+    if (R_cycle[l] < 1) return fail(c, SPS_E_CONFIG, "sps_set_design: R_%d < 1", l + 1);
+    if (power ? !(phi_cycle[l] > (l ? phi_cycle[l - 1] : 0.0) && phi_cycle[l] <= 1.0)
+              : !(t_cycle[l] > (l ? t_cycle[l - 1] : 0) && t_cycle[l] <= c->n))
+      return fail(c, SPS_E_CONFIG, "sps_set_design: schedule not increasing at cycle %d", l + 1);
+    steps += R_cycle[l];
+  }
+  const int64_t dd = (int64_t)c->d * c->d;
+  TRY(dalloc(c, &c->sig_in, (size_t)(steps * dd)));
+  CU(c, cudaMemcpyAsync(c->sig_in, sigma, sizeof(double) * steps * dd, cudaMemcpyHostToDevice, c->stream));
+  CU(c, cudaStreamSynchronize(c->stream));
+  c->sig_in_n = steps;
+  c->des_R.assign(R_cycle, R_cycle + L);
+  if (power)
+    c->des_phi.assign(phi_cycle, phi_cycle + L);
+  else
+    c->des_t.assign(t_cycle, t_cycle + L);
   return SPS_OK;
 }
 
