@@ -42,7 +42,7 @@ ORACLE_SAMPLE = dict(J=16, N=256)
 FP64_PEAK_TFLOPS = 37.07
 # FP64-pipe operations per pair of K1's binary epilogue (1 DADD relu-sum,
 # 10 table-exp, 1 DADD (1 + e), 1 DMUL product), counted from the SASS of k_loglik_bin_mma.
-EPILOGUE_DP_OPS_BINARY = 12.0  # counted DP ops of the implemented epilogue (SURVEY 8(d) ii): exp 10, fma(P, e, P), +relu
+EPILOGUE_DP_OPS_BINARY = 11.0  # counted DP ops of the implemented epilogue (SURVEY 8(d) ii): exp 9, fma(P, e, P), +relu
 # K1 contraction: 4 floor(k/4) covariates on DMMA + (k mod 4 <= 2) DFMAs, i.e. k FMAs per pair for
 # k = 25; algorithmic contraction flops per pair = 2 k (C - 1).
 

@@ -17,7 +17,8 @@
 //    multiplied into a running product with its exponent renormalized every
 //    64 observations, and ONE log per particle is taken at the end.  e^-a is
 //    a table-driven exp (2^(i/64) table in smem, degree-5 polynomial on
-//    |r| <= ln2/128): 10 FP64 ops.  Binary total: 15 FP64 ops per pair + k FMAs.
+//    |r| <= ln2/128, one-fma range reduction): 9 FP64 ops.  Binary total (DMMA kernel): 11 FP64
+//    ops per pair + k FMAs (exp 9, Pp (1 + e) as one fma, + relu).
 //  * Grid = particle tiles x observation chunks, chunk count chosen so the
 //    block count fills whole waves of 148 SMs x resident blocks; chunk
 //    partials are summed in fixed order by the consumer (deterministic).
@@ -149,12 +150,13 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
                : "d"(a), "d"(b));
 }
 
-// e^-a for 0 <= a <= 708: table-driven, ~1 ulp.  sT = 2^(i/64).
+// e^-a for 0 <= a <= 708: table-driven, ~1 ulp.  sT = 2^(i/64).  Range reduction by ONE fma
+// with ln2/64 rounded to double: its error (1.2e-18) times |k| <= 65600 perturbs r by < 8e-14
+// only where e^-a < 1e-300; the absolute error it adds to e^-a is < 4e-17 for every a.
 __device__ __forceinline__ double exp_neg(double a, const double* __restrict__ sT) {
   const double t = fma(a, -0x1.71547652b82fep+6, 0x1.8p52);  // MAGIC - round(a 64/ln2)
   const double kd = t - 0x1.8p52;                             // k = -round(a 64/ln2)
-  double r = fma(kd, -0x1.62e42fec00000p-7, -a);              // r = -a - k ln2/64 (hi/lo)
-  r = fma(kd, -0x1.d1cf79abc9e3bp-38, r);
+  const double r = fma(kd, -0x1.62e42fefa39efp-7, -a);        // r = -a - k ln2/64
   const int ki = __double2loint(t);
   const double T = sT[ki & 63];
   const double q = r * fma(fma(fma(fma(r, 1.0 / 120.0, 1.0 / 24.0), r, 1.0 / 6.0), r, 0.5), r, 1.0);
@@ -163,16 +165,35 @@ __device__ __forceinline__ double exp_neg(double a, const double* __restrict__ s
 }
 
 // e^-a for 0 <= a <= 708 with the 2^(i/256) table (sT256 in smem): |r| <= ln2/512,
-// degree-4 polynomial (truncation 4e-17): 9 FP64 ops.
+// degree-4 polynomial (truncation 4e-17): 8 FP64 ops.
 __device__ __forceinline__ double exp_neg256(double a, const double* __restrict__ sT) {
   const double t = fma(a, -0x1.71547652b82fep+8, 0x1.8p52);  // MAGIC - round(a 256/ln2)
   const double kd = t - 0x1.8p52;
-  double r = fma(kd, -0x1.62e42fec00000p-9, -a);
-  r = fma(kd, -0x1.d1cf79abc9e3bp-40, r);
+  const double r = fma(kd, -0x1.62e42fefa39efp-9, -a);  // one fma (see exp_neg)
   const int ki = __double2loint(t);
   const double T = sT[ki & 255];
   const double q = r * fma(fma(fma(r, 1.0 / 24.0, 1.0 / 6.0), r, 0.5), r, 1.0);
   const double Ts = __hiloint2double(__double2hiint(T) + ((ki >> 8) << 20), __double2loint(T));
+  return fma(Ts, q, Ts);
+}
+
+// 2^(j/1024), j = 0..1023 (global; staged into shared memory by K1's prologue)
+__device__ const double g_exp2tab1024[1024] = {
+#include "exp2tab1024.inc"
+};
+
+// e^-a for 0 <= a <= 708 with the 2^(j/1024) table (sT in smem): |r| <= ln2/2048, degree-3
+// polynomial (truncation r^4/24 <= 5.5e-16 relative), range reduction by ONE fma with ln2/1024
+// rounded to double (its error 7.5e-20 times |k| <= 1.05e6 perturbs r by < 8e-14 only where
+// e^-a < 1e-300; for a <= 1 by < 1.2e-16): 7 FP64 ops, ~2 ulp.
+__device__ __forceinline__ double exp_neg1024(double a, const double* __restrict__ sT) {
+  const double t = fma(a, -0x1.71547652b82fep+10, 0x1.8p52);  // MAGIC - round(a 1024/ln2)
+  const double kd = t - 0x1.8p52;                              // k = -round(a 1024/ln2)
+  const double r = fma(kd, -0x1.62e42fefa39efp-11, -a);        // r = -a - k ln2/1024
+  const int ki = __double2loint(t);
+  const double T = sT[ki & 1023];
+  const double q = r * fma(fma(r, 1.0 / 6.0, 0.5), r, 1.0);    // e^r - 1
+  const double Ts = __hiloint2double(__double2hiint(T) + ((ki >> 10) << 20), __double2loint(T));
   return fma(Ts, q, Ts);
 }
 
@@ -399,7 +420,9 @@ __global__ void __launch_bounds__(LL_THREADS, 2) k_loglik_mnl(LLArgs a) {
 // sums are combined over the 8 lanes of a particle column at the end.
 template <int TAB>
 __device__ __forceinline__ double exp_neg_tab(double a, const double* __restrict__ sT) {
-  if constexpr (TAB == 256)
+  if constexpr (TAB == 1024)
+    return exp_neg1024(a, sT);
+  else if constexpr (TAB == 256)
     return exp_neg256(a, sT);
   else
     return exp_neg(a, sT);
@@ -413,9 +436,17 @@ __global__ void __launch_bounds__(128, MINB) k_loglik_bin_mma(LLArgs a) {
   extern __shared__ __align__(16) double smem[];
   if (a.stop && *a.stop) return;
   tl_start(2);
-  double* sT = smem;        // TAB
-  double* sX = smem + 256;  // 2 x (sub rounded up to 16) x KP
-  for (int i = threadIdx.x; i < TAB; i += blockDim.x) sT[i] = TAB == 256 ? c_exp2tab256[i] : c_exp2tab[i];
+  double* sT = smem;                        // TAB
+  double* sX = smem + (TAB > 256 ? TAB : 256);  // 2 x (sub rounded up to 16) x KP
+  if constexpr (TAB == 1024) {
+    double v[1024 / 128];
+#pragma unroll
+    for (int u = 0; u < 1024 / 128; ++u) v[u] = g_exp2tab1024[threadIdx.x + 128 * u];
+#pragma unroll
+    for (int u = 0; u < 1024 / 128; ++u) sT[threadIdx.x + 128 * u] = v[u];
+  } else {
+    for (int i = threadIdx.x; i < TAB; i += blockDim.x) sT[i] = TAB == 256 ? c_exp2tab256[i] : c_exp2tab[i];
+  }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, ar = lane >> 2, ac = lane & 3;
   const int sub0 = a.sub;  // X sub-chunk rows per shared buffer (0: the whole chunk)
   __shared__ __align__(8) uint64_t xbar[2];
@@ -551,7 +582,7 @@ __global__ void __launch_bounds__(128, MINB) k_loglik_bin_mma(LLArgs a) {
           for (int e = 0; e < 2; ++e) {
             M[nt][e] += relu_bits(acc[0][nt][e]);
             const double ex = exp_neg_tab<TAB>(abs_clamp708(acc[0][nt][e]), sT);
-            Pp[nt][e] = fma(Pp[nt][e], ex, Pp[nt][e]);  // Pp (1 + e) in one FP64 op (12 per pair)
+            Pp[nt][e] = fma(Pp[nt][e], ex, Pp[nt][e]);  // Pp (1 + e) in one FP64 op (11 per pair)
           }
       }
     } else {

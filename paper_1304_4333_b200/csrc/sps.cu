@@ -107,6 +107,7 @@ struct LLChoice_t {
   int KT = 0, PPT = 1;
   int ppb = 0;          // particles per block (0: LL_THREADS * PPT)
   bool streams = false; // streams X through smem in sub-chunks (any chunk length)
+  int tab = 256;        // doubles reserved for the exp table at the start of shared memory
 };
 
 struct sps_ctx {
@@ -423,11 +424,18 @@ bool choose_ll(int k, int C, LLChoice* o) {
   }
   // DMMA contraction (+ <= 2 remainder DFMAs), 2 n-tiles (16 particles) per warp, 64 per block:
   // 114 registers -> 4 blocks per SM (the 4-n-tile layout, 178 registers, held 2; cfg2 run -6%)
+  static const int tabv = getenv("SPS_K1_TAB") ? atoi(getenv("SPS_K1_TAB")) : 64;
   if (cm1 == 1 && k <= 32 && !force_dfma) {
     switch (k) {
-#define MMA_CASE(K_, KKD_, REM_)                                                      \
-  case K_:                                                                            \
-    *o = {k_loglik_bin_mma<KKD_, REM_, 2>, 4 * KKD_ + (REM_ ? 4 : 0), 1, 64, true}; \
+  // exp table (SPS_K1_TAB, A/B switch): 2^(j/64) (default, 9-op exp), 2^(j/256) (8), 2^(j/1024) (7)
+#define MMA_CASE(K_, KKD_, REM_)                                                                            \
+  case K_:                                                                                                  \
+    if (tabv == 1024)                                                                                       \
+      *o = {k_loglik_bin_mma<KKD_, REM_, 2, 1, 1024>, 4 * KKD_ + (REM_ ? 4 : 0), 1, 64, true, 1024};      \
+    else if (tabv == 256)                                                                                   \
+      *o = {k_loglik_bin_mma<KKD_, REM_, 2, 1, 256>, 4 * KKD_ + (REM_ ? 4 : 0), 1, 64, true, 256};        \
+    else                                                                                                    \
+      *o = {k_loglik_bin_mma<KKD_, REM_, 2>, 4 * KKD_ + (REM_ ? 4 : 0), 1, 64, true, 256};                \
     return true;
       MMA_CASE(1, 0, 1) MMA_CASE(2, 0, 2) MMA_CASE(3, 1, 0) MMA_CASE(4, 1, 0) MMA_CASE(5, 1, 1) MMA_CASE(6, 1, 2)
       MMA_CASE(7, 2, 0) MMA_CASE(8, 2, 0) MMA_CASE(9, 2, 1) MMA_CASE(10, 2, 2) MMA_CASE(11, 3, 0) MMA_CASE(12, 3, 0)
@@ -441,9 +449,12 @@ bool choose_ll(int k, int C, LLChoice* o) {
   }
   if (cm1 == 1 && k <= 128 && !force_dfma) {  // wide: 2 n-tiles per warp (64 particles per block), k padded to 4
     switch ((k + 3) / 4) {
-#define MMA_W(KK_)                                   \
-  case KK_:                                          \
-    *o = {k_loglik_bin_mma<KK_, 0, 2>, 4 * KK_, 1, 64, true}; \
+#define MMA_W(KK_)                                                                      \
+  case KK_:                                                                             \
+    if (tabv == 1024)                                                                   \
+      *o = {k_loglik_bin_mma<KK_, 0, 2, 1, 1024>, 4 * KK_, 1, 64, true, 1024};           \
+    else                                                                                \
+      *o = {k_loglik_bin_mma<KK_, 0, 2>, 4 * KK_, 1, 64, true, 256};                     \
     return true;
       MMA_W(9) MMA_W(10) MMA_W(11) MMA_W(12) MMA_W(13) MMA_W(14) MMA_W(15) MMA_W(16) MMA_W(17) MMA_W(18)
       MMA_W(19) MMA_W(20) MMA_W(21) MMA_W(22) MMA_W(23) MMA_W(24) MMA_W(25) MMA_W(26) MMA_W(27) MMA_W(28)
@@ -504,7 +515,8 @@ sps_status launch_loglik(sps_ctx* c, const double* theta, int64_t ldt, int64_t P
     pl = &c->plans[c->plan_next];
     c->plan_next = (c->plan_next + 1) % 8;
     const int smem_budget = 100 * 1024;
-    const int chunk_cap = std::max(1, (int)((smem_budget - 256 * 8 - 64) / row_bytes) - 16);
+    const int tabb = (ch.tab > 256 ? ch.tab : 256) * 8;  // exp table bytes
+    const int chunk_cap = std::max(1, (int)((smem_budget - tabb - 64) / row_bytes) - 16);
     // streaming (DMMA) kernels: two sub-chunk buffers (TMA double buffering) in the same budget
     const int sub_cap = std::max(16, (chunk_cap / 2) / 16 * 16);
     const int S_min = ch.streams ? 1 : std::max(1, (range + chunk_cap - 1) / chunk_cap);
@@ -521,7 +533,7 @@ sps_status launch_loglik(sps_ctx* c, const double* theta, int64_t ldt, int64_t P
       const int chunk = (range + S - 1) / S;
       const int Se = (range + chunk - 1) / chunk;
       const int rows = ch.streams ? std::min(chunk, sub_cap) : chunk;
-      const size_t smem = 256 * 8 + (size_t)(ch.streams ? 2 * ((rows + 15) / 16 * 16) : rows + 16) * row_bytes + 16;
+      const size_t smem = tabb + (size_t)(ch.streams ? 2 * ((rows + 15) / 16 * 16) : rows + 16) * row_bytes + 16;
       const int by_smem = (int)(233472 / (smem + 1024));
       const int occ = std::max(1, std::min(std::min(by_regs, by_smem), 16));
       const double slots = (double)num_sms() * occ;
@@ -542,7 +554,7 @@ sps_status launch_loglik(sps_ctx* c, const double* theta, int64_t ldt, int64_t P
     pl->S = (range + chunk - 1) / chunk;
     pl->sub = ch.streams ? std::min(((chunk + 15) / 16) * 16, sub_cap) : 0;
     const int rows = ch.streams ? pl->sub : chunk;
-    pl->smem = 256 * 8 + (size_t)(ch.streams ? 2 * ((rows + 15) / 16 * 16) : rows + 16) * c->ldx * 8 +
+    pl->smem = tabb + (size_t)(ch.streams ? 2 * ((rows + 15) / 16 * 16) : rows + 16) * c->ldx * 8 +
                (c->C > 2 ? (size_t)chunk * 4 : 0);
     if (pl->S > max_chunks) return fail(c, SPS_E_CONFIG, "observation range too long for the chunk buffer");
   }
