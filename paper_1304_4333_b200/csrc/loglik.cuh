@@ -177,26 +177,6 @@ __device__ __forceinline__ double exp_neg256(double a, const double* __restrict_
   return fma(Ts, q, Ts);
 }
 
-// 2^(j/1024), j = 0..1023 (global; staged into shared memory by K1's prologue)
-__device__ const double g_exp2tab1024[1024] = {
-#include "exp2tab1024.inc"
-};
-
-// e^-a for 0 <= a <= 708 with the 2^(j/1024) table (sT in smem): |r| <= ln2/2048, degree-3
-// polynomial (truncation r^4/24 <= 5.5e-16 relative), range reduction by ONE fma with ln2/1024
-// rounded to double (its error 7.5e-20 times |k| <= 1.05e6 perturbs r by < 8e-14 only where
-// e^-a < 1e-300; for a <= 1 by < 1.2e-16): 7 FP64 ops, ~2 ulp.
-__device__ __forceinline__ double exp_neg1024(double a, const double* __restrict__ sT) {
-  const double t = fma(a, -0x1.71547652b82fep+10, 0x1.8p52);  // MAGIC - round(a 1024/ln2)
-  const double kd = t - 0x1.8p52;                              // k = -round(a 1024/ln2)
-  const double r = fma(kd, -0x1.62e42fefa39efp-11, -a);        // r = -a - k ln2/1024
-  const int ki = __double2loint(t);
-  const double T = sT[ki & 1023];
-  const double q = r * fma(fma(r, 1.0 / 6.0, 0.5), r, 1.0);    // e^r - 1
-  const double Ts = __hiloint2double(__double2hiint(T) + ((ki >> 10) << 20), __double2loint(T));
-  return fma(Ts, q, Ts);
-}
-
 // Split a positive running product into mantissa in [1,2) and exponent count.
 __device__ __forceinline__ void renorm(double& Pp, int& E) {
   const int hi = __double2hiint(Pp);
@@ -420,9 +400,7 @@ __global__ void __launch_bounds__(LL_THREADS, 2) k_loglik_mnl(LLArgs a) {
 // sums are combined over the 8 lanes of a particle column at the end.
 template <int TAB>
 __device__ __forceinline__ double exp_neg_tab(double a, const double* __restrict__ sT) {
-  if constexpr (TAB == 1024)
-    return exp_neg1024(a, sT);
-  else if constexpr (TAB == 256)
+  if constexpr (TAB == 256)
     return exp_neg256(a, sT);
   else
     return exp_neg(a, sT);
@@ -436,17 +414,9 @@ __global__ void __launch_bounds__(128, MINB) k_loglik_bin_mma(LLArgs a) {
   extern __shared__ __align__(16) double smem[];
   if (a.stop && *a.stop) return;
   tl_start(2);
-  double* sT = smem;                        // TAB
-  double* sX = smem + (TAB > 256 ? TAB : 256);  // 2 x (sub rounded up to 16) x KP
-  if constexpr (TAB == 1024) {
-    double v[1024 / 128];
-#pragma unroll
-    for (int u = 0; u < 1024 / 128; ++u) v[u] = g_exp2tab1024[threadIdx.x + 128 * u];
-#pragma unroll
-    for (int u = 0; u < 1024 / 128; ++u) sT[threadIdx.x + 128 * u] = v[u];
-  } else {
-    for (int i = threadIdx.x; i < TAB; i += blockDim.x) sT[i] = TAB == 256 ? c_exp2tab256[i] : c_exp2tab[i];
-  }
+  double* sT = smem;        // TAB
+  double* sX = smem + 256;  // 2 x (sub rounded up to 16) x KP
+  for (int i = threadIdx.x; i < TAB; i += blockDim.x) sT[i] = TAB == 256 ? c_exp2tab256[i] : c_exp2tab[i];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, ar = lane >> 2, ac = lane & 3;
   const int sub0 = a.sub;  // X sub-chunk rows per shared buffer (0: the whole chunk)
   __shared__ __align__(8) uint64_t xbar[2];

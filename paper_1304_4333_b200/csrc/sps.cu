@@ -427,12 +427,11 @@ bool choose_ll(int k, int C, LLChoice* o) {
   static const int tabv = getenv("SPS_K1_TAB") ? atoi(getenv("SPS_K1_TAB")) : 64;
   if (cm1 == 1 && k <= 32 && !force_dfma) {
     switch (k) {
-  // exp table (SPS_K1_TAB, A/B switch): 2^(j/64) (default, 9-op exp), 2^(j/256) (8), 2^(j/1024) (7)
+  // exp table (SPS_K1_TAB, A/B switch): 2^(j/64) (default, 9-op exp) or 2^(j/256) (8 ops, 1% slower:
+  // bank conflicts); 2^(j/1024) (7 ops) and an fp32 second-order term (5 FP64 ops) measured 10% slower
 #define MMA_CASE(K_, KKD_, REM_)                                                                            \
   case K_:                                                                                                  \
-    if (tabv == 1024)                                                                                       \
-      *o = {k_loglik_bin_mma<KKD_, REM_, 2, 1, 1024>, 4 * KKD_ + (REM_ ? 4 : 0), 1, 64, true, 1024};      \
-    else if (tabv == 256)                                                                                   \
+    if (tabv == 256)                                                                                        \
       *o = {k_loglik_bin_mma<KKD_, REM_, 2, 1, 256>, 4 * KKD_ + (REM_ ? 4 : 0), 1, 64, true, 256};        \
     else                                                                                                    \
       *o = {k_loglik_bin_mma<KKD_, REM_, 2>, 4 * KKD_ + (REM_ ? 4 : 0), 1, 64, true, 256};                \
@@ -451,10 +450,7 @@ bool choose_ll(int k, int C, LLChoice* o) {
     switch ((k + 3) / 4) {
 #define MMA_W(KK_)                                                                      \
   case KK_:                                                                             \
-    if (tabv == 1024)                                                                   \
-      *o = {k_loglik_bin_mma<KK_, 0, 2, 1, 1024>, 4 * KK_, 1, 64, true, 1024};           \
-    else                                                                                \
-      *o = {k_loglik_bin_mma<KK_, 0, 2>, 4 * KK_, 1, 64, true, 256};                     \
+    *o = {k_loglik_bin_mma<KK_, 0, 2>, 4 * KK_, 1, 64, true, 256};                       \
     return true;
       MMA_W(9) MMA_W(10) MMA_W(11) MMA_W(12) MMA_W(13) MMA_W(14) MMA_W(15) MMA_W(16) MMA_W(17) MMA_W(18)
       MMA_W(19) MMA_W(20) MMA_W(21) MMA_W(22) MMA_W(23) MMA_W(24) MMA_W(25) MMA_W(26) MMA_W(27) MMA_W(28)
