@@ -90,6 +90,9 @@ typedef struct sps_report {
   int32_t n_report;
   const double* report_fns;
   double *mean, *sd, *nse, *rne; /* PAPER.md:160-223 with NSE = [(JN)^-1 vhat]^1/2 (R2)     */
+  /* caller-owned, capacity n, may be NULL: log predictive likelihoods log p(y_s | y_{1:s-1}),
+   * s = 1..T (data tempering; see sps_predictive)                                          */
+  double* logpl;
 } sps_report;
 
 typedef struct sps_ctx sps_ctx;
@@ -159,6 +162,15 @@ sps_status sps_get_particles(sps_ctx* ctx, double* theta_host, double* L_host, d
  * caller repeat runs (e.g. independent runs A, B, C)
  * without re-uploading data.  Collective. */
 sps_status sps_reset(sps_ctx* ctx, uint64_t seed, int32_t pass);
+
+/* Log predictive likelihoods (R18), a
+ * by-product of the data-tempering C phase: out[s - s0] = log p(y_{s+1} | y_{1:s})
+ * for 0-based observations s0 <= s < s1, each the log ratio of the pooled weight
+ * sums after and before absorbing the observation, over the particles of the
+ * cycle that absorbed it.  Sum over a cycle = its log-ML increment; sum over all
+ * T = log ML.  out: host, s1 - s0 doubles.  Errors: SPS_E_STATE (power tempering,
+ * or s1 > observations absorbed so far), SPS_E_CONFIG. */
+sps_status sps_predictive(sps_ctx* ctx, int32_t s0, int32_t s1, double* out);
 
 /* ---- Algorithm 3: two passes --------------------------
  * Pass 1 runs Algorithm 2 and records its design: the cycle break points t_l

@@ -58,6 +58,7 @@ class Report(C.Structure):
         ("min_rne", C.POINTER(C.c_double)), ("h_cycle", C.POINTER(C.c_int32)),
         ("mean", C.POINTER(C.c_double)), ("sd", C.POINTER(C.c_double)),
         ("nse", C.POINTER(C.c_double)), ("rne", C.POINTER(C.c_double)),
+        ("logpl", C.POINTER(C.c_double)),
     ]
 
 
@@ -292,7 +293,8 @@ def default_report(X, C_):
 
 def run(X, y, C_, J, N, seed, prior_mean, prior_cov, monitors=None, report_fns=None, max_cycles=None,
         return_theta=False, replay=None, record_sigma=False, **kw):
-    """Algorithm 2 (one pass).  replay: dict(t_cycle, phi_cycle, R_cycle, sigma) of a pass-1 run ->
+    """Algorithm 2 (one pass); data tempering also returns the log predictive likelihoods
+    out["logpl"][s-1] = log p(y_s | y_{1:s-1}).  replay: dict(t_cycle, phi_cycle, R_cycle, sigma) of a pass-1 run ->
     Algorithm 3 step 2 with that fixed design (pass tag kw `pass_`); record_sigma: return the
     proposal variances Sigma_lr actually used (out["sigma"], M steps x d x d)."""
     X, Xp = _d(X)
@@ -311,7 +313,8 @@ def run(X, y, C_, J, N, seed, prior_mean, prior_cov, monitors=None, report_fns=N
                 R_cycle=np.zeros(max_cycles, np.int32), logml_inc=np.zeros(max_cycles),
                 min_rne=np.zeros(max_cycles), h_cycle=np.zeros(max_cycles, np.int32),
                 mean=np.zeros(report_fns.shape[0]), sd=np.zeros(report_fns.shape[0]),
-                nse=np.zeros(report_fns.shape[0]), rne=np.zeros(report_fns.shape[0]))
+                nse=np.zeros(report_fns.shape[0]), rne=np.zeros(report_fns.shape[0]),
+                logpl=np.full(n, np.nan))
     rep = Report()
     for key, a in arrs.items():
         ct = C.c_int32 if a.dtype == np.int32 else C.c_double
@@ -345,6 +348,8 @@ def run(X, y, C_, J, N, seed, prior_mean, prior_cov, monitors=None, report_fns=N
                R_cycle=arrs["R_cycle"][:L].copy(), logml_inc=arrs["logml_inc"][:L].copy(),
                min_rne=arrs["min_rne"][:L].copy(), h_cycle=arrs["h_cycle"][:L].copy(),
                mean=arrs["mean"], sd=arrs["sd"], nse=arrs["nse"], rne=arrs["rne"])
+    if opts["tempering"] == DATA:  # log p(y_s | y_{1:s-1}), s = 1..T (R18)
+        out["logpl"] = arrs["logpl"]
     if return_theta:
         out["theta"] = theta
     if record_sigma:

@@ -588,6 +588,8 @@ int32_t or_run2(const or_config* cfg, const double* X, const int32_t* y, const d
        * end rule of PAPER.md:392-402: first s with ESS(s)/(JN) < 0.5, or T. */
       for (int64_t p = 0; p < P; ++p) lw[p] = 0.0;
       int32_t s = t;
+      /* log sum_jn w_jn^(s-1): the weights are all 1 after the S phase of the last cycle */
+      double lse_prev = log((double)P);
       for (;;) {
         s = s + 1;
         int32_t obs = s - 1;
@@ -610,6 +612,13 @@ int32_t or_run2(const or_config* cfg, const double* X, const int32_t* y, const d
           double w = exp(lw[p] - m);
           s1 += w;
           s2 += w * w;
+        }
+        /* log predictive likelihood of y_s (R18): the ratio of the weight
+         * sums after and before absorbing observation s, w^(s) = w^(s-1) p(y_s | theta) */
+        {
+          const double lse = m + log(s1);
+          if (rep->logpl) rep->logpl[obs] = lse - lse_prev;
+          lse_prev = lse;
         }
         if (replay ? s == replay->t_cycle[ell - 1]
                    : (s1 * s1 < cfg->ess_frac * (double)P * s2 || s == n))

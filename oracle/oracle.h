@@ -69,6 +69,11 @@ typedef struct {
   double* sd;
   double* nse;
   double* rne;
+  /* caller-owned, capacity n, or NULL: log predictive likelihoods (data tempering)
+   * logpl[s-1] = log p(y_s | y_{1:s-1}) = log[sum_jn w_jn^(s-1) p(y_s | theta_jn) /
+   * sum_jn w_jn^(s-1)] over the particles of the cycle that absorbs s (PAPER.md:532-535,
+   * 1413-1416; R18) */
+  double* logpl;
 } or_report;
 
 /* ---- random numbers ---------------------- */

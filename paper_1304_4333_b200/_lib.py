@@ -68,7 +68,7 @@ EXPORTED = [
     "sps_moments", "sps_get_particles", "sps_shard", "sps_destroy", "sps_last_error", "sps_nccl_unique_id",
     "sps_g_prior", "sps_test_philox", "sps_test_normals", "sps_test_portable", "sps_test_resample_int",
     "sps_test_resample_group", "sps_test_accept", "sps_reset", "sps_set_profiling", "sps_get_counters", "sps_sync", "sps_loopback_unique_id",
-    "sps_record_sigma", "sps_get_sigma", "sps_set_design",
+    "sps_record_sigma", "sps_get_sigma", "sps_set_design", "sps_predictive",
 ]
 
 
@@ -102,6 +102,7 @@ class Report(C.Structure):
         ("n_report", C.c_int32), ("report_fns", C.POINTER(C.c_double)),
         ("mean", C.POINTER(C.c_double)), ("sd", C.POINTER(C.c_double)),
         ("nse", C.POINTER(C.c_double)), ("rne", C.POINTER(C.c_double)),
+        ("logpl", C.POINTER(C.c_double)),
     ]
 
 
@@ -138,6 +139,7 @@ def _declare(L):
         "sps_record_sigma": ([vp, C.c_int32], st),
         "sps_get_sigma": ([vp, C.c_int64, C.c_int64, dp], st),
         "sps_set_design": ([vp, C.c_int32, ip, dp, ip, dp], st),
+        "sps_predictive": ([vp, C.c_int32, C.c_int32, dp], st),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

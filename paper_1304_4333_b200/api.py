@@ -121,7 +121,8 @@ class Sps:
         nrep = (self.C - 1) if report_fns is None else np.asarray(report_fns).shape[0]
         arrs = dict(t_cycle=np.zeros(cap, np.int32), phi_cycle=np.zeros(cap), R_cycle=np.zeros(cap, np.int32),
                     logml_inc=np.zeros(cap), min_rne=np.zeros(cap), h_cycle=np.zeros(cap, np.int32),
-                    mean=np.zeros(nrep), sd=np.zeros(nrep), nse=np.zeros(nrep), rne=np.zeros(nrep))
+                    mean=np.zeros(nrep), sd=np.zeros(nrep), nse=np.zeros(nrep), rne=np.zeros(nrep),
+                    logpl=np.full(self.n, np.nan))
         rep = Report()
         rep.cap_cycles = cap
         rep.n_report = nrep
@@ -141,6 +142,15 @@ class Sps:
             out[key] = arrs[key][:L].copy()
         for key in ("mean", "sd", "nse", "rne"):
             out[key] = arrs[key]
+        if self.cfg.tempering == DATA:
+            out["logpl"] = arrs["logpl"]
+        return out
+
+    def predictive(self, s0=0, s1=None):
+        """sps_predictive: log p(y_{s+1} | y_{1:s}) for 0-based s in [s0, s1) (data tempering)."""
+        s1 = self.n if s1 is None else s1
+        out = np.zeros(max(s1 - s0, 0))
+        _check(lib().sps_predictive(self.ctx, int(s0), int(s1), _dptr(out)), self.ctx)
         return out
 
     def reset(self, seed, pass_=0):

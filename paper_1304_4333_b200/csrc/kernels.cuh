@@ -356,9 +356,13 @@ __global__ void k_ess_rank(const double* __restrict__ parts, int ntiles, int B, 
 }
 
 // K3 (Algorithm 2 step 1; R3, R4): combine ranks in rank order;
-// s* = first s in the chunk with S1^2 < ess_frac P S2, or s == n (ends the cycle).
+// s* = first s in the chunk with S1^2 < ess_frac P S2, or s == n (ends the cycle);
+// with t_fix >= 0 (fixed schedule) s* = t_fix.  Also the log predictive likelihood of
+// every absorbed observation (R18): lse[s] = log sum_p w_p^(s) =
+// M + log S1, logpl[s-1] = lse[s] - lse[s-1], with lse[t_start] = log P (the weights
+// are all 1 after the last S phase).
 __global__ void k_ess_final(const double* __restrict__ gath, int G, int B, int s0, int n, double ess_frac, double P,
-                            Ctl* ctl) {
+                            Ctl* ctl, int t_fix, int t_start, double* __restrict__ lse, double* __restrict__ logpl) {
   if (threadIdx.x != 0) return;
   ctl->s_star = -1;
   for (int b = 0; b < B; ++b) {
@@ -368,7 +372,12 @@ __global__ void k_ess_final(const double* __restrict__ gath, int G, int B, int s
       combine3(M, S1, S2, o[0], o[1], o[2]);
     }
     const int s = s0 + b + 1;
-    if (S1 * S1 < ess_frac * P * S2 || s == n) {
+    if (lse) {
+      const double l = M + log(S1);
+      logpl[s - 1] = l - (s - 1 == t_start ? log(P) : lse[s - 1]);
+      lse[s] = l;
+    }
+    if (t_fix >= 0 ? s == t_fix : (S1 * S1 < ess_frac * P * S2 || s == n)) {
       ctl->s_star = s;
       ctl->ess = S1 * S1 / S2;
       return;

@@ -129,6 +129,7 @@ struct sps_ctx {
   double *gpart = nullptr, *mpart = nullptr, *slice = nullptr, *gath = nullptr;
   double *shift = nullptr, *Lprop = nullptr, *V = nullptr, *rne = nullptr;
   double *lwbuf = nullptr, *essparts = nullptr, *essslice = nullptr, *essgath = nullptr;
+  double *lse = nullptr, *logpl = nullptr;  // data tempering: log weight sums (n + 1), log predictives (n)
   double *grp_ms = nullptr, *grp_ms_gath = nullptr, *Lj = nullptr, *Lj_gath = nullptr, *scal = nullptr;
   double *pw_parts = nullptr, *pw_slice = nullptr, *pw_gath = nullptr, *mx_parts = nullptr, *mx_slice = nullptr,
          *mx_gath = nullptr;
@@ -906,7 +907,7 @@ void free_ctx(sps_ctx* c) {
   lap("graphs/ev");
   void* ptrs[] = {c->X, c->Xs, c->mu, c->Lprior, c->xbar, c->mon, c->y, c->theta, c->theta2, c->L, c->L2, c->lp,
                   c->lp2, c->lw, c->lw_cur, c->theta_s, c->lp_s, c->part, c->gpart, c->mpart, c->slice, c->gath,
-                  c->shift, c->Lprop, c->V, c->rne, c->lwbuf, c->essparts, c->essslice, c->essgath, c->grp_ms,
+                  c->shift, c->Lprop, c->V, c->rne, c->lwbuf, c->essparts, c->essslice, c->essgath, c->lse, c->logpl, c->grp_ms,
                   c->grp_ms_gath, c->Lj, c->Lj_gath, c->scal, c->pw_parts, c->pw_slice, c->pw_gath, c->mx_parts,
                   c->mx_slice, c->mx_gath, c->fn_A, c->fn_out, c->ll_scratch, c->Sinv, c->LpriorP, c->SinvP, c->Rp, c->RpP, c->bpart, c->ctl, c->inc_dev,
                   c->sig_rec, c->sig_in};
@@ -1164,6 +1165,10 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
   TRY(dalloc(c, &c->essslice, (size_t)c->Bmax * 3));
   TRY(dalloc(c, &c->grp_ms, (size_t)c->Jl * 2));
   TRY(dalloc(c, &c->inc_dev, (size_t)c->inc_cap));
+  if (cfg.tempering == SPS_DATA_TEMPERING) {
+    TRY(dalloc(c, &c->lse, (size_t)c->n + 1));
+    TRY(dalloc(c, &c->logpl, (size_t)c->n));
+  }
   TRY(dalloc(c, &c->Lj, (size_t)c->Jl));
   if (c->G > 1) {
     TRY(dalloc(c, &c->essgath, (size_t)c->Bmax * 3 * c->G));
@@ -1487,18 +1492,21 @@ sps_status sps_cphase(sps_ctx* c, int32_t t_target, double phi_target, int32_t* 
           c->Xs, c->y, c->ldx, c->k, c->C, c->theta, c->d, Pl, s, Be, c->lw_cur, c->lwbuf);
       CHECK_LAUNCH(c);
       c->pairs += P * Be;
+      // pooled (M, S1, S2) per observation: the ESS rule (adaptive) and the log predictive
+      // likelihoods (both modes; with a fixed target the crossing is known on the host)
+      k_ess_partials<<<dim3((unsigned)ntiles, (unsigned)Be), 256, 0, c->stream>>>(c->lwbuf, Pl, ESS_TILE,
+                                                                                 c->essparts);
+      CHECK_LAUNCH(c);
+      k_ess_rank<<<1, 256, 0, c->stream>>>(c->essparts, ntiles, Be, c->essslice);
+      CHECK_LAUNCH(c);
+      TRY(gather(c, c->essslice, c->essgath, (size_t)Be * 3));
+      k_ess_final<<<1, 32, 0, c->stream>>>(c->essgath, c->G, Be, s, c->n, c->cfg.ess_frac, P, c->ctl,
+                                           t_target >= 0 ? t_target : -1, c->t, c->lse, c->logpl);
+      CHECK_LAUNCH(c);
       int sstar = -1;
       if (t_target >= 0) {
         if (s + Be == t_target) sstar = t_target;
       } else {
-        k_ess_partials<<<dim3((unsigned)ntiles, (unsigned)Be), 256, 0, c->stream>>>(c->lwbuf, Pl, ESS_TILE,
-                                                                                   c->essparts);
-        CHECK_LAUNCH(c);
-        k_ess_rank<<<1, 256, 0, c->stream>>>(c->essparts, ntiles, Be, c->essslice);
-        CHECK_LAUNCH(c);
-        TRY(gather(c, c->essslice, c->essgath, (size_t)Be * 3));
-        k_ess_final<<<1, 32, 0, c->stream>>>(c->essgath, c->G, Be, s, c->n, c->cfg.ess_frac, P, c->ctl);
-        CHECK_LAUNCH(c);
         TRY(read_ctl(c));
         sstar = c->hctl->s_star;
       }
@@ -2045,6 +2053,7 @@ sps_status sps_run(sps_ctx* c, sps_report* rep) {
   }
   if (st != SPS_OK) return st;
   TRY(sps_logml(c, &rep->logml, &rep->logml_nse));
+  if (rep->logpl && c->cfg.tempering == SPS_DATA_TEMPERING) TRY(sps_predictive(c, 0, c->t, rep->logpl));
   if (rep->n_report > 0) {
     std::vector<double> A;
     const double* fns = rep->report_fns;
@@ -2060,6 +2069,18 @@ sps_status sps_run(sps_ctx* c, sps_report* rep) {
     }
     TRY(sps_moments(c, rep->n_report, fns, rep->mean, rep->sd, rep->nse, rep->rne));
   }
+  return SPS_OK;
+}
+
+sps_status sps_predictive(sps_ctx* c, int32_t s0, int32_t s1, double* out) {
+  if (!c || s0 < 0 || s1 < s0 || (s1 > s0 && !out)) return SPS_E_CONFIG;
+  if (c->cfg.tempering != SPS_DATA_TEMPERING)
+    return fail(c, SPS_E_STATE, "sps_predictive: log predictive likelihoods need data tempering");
+  if (s1 > c->t) return fail(c, SPS_E_STATE, "sps_predictive: observations [%d, %d) not absorbed yet (t = %d)", s0, s1, c->t);
+  if (s1 == s0) return SPS_OK;
+  CU(c, cudaSetDevice(c->cfg.device));
+  CU(c, cudaMemcpyAsync(out, c->logpl + s0, sizeof(double) * (s1 - s0), cudaMemcpyDeviceToHost, c->stream));
+  CU(c, cudaStreamSynchronize(c->stream));
   return SPS_OK;
 }
 

@@ -190,6 +190,8 @@ def _compare_runs(g, o):
     assert np.all(np.abs(g["sd"] - o["sd"]) <= 1e-6)
     assert abs(g["logml_nse"] - o["logml_nse"]) <= 1e-6
     assert np.all(np.abs(g["nse"] - o["nse"]) <= 1e-6)
+    if "logpl" in o:  # log predictive likelihoods (data tempering, R18)
+        assert np.all(np.abs(g["logpl"] - o["logpl"]) <= 1e-9)
 
 
 @pytest.mark.parametrize("tempering", [0, 1])
@@ -245,3 +247,23 @@ def test_g_prior_and_moments_match_oracle(sps, orc):
     Lp = orc.cholesky(cov)
     z = orc.normals(1 if False else 8, 5, 0, orc.TAG_INIT, 4)
     assert np.allclose(th[5], Lp @ z, rtol=1e-14, atol=1e-15)
+
+
+def test_predictive_api(sps, orc):
+    """sps_predictive between cycles: the absorbed prefix matches the oracle's full-run values
+    (same streams), the rest is refused until absorbed; power tempering has none."""
+    X, y = sps_synth.config_data("cfg1")
+    cov = orc.g_prior(X, 2, 0.25)
+    o = orc.run(X, y, 2, 4, 128, seed=1, prior_mean=np.zeros(4), prior_cov=cov)
+    s = sps.Sps(X, y, np.zeros(4), cov, J=4, N=128, seed=1)
+    t, _, inc = s.cphase()
+    got = s.predictive(0, t)
+    assert np.all(np.abs(got - o["logpl"][:t]) <= 1e-9)
+    assert abs(got.sum() - inc) <= 1e-10
+    with pytest.raises(sps.SpsError):
+        s.predictive(0, t + 1)
+    s.close()
+    s = sps.Sps(X, y, np.zeros(4), cov, J=4, N=128, seed=1, tempering=1)
+    with pytest.raises(sps.SpsError):
+        s.predictive(0, 1)
+    s.close()

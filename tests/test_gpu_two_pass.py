@@ -39,6 +39,8 @@ def _compare(g, o):
     assert abs(g["logml_nse"] - o["logml_nse"]) <= 1e-6
     for key in ("mean", "sd", "nse"):
         assert np.all(np.abs(g[key] - o[key]) <= 1e-6), key
+    if "logpl" in o:
+        assert np.all(np.abs(g["logpl"] - o["logpl"]) <= 1e-9)
 
 
 def _sigma_close(a, b):

@@ -147,3 +147,47 @@ def test_two_pass_sigma_is_the_pass1_proposal(orc):
         assert np.allclose(S, S.T) and np.all(np.linalg.eigvalsh(S) > 0)
     again = orc.run(X, y, 2, 4, 128, seed=3, prior_mean=np.zeros(2), prior_cov=cov, replay=p1, return_theta=True)
     assert again["logml"] == p1["logml"] and np.array_equal(again["theta"], p1["theta"])
+
+
+# ---------------------------------------------------------------- log predictive likelihoods (R18)
+def test_predictive_flat_likelihood(orc):
+    """X = 0: p(y_s | theta) = 1/C for every theta, so every one-step-ahead predictive
+    probability is exactly 1/C whatever the weights."""
+    n, k, C = 25, 3, 3
+    X = np.zeros((n, k))
+    y = (np.arange(n) % C).astype(np.int32)
+    d = k * (C - 1)
+    r = orc.run(X, y, C, 4, 64, seed=2, prior_mean=np.zeros(d), prior_cov=np.eye(d), monitors=np.eye(d)[:2])
+    assert np.allclose(r["logpl"], math.log(1.0 / C), rtol=1e-13, atol=0)
+
+
+def test_predictive_chain_rule(orc):
+    """p(y_{1:T}) = prod_s p(y_s | y_{1:s-1}): the predictive log likelihoods add up to the log ML,
+    cycle by cycle (the cycle's increment) and in total."""
+    X, y = sps_synth.config_data("cfg1")
+    cov = orc.g_prior(X, 2, 0.25)
+    r = orc.run(X, y, 2, 4, 128, seed=5, prior_mean=np.zeros(4), prior_cov=cov)
+    lp = r["logpl"]
+    assert np.all(np.isfinite(lp)) and np.all(lp < 0)
+    assert lp.sum() == pytest.approx(r["logml"], abs=1e-10)
+    t0 = 0
+    for t, inc in zip(r["t_cycle"], r["logml_inc"]):
+        assert lp[t0:t].sum() == pytest.approx(inc, abs=1e-11)
+        t0 = t
+
+
+def test_predictive_quadrature_prefixes(orc):
+    """Cumulative predictive sum_{s<=t} log p(y_s|y_{1:s-1}) = log p(y_{1:t}): against the d=2
+    quadrature log ML of the first t observations, within 3 NSE in >= 8 of 10 seeds, at
+    t = 10, 20, 30 (the intermediate posteriors' particle representations)."""
+    X, y = _tiny_binary()
+    cov = orc.g_prior(X, 2, 0.25)
+    fn = X.mean(axis=0)[None, :]
+    ts = (10, 20, 30)
+    q = {t: quadrature.posterior(X[:t], y[:t], 2, np.zeros(2), cov, fn)[0] for t in ts}
+    ok = 0
+    for seed in range(1, 11):
+        r = orc.run(X, y, 2, 10, 400, seed=seed, prior_mean=np.zeros(2), prior_cov=cov)
+        cum = np.cumsum(r["logpl"])
+        ok += all(abs(cum[t - 1] - q[t]) <= 3 * r["logml_nse"] for t in ts)
+    assert ok >= 8, ok
