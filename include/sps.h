@@ -20,7 +20,7 @@
  *  - No CPU fallback: every computation runs in the library's CUDA kernels;
  *    without a CUDA device sps_create fails with SPS_E_CUDA.
  *
- * The readings R1..R17 cited below are listed in DESIGN.md.
+ * The readings R1..R18 cited below are listed in DESIGN.md.
  */
 #ifndef SPS_H
 #define SPS_H
