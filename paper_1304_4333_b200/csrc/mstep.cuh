@@ -999,9 +999,13 @@ __device__ void finalize_body(const FinArgs& f, double* sm) {
   if (f.mode == 1 && threadIdx.x == 0) tl_mark_any(17);
   // ---- V (R11) and the factorization input (h/100) V, identity-padded to D x D
   const double hd = (double)s_h / 100.0;
+  const double rPm1 = 1.0 / (P - 1.0);
   const int DA = d > 32 ? d : D;
   // Algorithm 3: Sigma of the step this factor serves, from / into the design record
-  const int64_t sstep = f.sig_step >= 0 ? f.sig_step : (int64_t)__ldcg(&f.ctl->step_cur) + 1;
+  // (the device step is read only when a record / design is attached: a global load here is on
+  // the M step's critical path)
+  const int64_t sstep = (!f.sig_in && !f.sig_rec) ? 0
+                        : f.sig_step >= 0 ? f.sig_step : (int64_t)__ldcg(&f.ctl->step_cur) + 1;
   const double* sig = (f.sig_in && sstep < f.sig_in_n) ? f.sig_in + sstep * dd : nullptr;
   double* srec = (f.sig_rec && sstep < f.sig_rec_cap) ? f.sig_rec + sstep * dd : nullptr;
 #pragma unroll 2
@@ -1011,7 +1015,7 @@ __device__ void finalize_body(const FinArgs& f, double* sm) {
     for (int l = lane; l < DA; l += 32) {
       if (i < d && l < d) {
         const double cl = sbar[l] - sshift[l];
-        const double v = (sM[i * d + l] - P * ci * cl) / (P - 1.0);
+        const double v = (sM[i * d + l] - P * ci * cl) * rPm1;  // / (JN - 1) (R11), as one multiply
         sV[i * d + l] = v;
         const double a = sig ? __ldcg(sig + i * d + l) : hd * v;  // Sigma_lr = (h/100) V_lr
         sA[i * ldc + l] = a;
@@ -1044,6 +1048,7 @@ __device__ void finalize_body(const FinArgs& f, double* sm) {
     if (lane == 0) {
       f.ctl->chol_ridge = ridge_used;
       if (!ok) f.ctl->err = ERR_NUMERIC;
+      if (f.mode == 1) tl_mark_any(15);  // (debug timeline: Cholesky done)
     }
   } else if (w > 0 && f.mode == 1) {  // monitor RNEs: warp per monitor, lanes over groups
 #pragma unroll 1
@@ -1081,6 +1086,7 @@ __device__ void finalize_body(const FinArgs& f, double* sm) {
       const double var = quad * (P - 1.0) / P;
       if (lane == 0) sg[f.nmon * J + m] = vhat > 0.0 ? var / vhat : INFINITY;
     }
+    if (threadIdx.x == 32 && f.mode == 1) tl_mark_any(21);  // (debug timeline: warp 1's RNEs done)
   }
   __syncthreads();
   if (f.trace && threadIdx.x == 0) f.trace[4] = gtimer();

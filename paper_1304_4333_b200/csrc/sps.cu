@@ -1385,7 +1385,7 @@ sps_status sps_get_counters(const sps_ctx* cc, sps_counters* out) {
                                "gap accept<-K1", "gap reduce<-accept", "gap fin<-reduce", "normals start-propose end",
                                "normals end-K1 end", "gap next propose<-fin", "step", "acc0 load", "acc0 decide",
                                "acc0 wb+dmma", "acc0 combine..end(all)", "fin stage", "fin theta-bar", "fin V",
-                               "fin chol|RNE", "fin stats", "fin tail"};
+                               "fin chol|RNE", "fin(chol only)", "fin(RNE w1 only)"};
     fprintf(stderr, "SPS_TIMELINE mean us over %d steps:", c->tl_rows);
     for (int q = 0; q < 24; ++q) fprintf(stderr, " %s=%.2f", nm[q], c->tl_acc[q] / c->tl_rows / 1e3);
     fprintf(stderr, "\n");
@@ -1659,8 +1659,8 @@ static sps_status timeline_accumulate(sps_ctx* c, int R) {
       c->tl_acc[19] += (double)t[17] - (double)t[16];
       c->tl_acc[20] += (double)t[18] - (double)t[17];
       c->tl_acc[21] += (double)t[19] - (double)t[18];
-      c->tl_acc[22] += (double)t[20] - (double)t[19];
-      c->tl_acc[23] += (double)t[11] - (double)t[20];
+      c->tl_acc[22] += t[15] ? (double)t[15] - (double)t[18] : 0.0;  // warp 0: Cholesky
+      c->tl_acc[23] += t[21] ? (double)t[21] - (double)t[18] : 0.0;  // warp 1: monitor RNEs
     }
     if (t[12] && t[13] && t[14]) {  // accept block 0: load / decide+writeback / dmma phases
       c->tl_acc[14] += (double)t[12] - (double)t[6];
