@@ -201,6 +201,7 @@ struct sps_ctx {
   double* inc_dev = nullptr;
   int inc_cap = 1024, inc_base = 0;
   int last_adv = 0;  // observations absorbed by the last data-tempering C phase (first galloping chunk)
+  int64_t pre_normals_step = -1;  // the first M step's normals were launched by the C phase (step number)
   // Algorithm 3: Sigma_lr record of pass 1, fixed design of pass 2
   bool recording = false;
   double* sig_rec = nullptr;     // d x d per global M step
@@ -419,9 +420,12 @@ bool choose_ll(int k, int C, LLChoice* o) {
   static const bool force_dfma = getenv("SPS_K1_DFMA") != nullptr;
   // tuning hook (tools/k1_variants.py): the previous 4-n-tile layout for k = 25
   static const char* k1var = getenv("SPS_K1_VAR");
-  if (k1var && cm1 == 1 && k == 25 && !strcmp(k1var, "w4")) {
-    *o = {k_loglik_bin_mma<6, 1, 4>, 28, 1, 128, true};
-    return true;
+  if (k1var && cm1 == 1 && k == 25) {
+    if (!strcmp(k1var, "w4")) *o = {k_loglik_bin_mma<6, 1, 4>, 28, 1, 128, true};
+    else if (!strcmp(k1var, "h2")) *o = {k_loglik_bin_mma<6, 1, 2, 2>, 28, 1, 64, true};        // 16 obs per update
+    else if (!strcmp(k1var, "ks2")) *o = {k_loglik_bin_mma<6, 1, 2, 1, 64, 2>, 28, 1, 64, true};  // 2 DMMA chains over k
+    else if (!strcmp(k1var, "h2ks2")) *o = {k_loglik_bin_mma<6, 1, 2, 2, 64, 2, 4>, 28, 1, 64, true};
+    if (o->fn) return true;
   }
   // DMMA contraction (+ <= 2 remainder DFMAs), 2 n-tiles (16 particles) per warp, 64 per block:
   // 114 registers -> 4 blocks per SM (the 4-n-tile layout, 178 registers, held 2; cfg2 run -6%)
@@ -1322,6 +1326,7 @@ sps_status sps_reset(sps_ctx* c, uint64_t seed, int32_t pass) {
   c->tr_rne.clear();
   c->inc_base = 0;
   c->last_adv = 0;
+  c->pre_normals_step = -1;
   c->launches = c->k1_launches = c->syncs = 0;
   c->k1_pairs = c->k1_ms = 0.0;
   c->host_launch_us = c->host_wait_us = c->host_graph_us = 0.0;
@@ -1473,6 +1478,13 @@ sps_status sps_cphase(sps_ctx* c, int32_t t_target, double phi_target, int32_t* 
   const int64_t Pl = c->Pl;
   const double P = (double)c->P;
   const unsigned pgrid = (unsigned)((Pl + 255) / 256);
+  // the next M phase's first-step normals depend only on the step number: generate them on the
+  // low-priority side stream now, overlapped with the C and S phases (host round trips included)
+  if (!c->profiling) {
+    CU(c, cudaEventRecord(c->ev_zfree[c->mstep & 1u], c->stream));
+    TRY(launch_normals(c, TAG_PROPOSAL, c->mstep, (int)(c->mstep & 1u)));
+    c->pre_normals_step = (int64_t)c->mstep;
+  }
   PROF_BEGIN(c);
   if (c->cfg.tempering == SPS_DATA_TEMPERING) {
     // ---- absorb observations one at a time ----
@@ -1882,9 +1894,12 @@ sps_status sps_mphase(sps_ctx* c, int32_t R_fixed, int32_t* R_out, double* min_r
   static const bool no_loop = getenv("SPS_NO_LOOP") != nullptr;
   const bool graph = c->G == 1 && !c->profiling && !no_graph;
   const bool loop = graph && !no_loop;
-  // the first step's normals after all earlier work of the main stream (graph replays record no Zbuf events)
-  CU(c, cudaEventRecord(c->ev_zfree[step0 & 1u], c->stream));
-  TRY(launch_normals(c, TAG_PROPOSAL, step0, (int)(step0 & 1u)));
+  if (c->pre_normals_step != (int64_t)step0) {
+    // the first step's normals after all earlier work of the main stream (graph replays record no Zbuf events)
+    CU(c, cudaEventRecord(c->ev_zfree[step0 & 1u], c->stream));
+    TRY(launch_normals(c, TAG_PROPOSAL, step0, (int)(step0 & 1u)));
+  }
+  c->pre_normals_step = -1;
   if (loop) {  // the whole adaptive M phase on the device: one graph launch, one host sync
     const auto g0 = std::chrono::steady_clock::now();
     TRY(build_mstep_loop(c, adaptive, Rmax));
