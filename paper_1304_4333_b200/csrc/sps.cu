@@ -152,6 +152,7 @@ struct sps_ctx {
   unsigned long long* tl = nullptr;     // debug (SPS_TIMELINE): per-step kernel start / end clocks
   double tl_acc[24] = {};
   int tl_rows = 0;
+  double tl_bin[6][4] = {};  // by t_l bin (<=32, <=64, <=128, <=256, <=512, >512): steps, K1 span, step span, gap
   double trace_acc[80] = {};
   int trace_n = 0;
   double* Zbuf[2] = {nullptr, nullptr};  // standard normals, one M step ahead (side stream)
@@ -1394,6 +1395,12 @@ sps_status sps_get_counters(const sps_ctx* cc, sps_counters* out) {
     fprintf(stderr, "SPS_TIMELINE mean us over %d steps:", c->tl_rows);
     for (int q = 0; q < 24; ++q) fprintf(stderr, " %s=%.2f", nm[q], c->tl_acc[q] / c->tl_rows / 1e3);
     fprintf(stderr, "\n");
+    static const char* bn[] = {"t<=32", "t<=64", "t<=128", "t<=256", "t<=512", "t>512"};
+    for (int b = 0; b < 6; ++b)
+      if (c->tl_bin[b][0] > 0)
+        fprintf(stderr, "SPS_TIMELINE %-7s steps %5.0f  K1 %7.2f us  step %7.2f us  gap %5.2f us\n", bn[b], c->tl_bin[b][0],
+                c->tl_bin[b][1] / c->tl_bin[b][0] / 1e3, c->tl_bin[b][2] / c->tl_bin[b][0] / 1e3,
+                c->tl_bin[b][3] / c->tl_bin[b][0] / 1e3);
   }
   out->launches = c->launches;
   out->k1_launches = c->k1_launches;
@@ -1666,6 +1673,14 @@ static sps_status timeline_accumulate(sps_ctx* c, int R) {
     c->tl_acc[11] += (double)t[3] - (double)t[5];   // normals end - K1 end
     if (r + 1 < rows && h[(size_t)(r + 1) * TL_W]) c->tl_acc[12] += (double)h[(size_t)(r + 1) * TL_W] - (double)t[11];
     c->tl_acc[13] += (double)t[11] - (double)t[0];  // step: propose start -> finalize end
+    {
+      const int tt = c->cfg.tempering == SPS_POWER_TEMPERING ? c->n : c->t;
+      const int b = tt <= 32 ? 0 : tt <= 64 ? 1 : tt <= 128 ? 2 : tt <= 256 ? 3 : tt <= 512 ? 4 : 5;
+      c->tl_bin[b][0] += 1;
+      c->tl_bin[b][1] += (double)(t[5] - t[4]);
+      c->tl_bin[b][2] += (double)(t[11] - t[0]);
+      if (r + 1 < rows && h[(size_t)(r + 1) * TL_W]) c->tl_bin[b][3] += (double)h[(size_t)(r + 1) * TL_W] - (double)t[11];
+    }
     if (t[16] && t[17] && t[18] && t[19] && t[20]) {  // finalize phases: stage / theta-bar / V / chol|RNE / tail
       c->tl_acc[18] += (double)t[16] - (double)t[10];
       c->tl_acc[19] += (double)t[17] - (double)t[16];

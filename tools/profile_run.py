@@ -16,6 +16,7 @@ import sps_synth  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--runs", type=int, default=1)
 ap.add_argument("--loglik-only", action="store_true")
+ap.add_argument("--nt", type=int, default=0, help="--loglik-only: observation range [0, nt) (0: all)")
 a = ap.parse_args()
 X, y = sps_synth.config_data("cfg2")
 cov = sps.g_prior(X, 2, 1.0 / 16)
@@ -25,7 +26,7 @@ if a.loglik_only:
 
     th = torch.randn(65536, 25, dtype=torch.float64, device="cuda") * 0.3
     for _ in range(5):
-        ctx.loglik_tensor(th)
+        ctx.loglik_tensor(th, 0, a.nt or None)
 else:
     ctx.run()  # warm-up
     for r in range(a.runs):
