@@ -578,26 +578,61 @@ __global__ void __launch_bounds__(128, MINB) k_loglik_bin_mma(LLArgs a) {
   }
   __syncthreads();  // every warp is done with buffer `buf` before it is refilled
   }  // sub-chunks
-  // combine the 8 lanes (ar = 0..7) of each particle column: sums of M and E, product of P
+  // combine the 8 lanes (ar = 0..7) of each particle column: sums of M and E, product of P.
+  // Reduce-scatter over the lane bits of ar (offsets 4, 8, 16): each round halves the values a
+  // lane carries until one is left (then butterfly), so the 2 NTW particles of a column end on
+  // different lanes and each lane takes at most one log (not 2 NTW in turn).
+  {
+    constexpr int V = 2 * NTW;
+    double m[V], pp[V];
+    int ex[V];
 #pragma unroll
-  for (int nt = 0; nt < NTW; ++nt)
+    for (int nt = 0; nt < NTW; ++nt)
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      renorm(Pp[nt][e], E[nt][e]);
-      double m = M[nt][e], pp = Pp[nt][e];
-      int ex = E[nt][e];
-#pragma unroll
-      for (int o = 4; o < 32; o <<= 1) {
-        m += __shfl_xor_sync(0xffffffffu, m, o);
-        pp *= __shfl_xor_sync(0xffffffffu, pp, o);  // 8 factors in [1,2): < 2^8
-        ex += __shfl_xor_sync(0xffffffffu, ex, o);
+      for (int e = 0; e < 2; ++e) {
+        renorm(Pp[nt][e], E[nt][e]);
+        m[nt * 2 + e] = M[nt][e];
+        pp[nt * 2 + e] = Pp[nt][e];
+        ex[nt * 2 + e] = E[nt][e];
       }
-      const int64_t p = pw + nt * 8 + 2 * ac + e;
-      if (ar == 0 && p < a.P) {
-        renorm(pp, ex);
-        a.part[(int64_t)cy * a.P + p] = -(m + (log(pp) + (double)ex * 0x1.62e42fefa39efp-1));
+    int jsel = 0;  // index (nt * 2 + e) of the value this lane keeps
+    int cnt = V;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int o = 4 << r;
+      const int bit = (ar >> r) & 1;
+      if (cnt > 1) {  // keep half (upper if bit), add the partner's copy of it
+        const int h = cnt / 2;
+#pragma unroll
+        for (int q = 0; q < V / 2; ++q) {
+          if (q < h) {
+            const double sm = bit ? m[q] : m[q + h], sp = bit ? pp[q] : pp[q + h];
+            const int se = bit ? ex[q] : ex[q + h];
+            const double km = bit ? m[q + h] : m[q], kp = bit ? pp[q + h] : pp[q];
+            const int ke = bit ? ex[q + h] : ex[q];
+            m[q] = km + __shfl_xor_sync(0xffffffffu, sm, o);
+            pp[q] = kp * __shfl_xor_sync(0xffffffffu, sp, o);  // 8 factors in [1,2): < 2^8
+            ex[q] = ke + __shfl_xor_sync(0xffffffffu, se, o);
+          }
+        }
+        jsel += bit * h;
+        cnt = h;
+      } else {
+        m[0] += __shfl_xor_sync(0xffffffffu, m[0], o);
+        pp[0] *= __shfl_xor_sync(0xffffffffu, pp[0], o);
+        ex[0] += __shfl_xor_sync(0xffffffffu, ex[0], o);
       }
     }
+    // lanes whose remaining ar bits are 0 hold a distinct (nt, e) each
+    const int rest = ar >> (V == 8 ? 3 : V == 4 ? 2 : 1);
+    const int64_t p = pw + (jsel >> 1) * 8 + 2 * ac + (jsel & 1);
+    if (rest == 0 && p < a.P) {
+      double pv = pp[0];
+      int xv = ex[0];
+      renorm(pv, xv);
+      a.part[(int64_t)cy * a.P + p] = -(m[0] + (log(pv) + (double)xv * 0x1.62e42fefa39efp-1));
+    }
+  }
   }  // items
   griddep_launch();
   tl_end(2);
