@@ -520,7 +520,11 @@ sps_status launch_loglik(sps_ctx* c, const double* theta, int64_t ldt, int64_t P
     const int tabb = (ch.tab > 256 ? ch.tab : 256) * 8;  // exp table bytes
     const int chunk_cap = std::max(1, (int)((smem_budget - tabb - 64) / row_bytes) - 16);
     // streaming (DMMA) kernels: two sub-chunk buffers (TMA double buffering) in the same budget
-    const int sub_cap = std::max(16, (chunk_cap / 2) / 16 * 16);
+    // X sub-chunks of <= 64 rows (2 x 14 KB at k = 25): the shared-memory footprint no longer grows
+    // with the chunk, so long chunks (fewer blocks, fewer per-block prologues / final logs) keep 4
+    // blocks per SM (cfg2 run 173 -> 168 ms vs the budget-derived cap; SPS_K1_SUBCAP: tuning)
+    static const int sub_cap_env = getenv("SPS_K1_SUBCAP") ? atoi(getenv("SPS_K1_SUBCAP")) : 64;
+    const int sub_cap = std::min(std::max(16, sub_cap_env / 16 * 16), std::max(16, (chunk_cap / 2) / 16 * 16));
     const int S_min = ch.streams ? 1 : std::max(1, (range + chunk_cap - 1) / chunk_cap);
     static const int s_cap = getenv("SPS_K1_SMAX") ? std::max(1, atoi(getenv("SPS_K1_SMAX"))) : 1 << 20;  // tuning
     static const double ovh = getenv("SPS_K1_OVH") ? atof(getenv("SPS_K1_OVH")) : 24.0;
@@ -559,6 +563,10 @@ sps_status launch_loglik(sps_ctx* c, const double* theta, int64_t ldt, int64_t P
     pl->smem = tabb + (size_t)(ch.streams ? 2 * ((rows + 15) / 16 * 16) : rows + 16) * c->ldx * 8 +
                (c->C > 2 ? (size_t)chunk * 4 : 0);
     if (pl->S > max_chunks) return fail(c, SPS_E_CONFIG, "observation range too long for the chunk buffer");
+    static const bool dbg_plan = getenv("SPS_K1_PLAN") != nullptr;
+    if (dbg_plan)
+      fprintf(stderr, "K1 plan: P %lld range %d -> S %d chunk %d sub %d occ %d smem %zu\n", (long long)P, range, pl->S,
+              pl->chunk, pl->sub, pl->occ, pl->smem);
   }
   LLArgs a{c->Xs, c->y, theta, part, ldt, P, t0, t1, pl->chunk};
   a.k = c->k;
