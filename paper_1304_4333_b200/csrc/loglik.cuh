@@ -29,7 +29,9 @@ namespace sps {
 
 constexpr int LL_THREADS = 128;
 
-__constant__ double c_exp2tab[64] = {
+// in global memory (read coalesced through L1/L2: a constant-bank read with 64 distinct addresses
+// serializes per address)
+__device__ const double c_exp2tab[64] = {
     0x1.0000000000000p+0, 0x1.02c9a3e778061p+0, 0x1.059b0d3158574p+0, 0x1.0874518759bc8p+0,
     0x1.0b5586cf9890fp+0, 0x1.0e3ec32d3d1a2p+0, 0x1.11301d0125b51p+0, 0x1.1429aaea92de0p+0,
     0x1.172b83c7d517bp+0, 0x1.1a35beb6fcb75p+0, 0x1.1d4873168b9aap+0, 0x1.2063b88628cd6p+0,
@@ -47,7 +49,7 @@ __constant__ double c_exp2tab[64] = {
     0x1.d5818dcfba487p+0, 0x1.da9e603db3285p+0, 0x1.dfc97337b9b5fp+0, 0x1.e502ee78b3ff6p+0,
     0x1.ea4afa2a490dap+0, 0x1.efa1bee615a27p+0, 0x1.f50765b6e4540p+0, 0x1.fa7c1819e90d8p+0};
 
-__constant__ double c_exp2tab256[256] = {
+__device__ const double c_exp2tab256[256] = {
     0x1.0000000000000p+0, 0x1.00b1afa5abcbfp+0, 0x1.0163da9fb3335p+0, 0x1.02168143b0281p+0,
     0x1.02c9a3e778061p+0, 0x1.037d42e11bbccp+0, 0x1.04315e86e7f85p+0, 0x1.04e5f72f654b1p+0,
     0x1.059b0d3158574p+0, 0x1.0650a0e3c1f89p+0, 0x1.0706b29ddf6dep+0, 0x1.07bd42b72a836p+0,
@@ -412,11 +414,21 @@ template <int KKD, int REM, int NTW, int H = 1, int TAB = 64, int KS = 1, int MI
 __global__ void __launch_bounds__(128, MINB) k_loglik_bin_mma(LLArgs a) {
   constexpr int KP = 4 * KKD + (REM ? 4 : 0);  // X row stride (k padded to 4)
   extern __shared__ __align__(16) double smem[];
-  if (a.stop && *a.stop) return;
-  tl_start(2);
   double* sT = smem;        // TAB
   double* sX = smem + 256;  // 2 x (sub rounded up to 16) x KP
-  for (int i = threadIdx.x; i < TAB; i += blockDim.x) sT[i] = TAB == 256 ? c_exp2tab256[i] : c_exp2tab[i];
+  double tv[TAB / 128 > 0 ? TAB / 128 : 1];  // exp table: loads in flight with the stop-flag load
+#pragma unroll
+  for (int u = 0; u < (TAB + 127) / 128; ++u) {
+    const int i = threadIdx.x + 128 * u;
+    tv[u] = i < TAB ? __ldg(TAB == 256 ? c_exp2tab256 + i : c_exp2tab + i) : 0.0;
+  }
+  if (a.stop && *a.stop) return;
+  tl_start(2);
+#pragma unroll
+  for (int u = 0; u < (TAB + 127) / 128; ++u) {
+    const int i = threadIdx.x + 128 * u;
+    if (i < TAB) sT[i] = tv[u];
+  }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, ar = lane >> 2, ac = lane & 3;
   const int sub0 = a.sub;  // X sub-chunk rows per shared buffer (0: the whole chunk)
   __shared__ __align__(8) uint64_t xbar[2];
