@@ -80,7 +80,8 @@ static uint64_t bits_from_dbl(double d) {
 }
 
 /* Portable log for positive normal x: x = 2^e m, m in (sqrt(2)/2, sqrt(2)],
- * log m = 2 atanh(s), s = (m-1)/(m+1), series to s^23.  Only IEEE + - * /. */
+ * log m = 2 atanh(s), s = (m-1)/(m+1), series to s^23.  Only IEEE + - * / and fma (each
+ * a single correctly rounded IEEE operation, so the CUDA library reproduces it bit for bit; R15). */
 double or_plog(double x) {
   uint64_t b = bits_from_dbl(x);
   int e = (int)((b >> 52) & 0x7ff) - 1023;
@@ -93,20 +94,20 @@ double or_plog(double x) {
   double s = f / (2.0 + f);
   double z = s * s;
   double R = 0x1.642c8590b2164p-5;     /* 1/23 */
-  R = 0x1.8618618618618p-5 + z * R;    /* 1/21 */
-  R = 0x1.af286bca1af28p-5 + z * R;    /* 1/19 */
-  R = 0x1.e1e1e1e1e1e1ep-5 + z * R;    /* 1/17 */
-  R = 0x1.1111111111111p-4 + z * R;    /* 1/15 */
-  R = 0x1.3b13b13b13b14p-4 + z * R;    /* 1/13 */
-  R = 0x1.745d1745d1746p-4 + z * R;    /* 1/11 */
-  R = 0x1.c71c71c71c71cp-4 + z * R;    /* 1/9 */
-  R = 0x1.2492492492492p-3 + z * R;    /* 1/7 */
-  R = 0x1.999999999999ap-3 + z * R;    /* 1/5 */
-  R = 0x1.5555555555555p-2 + z * R;    /* 1/3 */
+  R = fma(z, R, 0x1.8618618618618p-5);    /* 1/21 */
+  R = fma(z, R, 0x1.af286bca1af28p-5);    /* 1/19 */
+  R = fma(z, R, 0x1.e1e1e1e1e1e1ep-5);    /* 1/17 */
+  R = fma(z, R, 0x1.1111111111111p-4);    /* 1/15 */
+  R = fma(z, R, 0x1.3b13b13b13b14p-4);    /* 1/13 */
+  R = fma(z, R, 0x1.745d1745d1746p-4);    /* 1/11 */
+  R = fma(z, R, 0x1.c71c71c71c71cp-4);    /* 1/9 */
+  R = fma(z, R, 0x1.2492492492492p-3);    /* 1/7 */
+  R = fma(z, R, 0x1.999999999999ap-3);    /* 1/5 */
+  R = fma(z, R, 0x1.5555555555555p-2);    /* 1/3 */
   double two_s = 2.0 * s;
-  double logm = two_s + two_s * (z * R);
+  double logm = fma(two_s, z * R, two_s);
   double ed = (double)e;
-  return ed * 0x1.62e42fee00000p-1 + (ed * 0x1.a39ef35793c76p-33 + logm);
+  return fma(ed, 0x1.62e42fee00000p-1, fma(ed, 0x1.a39ef35793c76p-33, logm));
 }
 
 /* Portable exp for x <= 0 (resampling weights).  x < -708 -> 0 (R8).
@@ -125,7 +126,8 @@ double or_pexp(double x) {
 }
 
 /* Portable (sin 2 pi u, cos 2 pi u) for u in (0,1): v = 4u exact, q = nearest
- * quadrant, f = v - q exact in [-1/2, 1/2], a = f pi/2; Taylor to a^17 / a^16. */
+ * quadrant, f = v - q exact in [-1/2, 1/2], a = f pi/2; Taylor to a^17 / a^16, Horner steps
+ * as fma (R15). */
 void or_psincos2pi(double u, double* s_out, double* c_out) {
   double v = 4.0 * u;
   double q = floor(v + 0.5);
@@ -133,23 +135,23 @@ void or_psincos2pi(double u, double* s_out, double* c_out) {
   double a = f * 0x1.921fb54442d18p+0;
   double a2 = a * a;
   double sp = 0x1.952c77030ad4ap-49;
-  sp = -0x1.ae7f3e733b81fp-41 + a2 * sp;
-  sp = 0x1.6124613a86d09p-33 + a2 * sp;
-  sp = -0x1.ae64567f544e4p-26 + a2 * sp;
-  sp = 0x1.71de3a556c734p-19 + a2 * sp;
-  sp = -0x1.a01a01a01a01ap-13 + a2 * sp;
-  sp = 0x1.1111111111111p-7 + a2 * sp;
-  sp = -0x1.5555555555555p-3 + a2 * sp;
-  double s = a + a * (a2 * sp);
+  sp = fma(a2, sp, -0x1.ae7f3e733b81fp-41);
+  sp = fma(a2, sp, 0x1.6124613a86d09p-33);
+  sp = fma(a2, sp, -0x1.ae64567f544e4p-26);
+  sp = fma(a2, sp, 0x1.71de3a556c734p-19);
+  sp = fma(a2, sp, -0x1.a01a01a01a01ap-13);
+  sp = fma(a2, sp, 0x1.1111111111111p-7);
+  sp = fma(a2, sp, -0x1.5555555555555p-3);
+  double s = fma(a, a2 * sp, a);
   double cp = 0x1.ae7f3e733b81fp-45;
-  cp = -0x1.93974a8c07c9dp-37 + a2 * cp;
-  cp = 0x1.1eed8eff8d898p-29 + a2 * cp;
-  cp = -0x1.27e4fb7789f5cp-22 + a2 * cp;
-  cp = 0x1.a01a01a01a01ap-16 + a2 * cp;
-  cp = -0x1.6c16c16c16c17p-10 + a2 * cp;
-  cp = 0x1.5555555555555p-5 + a2 * cp;
-  cp = -0x1.0000000000000p-1 + a2 * cp;
-  double c = 1.0 + a2 * cp;
+  cp = fma(a2, cp, -0x1.93974a8c07c9dp-37);
+  cp = fma(a2, cp, 0x1.1eed8eff8d898p-29);
+  cp = fma(a2, cp, -0x1.27e4fb7789f5cp-22);
+  cp = fma(a2, cp, 0x1.a01a01a01a01ap-16);
+  cp = fma(a2, cp, -0x1.6c16c16c16c17p-10);
+  cp = fma(a2, cp, 0x1.5555555555555p-5);
+  cp = fma(a2, cp, -0x1.0000000000000p-1);
+  double c = fma(a2, cp, 1.0);
   int qi = ((int)q) & 3;
   if (qi == 0) {
     *s_out = s;

@@ -64,20 +64,20 @@ __device__ __forceinline__ double plog(double x) {
   const double s = __ddiv_rn(f, __dadd_rn(2.0, f));
   const double z = __dmul_rn(s, s);
   double R = 0x1.642c8590b2164p-5;
-  R = __dadd_rn(0x1.8618618618618p-5, __dmul_rn(z, R));
-  R = __dadd_rn(0x1.af286bca1af28p-5, __dmul_rn(z, R));
-  R = __dadd_rn(0x1.e1e1e1e1e1e1ep-5, __dmul_rn(z, R));
-  R = __dadd_rn(0x1.1111111111111p-4, __dmul_rn(z, R));
-  R = __dadd_rn(0x1.3b13b13b13b14p-4, __dmul_rn(z, R));
-  R = __dadd_rn(0x1.745d1745d1746p-4, __dmul_rn(z, R));
-  R = __dadd_rn(0x1.c71c71c71c71cp-4, __dmul_rn(z, R));
-  R = __dadd_rn(0x1.2492492492492p-3, __dmul_rn(z, R));
-  R = __dadd_rn(0x1.999999999999ap-3, __dmul_rn(z, R));
-  R = __dadd_rn(0x1.5555555555555p-2, __dmul_rn(z, R));
+  R = __fma_rn(z, R, 0x1.8618618618618p-5);
+  R = __fma_rn(z, R, 0x1.af286bca1af28p-5);
+  R = __fma_rn(z, R, 0x1.e1e1e1e1e1e1ep-5);
+  R = __fma_rn(z, R, 0x1.1111111111111p-4);
+  R = __fma_rn(z, R, 0x1.3b13b13b13b14p-4);
+  R = __fma_rn(z, R, 0x1.745d1745d1746p-4);
+  R = __fma_rn(z, R, 0x1.c71c71c71c71cp-4);
+  R = __fma_rn(z, R, 0x1.2492492492492p-3);
+  R = __fma_rn(z, R, 0x1.999999999999ap-3);
+  R = __fma_rn(z, R, 0x1.5555555555555p-2);
   const double two_s = __dmul_rn(2.0, s);
-  const double logm = __dadd_rn(two_s, __dmul_rn(two_s, __dmul_rn(z, R)));
+  const double logm = __fma_rn(two_s, __dmul_rn(z, R), two_s);
   const double ed = (double)e;
-  return __dadd_rn(__dmul_rn(ed, 0x1.62e42fee00000p-1), __dadd_rn(__dmul_rn(ed, 0x1.a39ef35793c76p-33), logm));
+  return __fma_rn(ed, 0x1.62e42fee00000p-1, __fma_rn(ed, 0x1.a39ef35793c76p-33, logm));
 }
 
 // Same operation sequence as or_pexp (x <= 0; x < -708 -> 0, R8).
@@ -102,23 +102,23 @@ __device__ __forceinline__ void psincos2pi(double u, double* s_out, double* c_ou
   const double a = __dmul_rn(f, 0x1.921fb54442d18p+0);
   const double a2 = __dmul_rn(a, a);
   double sp = 0x1.952c77030ad4ap-49;
-  sp = __dadd_rn(-0x1.ae7f3e733b81fp-41, __dmul_rn(a2, sp));
-  sp = __dadd_rn(0x1.6124613a86d09p-33, __dmul_rn(a2, sp));
-  sp = __dadd_rn(-0x1.ae64567f544e4p-26, __dmul_rn(a2, sp));
-  sp = __dadd_rn(0x1.71de3a556c734p-19, __dmul_rn(a2, sp));
-  sp = __dadd_rn(-0x1.a01a01a01a01ap-13, __dmul_rn(a2, sp));
-  sp = __dadd_rn(0x1.1111111111111p-7, __dmul_rn(a2, sp));
-  sp = __dadd_rn(-0x1.5555555555555p-3, __dmul_rn(a2, sp));
-  const double s = __dadd_rn(a, __dmul_rn(a, __dmul_rn(a2, sp)));
+  sp = __fma_rn(a2, sp, -0x1.ae7f3e733b81fp-41);
+  sp = __fma_rn(a2, sp, 0x1.6124613a86d09p-33);
+  sp = __fma_rn(a2, sp, -0x1.ae64567f544e4p-26);
+  sp = __fma_rn(a2, sp, 0x1.71de3a556c734p-19);
+  sp = __fma_rn(a2, sp, -0x1.a01a01a01a01ap-13);
+  sp = __fma_rn(a2, sp, 0x1.1111111111111p-7);
+  sp = __fma_rn(a2, sp, -0x1.5555555555555p-3);
+  const double s = __fma_rn(a, __dmul_rn(a2, sp), a);
   double cp = 0x1.ae7f3e733b81fp-45;
-  cp = __dadd_rn(-0x1.93974a8c07c9dp-37, __dmul_rn(a2, cp));
-  cp = __dadd_rn(0x1.1eed8eff8d898p-29, __dmul_rn(a2, cp));
-  cp = __dadd_rn(-0x1.27e4fb7789f5cp-22, __dmul_rn(a2, cp));
-  cp = __dadd_rn(0x1.a01a01a01a01ap-16, __dmul_rn(a2, cp));
-  cp = __dadd_rn(-0x1.6c16c16c16c17p-10, __dmul_rn(a2, cp));
-  cp = __dadd_rn(0x1.5555555555555p-5, __dmul_rn(a2, cp));
-  cp = __dadd_rn(-0x1.0000000000000p-1, __dmul_rn(a2, cp));
-  const double c = __dadd_rn(1.0, __dmul_rn(a2, cp));
+  cp = __fma_rn(a2, cp, -0x1.93974a8c07c9dp-37);
+  cp = __fma_rn(a2, cp, 0x1.1eed8eff8d898p-29);
+  cp = __fma_rn(a2, cp, -0x1.27e4fb7789f5cp-22);
+  cp = __fma_rn(a2, cp, 0x1.a01a01a01a01ap-16);
+  cp = __fma_rn(a2, cp, -0x1.6c16c16c16c17p-10);
+  cp = __fma_rn(a2, cp, 0x1.5555555555555p-5);
+  cp = __fma_rn(a2, cp, -0x1.0000000000000p-1);
+  const double c = __fma_rn(a2, cp, 1.0);
   const int qi = ((int)q) & 3;
   if (qi == 0) {
     *s_out = s;

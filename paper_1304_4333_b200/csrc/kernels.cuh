@@ -263,7 +263,35 @@ __global__ void __launch_bounds__(128) k_cphase_scan(const double* __restrict__ 
   __syncthreads();
   if (!valid) return;
   double lw = lw_cur[p];
-  for (int b = 0; b < B; ++b) {
+  int b = 0;
+  if (C == 2) {  // binary: two observations per iteration, two accumulators each (latency-bound: ILP)
+    for (; b + 2 <= B; b += 2) {
+      const double* x0 = Xs + (int64_t)(s0 + b) * ldx;
+      const double* x1 = x0 + ldx;
+      double a0 = 0.0, a1 = 0.0, c0 = 0.0, c1 = 0.0;
+      int i = 0;
+      for (; i + 2 <= k; i += 2) {
+        const double t0 = sth[i * blockDim.x + threadIdx.x], t1 = sth[(i + 1) * blockDim.x + threadIdx.x];
+        a0 = fma(t0, __ldg(x0 + i), a0);
+        a1 = fma(t1, __ldg(x0 + i + 1), a1);
+        c0 = fma(t0, __ldg(x1 + i), c0);
+        c1 = fma(t1, __ldg(x1 + i + 1), c1);
+      }
+      if (i < k) {
+        const double t0 = sth[i * blockDim.x + threadIdx.x];
+        a0 = fma(t0, __ldg(x0 + i), a0);
+        c0 = fma(t0, __ldg(x1 + i), c0);
+      }
+      const double sa = a0 + a1, sc = c0 + c1;
+      const double la = -(fmax(sa, 0.0) + log1p(exp(-fabs(sa))));
+      const double lc = -(fmax(sc, 0.0) + log1p(exp(-fabs(sc))));
+      lw += la;
+      lwbuf[(int64_t)b * P + p] = lw;
+      lw += lc;
+      lwbuf[(int64_t)(b + 1) * P + p] = lw;
+    }
+  }
+  for (; b < B; ++b) {
     const int t = s0 + b;
     const double* x = Xs + (int64_t)t * ldx;
     double lpt;

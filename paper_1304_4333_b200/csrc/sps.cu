@@ -606,9 +606,16 @@ sps_status launch_normals(sps_ctx* c, uint32_t tag, uint32_t step, int slot, boo
     cudaLaunchConfig_t lc = {};
     // M steps: 2 blocks per SM (grid-stride); setup / first draws: full grid
     const int64_t full = (tasks + 255) / 256;
-    static const int nb_per_sm = getenv("SPS_NORMALS_BPS") ? atoi(getenv("SPS_NORMALS_BPS")) : 8;
-    lc.gridDim = dim3((unsigned)(forked && nb_per_sm > 0 ? std::min<int64_t>(full, nb_per_sm * (int64_t)num_sms()) : full));
-    lc.blockDim = dim3(256);
+    static const bool at_propose = getenv("SPS_NORMALS_FORK") && !strcmp(getenv("SPS_NORMALS_FORK"), "propose");
+    // forked at the proposal: one 64-thread block per SM (its 4 K registers fit beside 4 K1 blocks) over
+    // the whole step; forked at accept: 8 x 256 per SM into the tail
+    static const int nb_per_sm =
+        getenv("SPS_NORMALS_BPS") ? atoi(getenv("SPS_NORMALS_BPS")) : (at_propose ? 1 : 8);
+    static const int nthr = getenv("SPS_NORMALS_THREADS") ? atoi(getenv("SPS_NORMALS_THREADS")) : (at_propose ? 64 : 256);
+    const int64_t fullb = (tasks + nthr - 1) / nthr;
+    lc.gridDim = dim3((unsigned)(forked && nb_per_sm > 0 ? std::min<int64_t>(fullb, nb_per_sm * (int64_t)num_sms())
+                                                        : full));
+    lc.blockDim = dim3(forked ? nthr : 256);
     lc.stream = st;
     cudaLaunchAttribute at[1];
     int lo = 0, hi = 0;
@@ -1051,7 +1058,8 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
   // accept + moments layout: blocks of tp particles inside one group (tp divides N,
   // tp <= 256, staged tile tp x round_up(d, 8) doubles <= 96 KB)
   {
-    const int cap = std::max(1, std::min(256, 96 * 1024 / (8 * ((d + 7) / 8 * 8 + 4))));
+    static const int tp_env = getenv("SPS_ACC_TP") ? atoi(getenv("SPS_ACC_TP")) : 256;  // tuning
+    const int cap = std::max(1, std::min(std::max(1, std::min(tp_env, 256)), 96 * 1024 / (8 * ((d + 7) / 8 * 8 + 4))));
     c->tp = 1;
     for (int q = std::min(c->N, cap); q >= 1; --q)
       if (c->N % q == 0) {
@@ -1724,12 +1732,21 @@ static sps_status launch_mstep(sps_ctx* c, uint32_t step, bool allow_stop, bool 
   const int* stop = &c->ctl->stop;
   const int zs = (int)(step & 1u);
   TRY(launch_draw(c, zs, c->theta, c->Lprop, c->theta_s, c->lp_s, stop, graph, true));
+  // the next step's normals: forked after accept into the reduce / finalize tail (default), or after
+  // the proposal with a small resident footprint (SPS_NORMALS_FORK=propose, experiment)
+  // (measured: forking at the proposal stretches the normals to ~60 us and delays the next step by
+  // ~20 us; the tail fork, the default, costs the finalize SM some issue slots instead)
+  static const bool fork_at_propose = getenv("SPS_NORMALS_FORK") && !strcmp(getenv("SPS_NORMALS_FORK"), "propose");
+  if (fork_at_propose) {
+    CU(c, cudaEventRecord(c->ev_fork, c->stream));
+    TRY(launch_normals(c, TAG_PROPOSAL, step + 1u, (int)((step + 1u) & 1u), graph, true));
+  }
   int nch = 1;
   TRY(launch_loglik(c, c->theta_s, c->d, c->Pl, 0, t1, c->part, c->max_chunks, &nch, stop));
   // next step's normals on the low-priority side stream, forked after accept: they fill the SMs
   // the reduce / one-block finalize tail leaves idle (SPS_TIMELINE: launched before K1 they held
   // every SM while K1 waited 17.8 us; forked after K1 they stretched accept from 13 to 25 us)
-  TRY(moments_finalize(c, true, nch, temper, step, stop, c->LUbuf[zs], 1, allow_stop, zs, true));
+  TRY(moments_finalize(c, true, nch, temper, step, stop, c->LUbuf[zs], 1, allow_stop, zs, !fork_at_propose));
   if (graph) {
     CU(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
     if (!c->capturing_loop) CU(c, cudaEventRecordWithFlags(c->evs[zs], c->stream, cudaEventRecordExternal));
