@@ -76,3 +76,43 @@ def test_loopback_sharded_matches_single_rank(sps, orc, G, tempering):
     o = orc.run(X, y, 2, J, N, seed=seed, prior_mean=np.zeros(4), prior_cov=cov, tempering=tempering)
     assert abs(res[0][0]["logml"] - o["logml"]) <= 1e-6
     assert np.all(np.abs(res[0][0]["mean"] - o["mean"]) <= 1e-6)
+
+
+def test_loopback_sharded_two_pass_and_predictive(sps, orc):
+    """Algorithm 3 pass 2 (fixed design: the ESS partials are still gathered for the predictive
+    likelihoods, Sigma_lr replayed on every rank) and the log predictive likelihoods, sharded over
+    G = 2 loopback ranks, against the single-rank context on the same design."""
+    X, y = sps_synth.config_data("cfg1")
+    cov = orc.g_prior(X, 2, 0.25)
+    J, N = 8, 128
+    o1, o2 = orc.two_pass(X, y, 2, J, N, 4, 5, np.zeros(4), cov)
+    s = sps.Sps(X, y, np.zeros(4), cov, J=J, N=N, seed=5, pass_=1)
+    s.set_design(o1)
+    single = s.run()
+    s.close()
+    lid = sps.loopback_unique_id()
+    out = [None] * 2
+    errs = []
+
+    def worker(r):
+        try:
+            c = sps.Sps(X, y, np.zeros(4), cov, J=J, N=N, seed=5, pass_=1, rank=r, nranks=2, nccl_id=lid)
+            c.set_design(o1)
+            out[r] = c.run()
+            c.close()
+        except Exception as e:
+            errs.append(e)
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not errs, errs
+    for rep in out:
+        assert np.array_equal(rep["R_cycle"], single["R_cycle"]) and np.array_equal(rep["t_cycle"], single["t_cycle"])
+        assert abs(rep["logml"] - single["logml"]) < 1e-9
+        assert np.allclose(rep["logpl"], single["logpl"], atol=1e-9, rtol=0)
+        assert np.allclose(rep["mean"], single["mean"], atol=1e-9, rtol=0)
+    assert abs(out[0]["logml"] - o2["logml"]) <= 1e-6
+    assert np.all(np.abs(out[0]["logpl"] - o2["logpl"]) <= 1e-9)
