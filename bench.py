@@ -310,7 +310,10 @@ def main():
             "clocks": clk,
             "e2e": e2e,
             "gpu_launches": launches,
-            "roofline": {"bound": "alu", "kernel": "k_loglik_bin_mma<6,1,2> (K1: fp64 DMMA contraction + fused softplus/product epilogue)",
+            # K1's contraction runs on the tensor cores' FP64 (DMMA) subpipe, which B200 shares with
+            # the FP64 ALU pipe its epilogue uses: bound by that pipe, against its measured rate
+            # (MEASURED_PEAKS.json carries no FP64 figure)
+            "roofline": {"bound": "tensor", "kernel": "k_loglik_bin_mma<6,1,2> (K1: fp64 DMMA contraction + fused softplus/product epilogue)",
                          "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
                          "ops_per_pair": ops_per_pair, "k1_avg_ms": k1_avg_ms,
@@ -319,7 +322,8 @@ def main():
                          "fp64_pipe_frac": pipe_tflops / FP64_PEAK_TFLOPS,
                          "contraction_frac": pairs_per_launch * 2 * k * (WORKLOAD["C"] - 1) / (k1_avg_ms * 1e-3) / 1e12
                          / FP64_PEAK_TFLOPS,
-                         "peak_source": "measured FP64 pipe (profiles/r01_fp64_peaks.json)",
+                         "peak_source": "measured FP64 DMMA rate, 37.07 TF/s (tools/fp64_peaks.cu, profiles/r01_fp64_peaks.json; "
+                                        "the DFMA epilogue shares the pipe); ncu: profiles/r01_k1_full_ncu_v7.txt",
                          "full_data_eval": {"ms": full_ms, "pairs_per_s": full_pairs_s,
                                             "frac": full_pairs_s * ops_per_pair / 1e12 / FP64_PEAK_TFLOPS}},
             "cpu_baseline": cpu,

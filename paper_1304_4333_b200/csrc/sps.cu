@@ -1743,10 +1743,15 @@ static sps_status launch_mstep(sps_ctx* c, uint32_t step, bool allow_stop, bool 
   }
   int nch = 1;
   TRY(launch_loglik(c, c->theta_s, c->d, c->Pl, 0, t1, c->part, c->max_chunks, &nch, stop));
+  static const bool fork_at_k1 = getenv("SPS_NORMALS_FORK") && !strcmp(getenv("SPS_NORMALS_FORK"), "k1");
+  if (fork_at_k1) {  // (experiment) after K1: overlap accept + reduce + finalize
+    CU(c, cudaEventRecord(c->ev_fork, c->stream));
+    TRY(launch_normals(c, TAG_PROPOSAL, step + 1u, (int)((step + 1u) & 1u), graph, true));
+  }
   // next step's normals on the low-priority side stream, forked after accept: they fill the SMs
   // the reduce / one-block finalize tail leaves idle (SPS_TIMELINE: launched before K1 they held
   // every SM while K1 waited 17.8 us; forked after K1 they stretched accept from 13 to 25 us)
-  TRY(moments_finalize(c, true, nch, temper, step, stop, c->LUbuf[zs], 1, allow_stop, zs, !fork_at_propose));
+  TRY(moments_finalize(c, true, nch, temper, step, stop, c->LUbuf[zs], 1, allow_stop, zs, !fork_at_propose && !fork_at_k1));
   if (graph) {
     CU(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
     if (!c->capturing_loop) CU(c, cudaEventRecordWithFlags(c->evs[zs], c->stream, cudaEventRecordExternal));
