@@ -59,17 +59,21 @@ __global__ void __launch_bounds__(256) k_normals(int64_t P, int64_t p0, int np, 
     if (logu) logu = logualt;
   }
   const int64_t ntask = P * np;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntask; t += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x, g0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t t = g0; t < ntask; t += gstride) {
     const int64_t p = t / np;
     const int pr = (int)(t - p * np);
     double z0, z1;
     normal_pair(seed, (uint32_t)pr, (uint32_t)(p0 + p), step, tag, pass, &z0, &z1);
     reinterpret_cast<double2*>(Z + p * ldz)[pr] = make_double2(z0, z1);
-    if (logu && pr == 0) {
+  }
+  // the accept log-uniforms in a pass of their own: as a branch of the loop above (pr == 0) every
+  // warp paid one plog for its ~2.5 particle-leading lanes -- ~40% of the kernel's FP64 issue
+  if (logu)
+    for (int64_t p = g0; p < P; p += gstride) {
       const u4 w = stream_block(seed, 0u, (uint32_t)(p0 + p), step, TAG_ACCEPT, pass);
       logu[p] = plog(u01(w.x, w.y));
     }
-  }
   if (sctl) tl_end(1);
 }
 
