@@ -276,9 +276,14 @@ def main():
         e2e_pairs = 0.0
         d2h = 0
         for s in range(args.steps):
+            id2 = None
+            if world > 1:  # every communicator needs its own ncclUniqueId (rank 0 makes it, all receive it)
+                ids2 = [sps.nccl_unique_id() if rank == 0 else None]
+                dist.broadcast_object_list(ids2, src=0)
+                id2 = ids2[0]
             t0 = time.perf_counter()
             c2 = sps.Sps(Xp, yp, np.zeros(k), cov, J=J, N=N, seed=1 + s, rank=rank, nranks=world,
-                         nccl_id=None if world == 1 else nccl_id, device=local)
+                         nccl_id=id2, device=local)
             r2 = c2.run()
             c2.close()
             wall += time.perf_counter() - t0
