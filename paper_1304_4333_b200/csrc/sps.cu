@@ -426,6 +426,8 @@ bool choose_ll(int k, int C, LLChoice* o) {
     else if (!strcmp(k1var, "h2")) *o = {k_loglik_bin_mma<6, 1, 2, 2>, 28, 1, 64, true};        // 16 obs per update
     else if (!strcmp(k1var, "ks2")) *o = {k_loglik_bin_mma<6, 1, 2, 1, 64, 2>, 28, 1, 64, true};  // 2 DMMA chains over k
     else if (!strcmp(k1var, "h2ks2")) *o = {k_loglik_bin_mma<6, 1, 2, 2, 64, 2, 4>, 28, 1, 64, true};
+    else if (!strcmp(k1var, "m5")) *o = {k_loglik_bin_mma<6, 1, 2, 1, 64, 1, 5>, 28, 1, 64, true};    // <= 102 registers
+    else if (!strcmp(k1var, "m6")) *o = {k_loglik_bin_mma<6, 1, 2, 1, 64, 1, 6>, 28, 1, 64, true};    // <= 85 registers
     if (o->fn) return true;
   }
   // DMMA contraction (+ <= 2 remainder DFMAs), 2 n-tiles (16 particles) per warp, 64 per block:
