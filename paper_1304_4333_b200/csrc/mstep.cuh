@@ -690,19 +690,34 @@ __global__ void __launch_bounds__(256) k_accept_tile(AccArgs a) {
   if (tr) a.trace[66] = gtimer();
   if (dec) tl_mark(13);
   if (dec) {  // accepted rows only: theta* over the staged rows (one cp.async round), then back to theta
+    // compact the accepted rows first (ballot prefix; tp <= blockDim): the copy loops then touch
+    // nacc d elements instead of predicating all tp d (~1/4 accept)
+    __shared__ int s_list[256];
+    __shared__ int s_wc[8];
+    const bool okq = q0 < tp && acc[q0];
+    const unsigned bal = __ballot_sync(0xffffffffu, okq);
+    if (lane == 0) s_wc[w] = __popc(bal);
+    __syncthreads();
+    int off = 0;
+    for (int ww = 0; ww < w; ++ww) off += s_wc[ww];
+    if (okq) s_list[off + __popc(bal & ((1u << lane) - 1u))] = q0;
+    __syncthreads();
     const double* ts = a.theta_s + pbase * d;
     double* th = a.theta + pbase * d;
-#pragma unroll 5
-    for (int e = threadIdx.x; e < TD; e += blockDim.x) {
-      const int q = (int)(((uint64_t)e * a.dmagic) >> 32);
-      if (acc[q]) cp_async8(sTh + e, ts + e);
+    const int ne = nacc * d;
+#pragma unroll 4
+    for (int e = threadIdx.x; e < ne; e += blockDim.x) {
+      const int j = (int)(((uint64_t)e * a.dmagic) >> 32);
+      const int o = s_list[j] * d + (e - j * d);
+      cp_async8(sTh + o, ts + o);
     }
     cp_async_wait_all();
     __syncthreads();
-#pragma unroll 5
-    for (int e = threadIdx.x; e < TD; e += blockDim.x) {
-      const int q = (int)(((uint64_t)e * a.dmagic) >> 32);
-      if (acc[q]) th[e] = sTh[e];
+#pragma unroll 4
+    for (int e = threadIdx.x; e < ne; e += blockDim.x) {
+      const int j = (int)(((uint64_t)e * a.dmagic) >> 32);
+      const int o = s_list[j] * d + (e - j * d);
+      th[o] = sTh[o];
     }
   }
   // T'T, lower tiles; warp w takes k-steps k0 = 4 (w + 8 m)
