@@ -653,9 +653,18 @@ __global__ void __launch_bounds__(1024) k_resample(const double* __restrict__ lw
   if (anc_out)
     for (int n = threadIdx.x; n < N; n += blockDim.x) anc_out[(int64_t)j * N + n] = anc[n];
   const int64_t base = (int64_t)j * N;
-  for (int idx = threadIdx.x; idx < N * d; idx += blockDim.x) {
-    const int n = idx / d, c = idx % d;
-    th_dst[(base + n) * d + c] = th_src[(base + anc[n]) * d + c];
+  {  // flat (n, c) walk with incremental row / column (no integer division per element)
+    const int sr = (int)blockDim.x / d, sc = (int)blockDim.x - sr * d;
+    int n = (int)threadIdx.x / d, c = (int)threadIdx.x - n * d;
+    while (n < N) {
+      th_dst[(base + n) * d + c] = th_src[(base + anc[n]) * d + c];
+      n += sr;
+      c += sc;
+      if (c >= d) {
+        c -= d;
+        ++n;
+      }
+    }
   }
   for (int n = threadIdx.x; n < N; n += blockDim.x) {
     L_dst[base + n] = L_src[base + anc[n]];
