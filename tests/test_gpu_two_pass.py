@@ -125,3 +125,20 @@ def test_design_api_errors(sps):
     with pytest.raises(sps.SpsError):
         s.set_design(bad)
     s.close()
+
+
+def test_sigma_record_grows_across_phases(sps, orc):
+    """A small max_m_steps makes the Sigma_lr record reserve per M phase (mstep + max_m_steps + 2)
+    and grow several times during the run; the record still matches the oracle's, step for step."""
+    X, y = sps_synth.config_data("cfg1")
+    cov = orc.g_prior(X, 2, 0.25)
+    o1 = orc.run(X, y, 2, 4, 128, 3, np.zeros(4), cov, record_sigma=True, max_m_steps=30)
+    s = sps.Sps(X, y, np.zeros(4), cov, J=4, N=128, seed=3, max_m_steps=30)
+    s.record_sigma(True)
+    g1 = s.run()
+    sig = s.sigma(0, g1["total_m_steps"])
+    with pytest.raises(sps.SpsError):
+        s.sigma(0, g1["total_m_steps"] + 5)  # beyond the steps run
+    s.close()
+    _compare(g1, o1)
+    _sigma_close(sig, o1["sigma"])
