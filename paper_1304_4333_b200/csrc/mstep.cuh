@@ -190,10 +190,10 @@ template <int KK, int TILE>  // TILE particles per tile = TILE / 8 warps of 8 ro
 __global__ void __launch_bounds__(4 * TILE, TILE == 32 ? 5 : 3) k_propose_rb(DrawArgs a) {
   constexpr int KP = 4 * KK, NT = (KP + 7) / 8, NP = 8 * NT;
   extern __shared__ __align__(16) double sm[];
-  if (a.stop && *a.stop) return;
-  if (a.set_step && blockIdx.x == 0 && threadIdx.x == 0) a.ctl->step_cur = a.step0 + (uint32_t)a.ctl->steps_done;
-  if (a.set_step) tl_start(0);
-  griddep_launch();  // persistent grid (all CTAs resident): K1's CTAs may start their prologue
+  // with a static Z buffer (a.Zalt null) the first tile's loads are issued before the stop flag
+  // and the step counter are read (two dependent global loads off the critical path)
+  const bool early = a.Zalt == nullptr;
+  if (!early && a.stop && *a.stop) return;
   const double* Zsrc = a.Z;
   if (a.Zalt && ((a.step0 + (uint32_t)a.ctl->steps_done) & 1u)) Zsrc = a.Zalt;
   const int d = a.d, BS = round_up(TILE * d, 2);
@@ -227,6 +227,13 @@ __global__ void __launch_bounds__(4 * TILE, TILE == 32 ? 5 : 3) k_propose_rb(Dra
     }
   };
   if (threadIdx.x == 0 && (int64_t)blockIdx.x < ntl) issue(blockIdx.x, 0, true);
+  if (early && a.stop && *a.stop) {  // speculative step after the stop: drain the loads, exit
+    if (threadIdx.x == 0 && (int64_t)blockIdx.x < ntl) mbar_wait(&bar[0], 0u);
+    return;
+  }
+  if (a.set_step && blockIdx.x == 0 && threadIdx.x == 0) a.ctl->step_cur = a.step0 + (uint32_t)a.ctl->steps_done;
+  if (a.set_step) tl_start(0);
+  griddep_launch();  // persistent grid (all CTAs resident): K1's CTAs may start their prologue
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < ntl; tile += gridDim.x, ++it) {
     const int buf = it & 1;

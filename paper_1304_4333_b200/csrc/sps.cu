@@ -662,10 +662,8 @@ sps_status launch_draw(sps_ctx* c, int slot, const double* base, const double* L
   a.d = d;
   a.step0 = c->phase_step0;
   a.set_step = set_step ? 1 : 0;
-  if (c->capturing_loop) {  // device-side loop: the parity of the device step picks the buffer
-    a.Z = c->Zbuf[0];
-    a.Zalt = c->Zbuf[1];
-  }
+  // (device-side loop: the body's first step always runs at an even step count since the phase
+  // began, the second at an odd one, so each captured step's Z buffer is static: Zbuf[slot])
   if (!graph) CU(c, cudaStreamWaitEvent(c->stream, c->ev_zready[slot], 0));
   const int64_t ntl = (c->Pl + PR_TILE - 1) / PR_TILE;
   PROF_BEGIN(c);
