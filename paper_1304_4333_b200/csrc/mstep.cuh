@@ -623,8 +623,8 @@ __global__ void __launch_bounds__(256) k_accept_tile(AccArgs a) {
   __shared__ int red_i[32];
   const bool tr = a.trace && blockIdx.x == 0 && threadIdx.x == 0;
   if (tr) a.trace[64] = gtimer();
-  if (a.stop && *a.stop) return;
-  if (a.decide) tl_start(3);
+  const bool early = a.logualt == nullptr;  // static log-u buffer: loads issued before the stop flag is read
+  if (!early && a.stop && *a.stop) return;
   const int d = a.d, tp = a.tp, lane = threadIdx.x & 31, w = threadIdx.x >> 5, ar = lane >> 2, ac = lane & 3;
   const int TD = tp * d;
   const bool dec = a.decide != 0;
@@ -647,6 +647,11 @@ __global__ void __launch_bounds__(256) k_accept_tile(AccArgs a) {
       if (logu) bulk_g2s(sv + 3 * tp, logu + pbase, vb, &bar);
     }
   }
+  if (early && a.stop && *a.stop) {  // speculative step after the stop: drain the loads, exit
+    if (threadIdx.x == 0) mbar_wait(&bar, 0u);
+    return;
+  }
+  if (a.decide) tl_start(3);
   double shv[NT];  // c_i of this lane's fragment columns
 #pragma unroll
   for (int t = 0; t < NT; ++t) {

@@ -734,11 +734,7 @@ sps_status accept_moments(sps_ctx* c, bool decide, int nchunks, double temper, u
   a.pass = (uint32_t)c->cfg.pass;
   a.dmagic = ((1ull << 32) + (uint64_t)c->d - 1) / (uint64_t)c->d;
   a.trace = decide ? c->trace : nullptr;
-  if (c->capturing_loop && logu) {
-    a.logu = c->LUbuf[0];
-    a.logualt = c->LUbuf[1];
-    a.step0 = c->phase_step0;
-  }
+  // (device-side loop: each captured step's log-u buffer is static -- LUbuf[step & 1] -- like its Z)
   PROF_BEGIN(c);
   if (c->acc_tnt > 0) {  // tile layout: bulk-staged rows, on-the-fly DMMA fragments, ones column
     switch (c->acc_tnt) {
