@@ -44,6 +44,10 @@ typedef enum {
 enum { SPS_DATA_TEMPERING = 0, SPS_POWER_TEMPERING = 1 };
 enum { SPS_RESIDUAL = 0, SPS_SYSTEMATIC = 1, SPS_MULTINOMIAL = 2 };
 
+/* Instantiated model shapes (sps_create fails with SPS_E_CONFIG otherwise): binary (C = 2)
+ * k <= 128 on the DMMA log-likelihood kernel; C = 3: k <= 16; C = 4: k <= 16; C = 5..8: k <= 8
+ * (DFMA kernels).  d = k (C - 1) <= 512; the register-blocked proposal / accept / warp-Cholesky
+ * path for d <= 32, generic kernels and a block Cholesky above. */
 typedef struct sps_config {
   int32_t n, k, C;         /* observations T, covariates k, outcomes C (2 <= C <= 8)        */
   int32_t J, N;            /* groups (global) and particles per group (N <= 16384)          */

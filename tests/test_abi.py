@@ -67,3 +67,11 @@ def test_config_defaults_are_the_papers(so):
     assert (cfg.ess_frac, cfg.K_inter, cfg.K_final) == (0.5, 0.35, 0.9)
     assert (cfg.h_init, cfg.h_step, cfg.h_min, cfg.h_max) == (50, 1, 10, 100)
     assert cfg.accept_target == 0.25 and cfg.nranks == 1
+
+
+def test_header_states_the_instantiated_shapes():
+    """The header documents which (k, C) the library instantiates (sps_create refuses others)."""
+    import os
+
+    h = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "sps.h")).read()
+    assert "k <= 128" in h and "C = 5..8: k <= 8" in h
