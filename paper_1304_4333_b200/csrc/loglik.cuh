@@ -360,21 +360,28 @@ __global__ void __launch_bounds__(LL_THREADS, 2) k_loglik_mnl(LLArgs a) {
     }
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
-      double m = 0.0, ey = 0.0;
+      // Unshifted form 1 + sum_c e^eta_c (the reference term is e^0 = 1): C-1 exps, no max.
+      // Exact as long as every |eta_c| < 704 (no overflow; v < 2^1019); otherwise the
+      // max-shifted form below (never taken for the prior / posterior scales of the configs).
+      double ey = 0.0, v = 1.0;
+      int big = 0;
 #pragma unroll
       for (int c = 0; c < CM1; ++c) {
-        m = fmax(m, eta[j][c]);
         ey = (yt == c + 1) ? eta[j][c] : ey;
+        big |= (__double2hiint(eta[j][c]) & 0x7fffffff) >= 0x40860000;  // |eta| >= 704, inf, nan
+        v += exp_neg(-eta[j][c], sT);
+      }
+      double m = 0.0;
+      if (big) {
+#pragma unroll
+        for (int c = 0; c < CM1; ++c) m = fmax(m, eta[j][c]);
+        v = exp_neg(abs_clamp708(m), sT);  // reference category, eta_0 = 0
+#pragma unroll
+        for (int c = 0; c < CM1; ++c) v += exp_neg(abs_clamp708(m - eta[j][c]), sT);
       }
       D[j] += m - ey;
-      double v = exp_neg(abs_clamp708(m), sT);  // reference category, eta_0 = 0
-#pragma unroll
-      for (int c = 0; c < CM1; ++c) v += exp_neg(abs_clamp708(m - eta[j][c]), sT);
       Pp[j] *= v;
-    }
-    if ((t & 63) == 63) {
-#pragma unroll
-      for (int j = 0; j < PPT; ++j) renorm(Pp[j], E[j]);
+      renorm(Pp[j], E[j]);  // v can reach ~C e^704: keep Pp in [1, 2) every observation (ALU only)
     }
   }
 #pragma unroll

@@ -481,6 +481,8 @@ bool choose_ll(int k, int C, LLChoice* o) {
     return false;
   }
   if (cm1 == 3) {
+    static const bool ppt2 = getenv("SPS_MNL_PPT2") != nullptr;  // A/B hook: 2 particles per thread
+    if (ppt2 && k <= 12) return pick_exact<3, 2>(k, o, std::make_integer_sequence<int, 12>{});
     if (k <= 16) return pick_exact<3, 1>(k, o, std::make_integer_sequence<int, 16>{});
     return false;
   }

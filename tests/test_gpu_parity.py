@@ -148,6 +148,24 @@ def test_loglik_extreme_and_degenerate(sps, orc):
     assert np.allclose(got[-8:], -n * math.log(2), rtol=1e-14)
 
 
+@pytest.mark.parametrize("C", [3, 4, 6])
+def test_loglik_multinomial_extreme(sps, orc, C):
+    """Multinomial K1: the unshifted 1 + sum e^eta form for |eta| < 704 and the max-shifted
+    fallback (|eta| >= 704 in some class) on the same observations; theta = 0 -> -n log C."""
+    rng = np.random.default_rng(70 + C)
+    n, k = 150, 4
+    X = np.column_stack([np.ones(n), rng.normal(size=(n, k - 1))])
+    y = rng.integers(0, C, n).astype(np.int32)
+    d = k * (C - 1)
+    theta = np.concatenate([rng.normal(0, 30, (64, d)),     # |eta| up to ~200: large products of v
+                            rng.normal(0, 400, (16, d)),    # |eta| > 704: shifted fallback
+                            np.zeros((8, d))])
+    theta[64:72, 0] = 705.0  # one class just past the switch, the rest moderate
+    theta[64:72, 1:] = rng.normal(0, 0.1, (8, d - 1))
+    got, _ = _loglik_case(sps, orc, X, y, C, theta, 0, n)
+    assert np.allclose(got[-8:], -n * math.log(C), rtol=1e-14)
+
+
 def test_loglik_full_size_cfg2_sampled(sps, orc):
     """configs[1] at full size (P = 65536, n = 1000) in the bench launch
     configuration; 512 sampled particles recomputed by the oracle."""

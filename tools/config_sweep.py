@@ -79,9 +79,12 @@ def oracle_loglik(X, y, C, P, d):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--no-oracle", action="store_true")
+    ap.add_argument("--only", default=None, help="one of cfg1..cfg4, cfg5 (skip the rest)")
     a = ap.parse_args()
     out = {"gpu": torch.cuda.get_device_name(0), "host_threads": os.cpu_count(), "configs": {}}
     for name in ("cfg1", "cfg2", "cfg3", "cfg4"):
+        if a.only and a.only != name:
+            continue
         c = sps_synth.CONFIGS[name]
         X, y = sps_synth.config_data(name)
         n, k = X.shape
@@ -108,6 +111,9 @@ def main():
         out["configs"][name] = ent
         print(name, json.dumps(ent), file=sys.stderr, flush=True)
     # configs[4]: particle sweep at the cfg2 shape
+    if a.only and a.only != "cfg5":
+        print(json.dumps(out, indent=1))
+        return
     X, y = sps_synth.config_data("cfg2")
     cov = sps.g_prior(X, 2, 1.0 / 16)
     sweep = {}
