@@ -12,10 +12,11 @@
 //  * The epilogue dominates with libm (log1p(exp) = ~84 DFMA-equivalents,
 //    measured).  Here: log p = -(max(s,0) + log(1 + e^-|s|)) for binary with
 //    s = (1-2y) x'theta (y folded into a sign-flipped copy of X), and
-//    log p = (eta_y - m) - log(sum_c e^(eta_c - m)) for C > 2.  The logs are
-//    deferred: the factors (1 + e^-|s|) / sum_c e^(eta_c-m) in [1, C] are
-//    multiplied into a running product with its exponent renormalized every
-//    64 observations, and ONE log per particle is taken at the end.  e^-a is
+//    log p = eta_y - log(1 + sum_c e^eta_c) for C > 2 (max-shifted only when
+//    some |eta_c| >= 704).  The logs are deferred: the factors (1 + e^-|s|)
+//    in [1, 2] / 1 + sum_c e^eta_c are multiplied into a running product with
+//    its exponent renormalized every 64 (binary) / every (C > 2) observation,
+//    and ONE log per particle is taken at the end.  e^-a is
 //    a table-driven exp (2^(i/64) table in smem, degree-5 polynomial on
 //    |r| <= ln2/128, one-fma range reduction): 9 FP64 ops.  Binary total (DMMA kernel): 11 FP64
 //    ops per pair + k FMAs (exp 9, Pp (1 + e) as one fma, + relu).
@@ -179,6 +180,14 @@ __device__ __forceinline__ double exp_neg256(double a, const double* __restrict_
   return fma(Ts, q, Ts);
 }
 
+template <int TAB>
+__device__ __forceinline__ double exp_neg_tab(double a, const double* __restrict__ sT) {
+  if constexpr (TAB == 256)
+    return exp_neg256(a, sT);
+  else
+    return exp_neg(a, sT);
+}
+
 // Split a positive running product into mantissa in [1,2) and exponent count.
 __device__ __forceinline__ void renorm(double& Pp, int& E) {
   const int hi = __double2hiint(Pp);
@@ -299,19 +308,20 @@ __global__ void __launch_bounds__(LL_THREADS, 2) k_loglik_bin(LLArgs a) {
 // ---------------------------------------------------------------------------
 // Multinomial (C = CM1 + 1 >= 3): eta_0 = 0, eta_c = theta_c' x_t;
 // log p = (eta_y - m) - log(sum_c e^(eta_c - m)), m = max_c eta_c.
-template <int K, int CM1, int PPT>
+// TAB: exp table 2^(j/64) (9-op exp) or 2^(j/256) (8-op exp; the host reserves 256 doubles).
+template <int K, int CM1, int PPT, int TAB = 64>
 __global__ void __launch_bounds__(LL_THREADS, 2) k_loglik_mnl(LLArgs a) {
   constexpr int LDX = ldx_of<K>();
   extern __shared__ __align__(16) double smem[];
   if (a.stop && *a.stop) return;
   griddep_wait();  // launched with PDL: theta (the proposal kernel's output) after this
   double* sT = smem;
-  double* sX = smem + 64;
+  double* sX = smem + TAB;
   const int c0 = a.t0 + blockIdx.y * a.chunk;
   const int c1 = min(c0 + a.chunk, a.t1);
   const int nobs = max(c1 - c0, 0);
   int* sY = reinterpret_cast<int*>(sX + (size_t)a.chunk * LDX);
-  for (int i = threadIdx.x; i < 64; i += blockDim.x) sT[i] = c_exp2tab[i];
+  for (int i = threadIdx.x; i < TAB; i += blockDim.x) sT[i] = TAB == 256 ? c_exp2tab256[i] : c_exp2tab[i];
   {
     const double2* src = reinterpret_cast<const double2*>(a.X + (int64_t)c0 * LDX);
     double2* dst = reinterpret_cast<double2*>(sX);
@@ -369,17 +379,18 @@ __global__ void __launch_bounds__(LL_THREADS, 2) k_loglik_mnl(LLArgs a) {
       for (int c = 0; c < CM1; ++c) {
         ey = (yt == c + 1) ? eta[j][c] : ey;
         big |= (__double2hiint(eta[j][c]) & 0x7fffffff) >= 0x40860000;  // |eta| >= 704, inf, nan
-        v += exp_neg(-eta[j][c], sT);
+        v += exp_neg_tab<TAB>(-eta[j][c], sT);
       }
-      double m = 0.0;
+      D[j] -= ey;
       if (big) {
+        double m = 0.0;
 #pragma unroll
         for (int c = 0; c < CM1; ++c) m = fmax(m, eta[j][c]);
-        v = exp_neg(abs_clamp708(m), sT);  // reference category, eta_0 = 0
+        v = exp_neg_tab<TAB>(abs_clamp708(m), sT);  // reference category, eta_0 = 0
 #pragma unroll
-        for (int c = 0; c < CM1; ++c) v += exp_neg(abs_clamp708(m - eta[j][c]), sT);
+        for (int c = 0; c < CM1; ++c) v += exp_neg_tab<TAB>(abs_clamp708(m - eta[j][c]), sT);
+        D[j] += m;
       }
-      D[j] += m - ey;
       Pp[j] *= v;
       renorm(Pp[j], E[j]);  // v can reach ~C e^704: keep Pp in [1, 2) every observation (ALU only)
     }
@@ -407,13 +418,6 @@ __global__ void __launch_bounds__(LL_THREADS, 2) k_loglik_mnl(LLArgs a) {
 // Lane l holds C[obs = l/4][particle = 2 (l%4) + e] of every n-tile; two
 // observation tiles are folded into each product update; per-lane running
 // sums are combined over the 8 lanes of a particle column at the end.
-template <int TAB>
-__device__ __forceinline__ double exp_neg_tab(double a, const double* __restrict__ sT) {
-  if constexpr (TAB == 256)
-    return exp_neg256(a, sT);
-  else
-    return exp_neg(a, sT);
-}
 
 // H: 8-observation tiles folded into one product update (1 or 2); TAB: exp table size (64 or 256);
 // KS: independent DMMA accumulator chains over k (1 or 2); MINB: min resident blocks (register budget).
