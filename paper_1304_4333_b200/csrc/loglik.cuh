@@ -309,8 +309,8 @@ __global__ void __launch_bounds__(LL_THREADS, 2) k_loglik_bin(LLArgs a) {
 // Multinomial (C = CM1 + 1 >= 3): eta_0 = 0, eta_c = theta_c' x_t;
 // log p = (eta_y - m) - log(sum_c e^(eta_c - m)), m = max_c eta_c.
 // TAB: exp table 2^(j/64) (9-op exp) or 2^(j/256) (8-op exp; the host reserves 256 doubles).
-template <int K, int CM1, int PPT, int TAB = 64>
-__global__ void __launch_bounds__(LL_THREADS, 2) k_loglik_mnl(LLArgs a) {
+template <int K, int CM1, int PPT, int TAB = 64, int MINB = 2>
+__global__ void __launch_bounds__(LL_THREADS, MINB) k_loglik_mnl(LLArgs a) {
   constexpr int LDX = ldx_of<K>();
   extern __shared__ __align__(16) double smem[];
   if (a.stop && *a.stop) return;

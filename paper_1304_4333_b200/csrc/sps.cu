@@ -394,12 +394,12 @@ sps_status read_ctl(sps_ctx* c) {
 }
 
 // ------------------------------------------------------------------ K1 dispatch
-template <int K, int CM1, int PPT, int TAB = 64>
+template <int K, int CM1, int PPT, int TAB = 64, int MINB = 2>
 LLKernel ll_ptr() {
   if constexpr (CM1 == 1)
     return k_loglik_bin<K, PPT>;
   else
-    return k_loglik_mnl<K, CM1, PPT, TAB>;
+    return k_loglik_mnl<K, CM1, PPT, TAB, MINB>;
 }
 
 // Instantiated shapes: binary k = 1..32 (PPT 2) and {40,48,56,64} (PPT 1);
@@ -407,10 +407,10 @@ LLKernel ll_ptr() {
 // Other k round up to the next instantiated KT (zero padding in X and theta loads).
 using LLChoice = LLChoice_t;
 
-template <int CM1, int PPT, int TAB = 64, int... Ks>
+template <int CM1, int PPT, int TAB = 64, int MINB = 2, int... Ks>
 bool pick_exact(int k, LLChoice* out, std::integer_sequence<int, Ks...>) {
   bool found = false;
-  ((k == Ks + 1 && !found ? (out->fn = ll_ptr<Ks + 1, CM1, PPT, TAB>(), out->KT = Ks + 1, out->PPT = PPT, found = true)
+  ((k == Ks + 1 && !found ? (out->fn = ll_ptr<Ks + 1, CM1, PPT, TAB, MINB>(), out->KT = Ks + 1, out->PPT = PPT, found = true)
                           : false),
    ...);
   return found;
@@ -483,6 +483,8 @@ bool choose_ll(int k, int C, LLChoice* o) {
   if (cm1 == 3) {
     static const bool tab256 = getenv("SPS_MNL_TAB256") != nullptr;  // A/B hook: 2^(j/256) exp table
     if (tab256 && k <= 16) return pick_exact<3, 1, 256>(k, o, std::make_integer_sequence<int, 16>{});
+    static const bool minb5 = getenv("SPS_MNL_MINB5") != nullptr;  // A/B hook: <= 102 registers, 5 blocks / SM
+    if (minb5 && k <= 16) return pick_exact<3, 1, 64, 5>(k, o, std::make_integer_sequence<int, 16>{});
     if (k <= 16) return pick_exact<3, 1>(k, o, std::make_integer_sequence<int, 16>{});
     return false;
   }
