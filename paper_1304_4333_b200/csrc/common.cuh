@@ -157,7 +157,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // Debug timeline (SPS_TIMELINE): per M step (row = *g_tl_steps, the step
 // index within the phase) and kernel slot k, [2k] = start of block (0,0),
 // [2k+1] = latest block end (atomicMax).  Null when disabled.
-constexpr int TL_W = 24, TL_ROWS = 4096;
+constexpr int TL_W = 28, TL_ROWS = 4096;
 __device__ unsigned long long* g_tl = nullptr;
 __device__ const int* g_tl_steps = nullptr;
 __device__ __forceinline__ void tl_start(int k) {
@@ -179,6 +179,13 @@ __device__ __forceinline__ void tl_mark(int slot) {  // block (0,0) thread 0: a 
   if (tl && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
     const int r = *g_tl_steps;
     if (r >= 0 && r < TL_ROWS) tl[r * TL_W + slot] = gtimer();
+  }
+}
+__device__ __forceinline__ void tl_max(int slot) {  // thread 0 of every block: latest clock in slot 24..27
+  unsigned long long* tl = g_tl;
+  if (tl && threadIdx.x == 0) {
+    const int r = *g_tl_steps;
+    if (r >= 0 && r < TL_ROWS) atomicMax(&tl[r * TL_W + slot], gtimer());
   }
 }
 __device__ __forceinline__ void tl_end(int k) {

@@ -435,6 +435,7 @@ __global__ void __launch_bounds__(128, MINB) k_loglik_bin_mma(LLArgs a) {
   }
   if (a.stop && *a.stop) return;
   tl_start(2);
+  tl_max(24);  // latest block start (the last wave)
 #pragma unroll
   for (int u = 0; u < (TAB + 127) / 128; ++u) {
     const int i = threadIdx.x + 128 * u;
@@ -449,6 +450,7 @@ __global__ void __launch_bounds__(128, MINB) k_loglik_bin_mma(LLArgs a) {
   }
   __syncthreads();
   griddep_wait();  // theta* (the proposal kernel's output) from here on
+  tl_mark(25);     // block (0,0): dependency released
   int it = 0;            // sub-chunk loads issued so far (mbarrier phases)
   int held_chunk = -1;   // chunk whose single sub-chunk is resident in buffer held_buf
   int held_buf = 0;
@@ -490,6 +492,12 @@ __global__ void __launch_bounds__(128, MINB) k_loglik_bin_mma(LLArgs a) {
     }
   }
   __syncthreads();
+  if (g_tl) {  // block (0,0): theta fragments loaded (a move of the last-loaded value waits on its scoreboard)
+    unsigned long long dep;
+    asm volatile("mov.b64 %0, %1;" : "=l"(dep) : "d"(b[NTW - 1][KKD > 0 ? KKD - 1 : 0] + tr[NTW - 1][1][0]) : "memory");
+    if (dep != 1ull) tl_mark(26);
+    else tl_mark(26);
+  }
   double M[NTW][2], Pp[NTW][2];
   int E[NTW][2];
 #pragma unroll
@@ -657,6 +665,7 @@ __global__ void __launch_bounds__(128, MINB) k_loglik_bin_mma(LLArgs a) {
     }
   }
   }  // items
+  tl_mark(27);  // block (0,0): done
   griddep_launch();
   tl_end(2);
 }

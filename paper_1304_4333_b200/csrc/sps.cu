@@ -152,7 +152,7 @@ struct sps_ctx {
   unsigned long long* tl = nullptr;     // debug (SPS_TIMELINE): per-step kernel start / end clocks
   double tl_acc[24] = {};
   int tl_rows = 0;
-  double tl_bin[6][4] = {};  // by t_l bin (<=32, <=64, <=128, <=256, <=512, >512): steps, K1 span, step span, gap
+  double tl_bin[6][8] = {};  // by t_l bin (<=32, <=64, <=128, <=256, <=512, >512): steps, K1 span, step span, gap
   double trace_acc[80] = {};
   int trace_n = 0;
   double* Zbuf[2] = {nullptr, nullptr};  // standard normals, one M step ahead (side stream)
@@ -1414,9 +1414,13 @@ sps_status sps_get_counters(const sps_ctx* cc, sps_counters* out) {
     static const char* bn[] = {"t<=32", "t<=64", "t<=128", "t<=256", "t<=512", "t>512"};
     for (int b = 0; b < 6; ++b)
       if (c->tl_bin[b][0] > 0)
-        fprintf(stderr, "SPS_TIMELINE %-7s steps %5.0f  K1 %7.2f us  step %7.2f us  gap %5.2f us\n", bn[b], c->tl_bin[b][0],
-                c->tl_bin[b][1] / c->tl_bin[b][0] / 1e3, c->tl_bin[b][2] / c->tl_bin[b][0] / 1e3,
-                c->tl_bin[b][3] / c->tl_bin[b][0] / 1e3);
+        fprintf(stderr,
+                "SPS_TIMELINE %-7s steps %5.0f  K1 %7.2f us  step %7.2f us  gap %5.2f us  K1 blk0: release %.2f theta %.2f "
+                "rest %.2f  last block start %.2f\n",
+                bn[b], c->tl_bin[b][0], c->tl_bin[b][1] / c->tl_bin[b][0] / 1e3, c->tl_bin[b][2] / c->tl_bin[b][0] / 1e3,
+                c->tl_bin[b][3] / c->tl_bin[b][0] / 1e3, c->tl_bin[b][4] / c->tl_bin[b][0] / 1e3,
+                c->tl_bin[b][5] / c->tl_bin[b][0] / 1e3, c->tl_bin[b][6] / c->tl_bin[b][0] / 1e3,
+                c->tl_bin[b][7] / c->tl_bin[b][0] / 1e3);
   }
   out->launches = c->launches;
   out->k1_launches = c->k1_launches;
@@ -1696,6 +1700,12 @@ static sps_status timeline_accumulate(sps_ctx* c, int R) {
       c->tl_bin[b][1] += (double)(t[5] - t[4]);
       c->tl_bin[b][2] += (double)(t[11] - t[0]);
       if (r + 1 < rows && h[(size_t)(r + 1) * TL_W]) c->tl_bin[b][3] += (double)h[(size_t)(r + 1) * TL_W] - (double)t[11];
+      if (t[24] && t[25] && t[26] && t[27]) {  // K1 phases: block (0,0) release / theta loaded / done, last block start
+        c->tl_bin[b][4] += (double)t[25] - (double)t[4];
+        c->tl_bin[b][5] += (double)t[26] - (double)t[25];
+        c->tl_bin[b][6] += (double)t[27] - (double)t[26];
+        c->tl_bin[b][7] += (double)t[24] - (double)t[4];
+      }
     }
     if (t[16] && t[17] && t[18] && t[19] && t[20]) {  // finalize phases: stage / theta-bar / V / chol|RNE / tail
       c->tl_acc[18] += (double)t[16] - (double)t[10];
