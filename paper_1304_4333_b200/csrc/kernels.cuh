@@ -251,73 +251,94 @@ __global__ void __launch_bounds__(256) k_functional_stats(const double* __restri
 // ============================================================ C phase, data tempering (K2/K3)
 // K2: cumulative log weights over observations [s0, s0 + B) for every
 // particle (PAPER.md:281-295 eq. C_phase_compute in log form):
-// lwbuf[b][p] = lw_p(s0 + b + 1).  theta staged transposed in shared memory.
-__global__ void __launch_bounds__(128) k_cphase_scan(const double* __restrict__ Xs, const int32_t* __restrict__ y,
-                                                     int ldx, int k, int C, const double* __restrict__ theta, int d,
-                                                     int64_t P, int s0, int B, double* __restrict__ lw_cur,
-                                                     double* __restrict__ lwbuf) {
-  extern __shared__ double sth[];  // d x blockDim (transposed)
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool valid = p < P;
-  for (int i = 0; i < d; ++i) sth[i * blockDim.x + threadIdx.x] = valid ? theta[p * d + i] : 0.0;
+// lwbuf[b][p] = lw_p(s0 + b + 1).  A block holds SCAN_PB particles and
+// SCAN_Q warps: warp q evaluates log p(y_t | theta_p) for its contiguous
+// quarter of the chunk (the latency-bound exp/log1p chains spread over 4x the
+// threads) and stores the terms; then one warp accumulates them per particle
+// in observation order (the same serial sum as one thread per particle).
+// theta staged transposed in shared memory (d x SCAN_PB).
+constexpr int SCAN_PB = 32, SCAN_Q = 4;
+
+__device__ __forceinline__ double scan_term_bin(const double* __restrict__ x, const double* __restrict__ sth, int k,
+                                                int pl) {
+  double a0 = 0.0, a1 = 0.0;
+  int i = 0;
+  for (; i + 2 <= k; i += 2) {
+    a0 = fma(sth[i * SCAN_PB + pl], __ldg(x + i), a0);
+    a1 = fma(sth[(i + 1) * SCAN_PB + pl], __ldg(x + i + 1), a1);
+  }
+  if (i < k) a0 = fma(sth[i * SCAN_PB + pl], __ldg(x + i), a0);
+  const double s = a0 + a1;
+  return -(fmax(s, 0.0) + log1p(exp(-fabs(s))));
+}
+
+__global__ void __launch_bounds__(SCAN_PB * SCAN_Q) k_cphase_scan(
+    const double* __restrict__ Xs, const int32_t* __restrict__ y, int ldx, int k, int C,
+    const double* __restrict__ theta, int d, int64_t P, int s0, int B, double* __restrict__ lw_cur,
+    double* __restrict__ lwbuf) {
+  extern __shared__ double sth[];  // d x SCAN_PB (transposed)
+  const int pl = threadIdx.x % SCAN_PB, q = threadIdx.x / SCAN_PB;
+  const int64_t p0 = (int64_t)blockIdx.x * SCAN_PB;
+  const int np = (int)min((int64_t)SCAN_PB, P - p0);
+  for (int e = threadIdx.x; e < d * SCAN_PB; e += blockDim.x) {
+    const int i = e / SCAN_PB, j = e % SCAN_PB;
+    sth[e] = j < np ? theta[(p0 + j) * d + i] : 0.0;
+  }
   __syncthreads();
-  if (!valid) return;
+  const int64_t p = p0 + pl;
+  const bool valid = pl < np;
+  const int per = (B + SCAN_Q - 1) / SCAN_Q;
+  const int b0 = min(B, q * per), b1 = min(B, b0 + per);
+  if (valid) {
+    int b = b0;
+    if (C == 2) {  // binary: two observations per iteration (ILP)
+      for (; b + 2 <= b1; b += 2) {
+        const double* x0 = Xs + (int64_t)(s0 + b) * ldx;
+        const double la = scan_term_bin(x0, sth, k, pl);
+        const double lc = scan_term_bin(x0 + ldx, sth, k, pl);
+        lwbuf[(int64_t)b * P + p] = la;
+        lwbuf[(int64_t)(b + 1) * P + p] = lc;
+      }
+      if (b < b1) lwbuf[(int64_t)b * P + p] = scan_term_bin(Xs + (int64_t)(s0 + b) * ldx, sth, k, pl);
+    } else {
+      for (; b < b1; ++b) {
+        const int t = s0 + b;
+        const double* x = Xs + (int64_t)t * ldx;
+        double eta[8];
+        eta[0] = 0.0;
+        double m = 0.0;
+        for (int c = 1; c < C; ++c) {
+          double s = 0.0;
+          for (int i = 0; i < k; ++i) s = fma(sth[((c - 1) * k + i) * SCAN_PB + pl], __ldg(x + i), s);
+          eta[c] = s;
+          m = fmax(m, s);
+        }
+        int cstar = 0;
+        for (int c = 1; c < C; ++c)
+          if (eta[c] > eta[cstar]) cstar = c;
+        double rest = 0.0;
+        for (int c = 0; c < C; ++c)
+          if (c != cstar) rest += exp(eta[c] - m);
+        lwbuf[(int64_t)b * P + p] = (eta[y[t]] - m) - log1p(rest);
+      }
+    }
+  }
+  __syncthreads();  // the block's terms (global, written by this block) visible to warp 0
+  if (q != 0 || !valid) return;
   double lw = lw_cur[p];
   int b = 0;
-  if (C == 2) {  // binary: two observations per iteration, two accumulators each (latency-bound: ILP)
-    for (; b + 2 <= B; b += 2) {
-      const double* x0 = Xs + (int64_t)(s0 + b) * ldx;
-      const double* x1 = x0 + ldx;
-      double a0 = 0.0, a1 = 0.0, c0 = 0.0, c1 = 0.0;
-      int i = 0;
-      for (; i + 2 <= k; i += 2) {
-        const double t0 = sth[i * blockDim.x + threadIdx.x], t1 = sth[(i + 1) * blockDim.x + threadIdx.x];
-        a0 = fma(t0, __ldg(x0 + i), a0);
-        a1 = fma(t1, __ldg(x0 + i + 1), a1);
-        c0 = fma(t0, __ldg(x1 + i), c0);
-        c1 = fma(t1, __ldg(x1 + i + 1), c1);
-      }
-      if (i < k) {
-        const double t0 = sth[i * blockDim.x + threadIdx.x];
-        a0 = fma(t0, __ldg(x0 + i), a0);
-        c0 = fma(t0, __ldg(x1 + i), c0);
-      }
-      const double sa = a0 + a1, sc = c0 + c1;
-      const double la = -(fmax(sa, 0.0) + log1p(exp(-fabs(sa))));
-      const double lc = -(fmax(sc, 0.0) + log1p(exp(-fabs(sc))));
-      lw += la;
-      lwbuf[(int64_t)b * P + p] = lw;
-      lw += lc;
-      lwbuf[(int64_t)(b + 1) * P + p] = lw;
+  for (; b + 8 <= B; b += 8) {  // loads batched ahead of the serial adds
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = lwbuf[(int64_t)(b + u) * P + p];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      lw += v[u];
+      lwbuf[(int64_t)(b + u) * P + p] = lw;
     }
   }
   for (; b < B; ++b) {
-    const int t = s0 + b;
-    const double* x = Xs + (int64_t)t * ldx;
-    double lpt;
-    if (C == 2) {
-      double s = 0.0;
-      for (int i = 0; i < k; ++i) s = fma(sth[i * blockDim.x + threadIdx.x], __ldg(x + i), s);
-      lpt = -(fmax(s, 0.0) + log1p(exp(-fabs(s))));
-    } else {
-      double eta[8];
-      eta[0] = 0.0;
-      double m = 0.0;
-      for (int c = 1; c < C; ++c) {
-        double s = 0.0;
-        for (int i = 0; i < k; ++i) s = fma(sth[((c - 1) * k + i) * blockDim.x + threadIdx.x], __ldg(x + i), s);
-        eta[c] = s;
-        m = fmax(m, s);
-      }
-      int cstar = 0;
-      for (int c = 1; c < C; ++c)
-        if (eta[c] > eta[cstar]) cstar = c;
-      double rest = 0.0;
-      for (int c = 0; c < C; ++c)
-        if (c != cstar) rest += exp(eta[c] - m);
-      lpt = (eta[y[t]] - m) - log1p(rest);
-    }
-    lw += lpt;
+    lw += lwbuf[(int64_t)b * P + p];
     lwbuf[(int64_t)b * P + p] = lw;
   }
   lw_cur[p] = lw;

@@ -1522,12 +1522,12 @@ sps_status sps_cphase(sps_ctx* c, int32_t t_target, double phi_target, int32_t* 
     int B = 8;  // first galloping chunk: twice the last cycle's advance (usually one chunk, one sync)
     while (B < 2 * c->last_adv && B < c->Bmax) B *= 2;
     const int ntiles = (int)((Pl + ESS_TILE - 1) / ESS_TILE);
-    const size_t scan_smem = sizeof(double) * c->d * 128;
+    const size_t scan_smem = sizeof(double) * c->d * SCAN_PB;
     CU(c, cudaFuncSetAttribute(k_cphase_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem + 1024));
     for (;;) {
       int Be = std::min(std::min(B, c->Bmax), c->n - s);
       if (t_target >= 0) Be = std::min(Be, t_target - s);
-      k_cphase_scan<<<(unsigned)((Pl + 127) / 128), 128, scan_smem, c->stream>>>(
+      k_cphase_scan<<<(unsigned)((Pl + SCAN_PB - 1) / SCAN_PB), SCAN_PB * SCAN_Q, scan_smem, c->stream>>>(
           c->Xs, c->y, c->ldx, c->k, c->C, c->theta, c->d, Pl, s, Be, c->lw_cur, c->lwbuf);
       CHECK_LAUNCH(c);
       c->pairs += P * Be;
