@@ -285,3 +285,36 @@ def test_predictive_api(sps, orc):
     with pytest.raises(sps.SpsError):
         s.predictive(0, 1)
     s.close()
+
+
+@pytest.mark.parametrize("C", [2, 3])
+def test_cphase_scan_ragged_chunks(sps, orc, C):
+    """Data-tempering C phase (K2 scan + K3 ESS) on a fixed schedule whose chunks are 1, 3, 7, 15
+    and 34 observations (chunk quarters empty, ragged and uneven) over J x N = 3 x 11 particles
+    (a partial particle block): after each C + S phase every particle's L equals its ancestor's L
+    plus the oracle's log-likelihood of the absorbed observations, and the log-ML increment is the
+    pooled log mean weight."""
+    rng = np.random.default_rng(500 + C)
+    n, k = 60, 5
+    X = np.column_stack([np.ones(n), rng.normal(size=(n, k - 1))])
+    y = rng.integers(0, C, n).astype(np.int32)
+    d = k * (C - 1)
+    s = sps.Sps(X, y, np.zeros(d), 0.25 * np.eye(d), J=3, N=11, seed=9, C_=C)
+    try:
+        t_prev = 0
+        th0, L0, _ = s.particles()
+        for t in [1, 4, 11, 26, 60]:
+            t_new, _, inc = s.cphase(t_target=t)
+            assert t_new == t
+            lw = orc.loglik_range(th0, X, y, C, t_prev, t)
+            want_inc = np.logaddexp.reduce(lw) - math.log(lw.size)
+            assert abs(inc - want_inc) <= 1e-9 * max(1.0, abs(want_inc))
+            th1, L1, _ = s.particles()
+            for i in range(th1.shape[0]):
+                a = np.flatnonzero(np.all(th0 == th1[i], axis=1))
+                assert a.size >= 1, "resampled particle is not a copy of an ancestor"  # copies share L
+                want = L0[a[0]] + lw[a[0]]
+                assert abs(L1[i] - want) <= LL_RTOL * abs(want) + 1e-12
+            th0, L0, t_prev = th1, L1, t
+    finally:
+        s.close()
