@@ -253,11 +253,12 @@ __global__ void __launch_bounds__(256) k_functional_stats(const double* __restri
 // particle (PAPER.md:281-295 eq. C_phase_compute in log form):
 // lwbuf[b][p] = lw_p(s0 + b + 1).  A block holds SCAN_PB particles and
 // SCAN_Q warps: warp q evaluates log p(y_t | theta_p) for its contiguous
-// quarter of the chunk (the latency-bound exp/log1p chains spread over 4x the
-// threads) and stores the terms; then one warp accumulates them per particle
+// 1/SCAN_Q of the chunk (the latency-bound exp/log1p chains spread over
+// SCAN_Q x the threads; cfg2 C phase per run: 9.8 ms at 1 warp, 8.9 at 4, 8.6
+// at 8, 8.7 at 16) and stores the terms; then one warp accumulates them per particle
 // in observation order (the same serial sum as one thread per particle).
 // theta staged transposed in shared memory (d x SCAN_PB).
-constexpr int SCAN_PB = 32, SCAN_Q = 4;
+constexpr int SCAN_PB = 32, SCAN_Q = 8;
 
 __device__ __forceinline__ double scan_term_bin(const double* __restrict__ x, const double* __restrict__ sth, int k,
                                                 int pl) {
