@@ -411,28 +411,46 @@ __global__ void k_ess_rank(const double* __restrict__ parts, int ntiles, int B, 
 // every absorbed observation (R18): lse[s] = log sum_p w_p^(s) =
 // M + log S1, logpl[s-1] = lse[s] - lse[s-1], with lse[t_start] = log P (the weights
 // are all 1 after the last S phase).
+// One warp: lane i takes observation base + i of each 32-observation round (the rank
+// combine, the log and the ESS test in parallel); the first crossing is the lowest
+// set lane of a ballot; lse / logpl are written up to it (same values as a serial
+// loop: the previous observation's lse comes from the neighbour lane).
 __global__ void k_ess_final(const double* __restrict__ gath, int G, int B, int s0, int n, double ess_frac, double P,
                             Ctl* ctl, int t_fix, int t_start, double* __restrict__ lse, double* __restrict__ logpl) {
-  if (threadIdx.x != 0) return;
-  ctl->s_star = -1;
-  for (int b = 0; b < B; ++b) {
+  const int lane = threadIdx.x;
+  double carry = lse && s0 != t_start ? lse[s0] : 0.0;  // lse of the observation before the round
+  for (int base = 0; base < B; base += 32) {
+    const int b = base + lane;
+    const bool in = b < B;
     double M = -INFINITY, S1 = 0.0, S2 = 0.0;
-    for (int r = 0; r < G; ++r) {
-      const double* o = gath + ((int64_t)r * B + b) * 3;
-      combine3(M, S1, S2, o[0], o[1], o[2]);
-    }
+    if (in)
+      for (int r = 0; r < G; ++r) {
+        const double* o = gath + ((int64_t)r * B + b) * 3;
+        combine3(M, S1, S2, o[0], o[1], o[2]);
+      }
     const int s = s0 + b + 1;
+    const bool cross = in && (t_fix >= 0 ? s == t_fix : (S1 * S1 < ess_frac * P * S2 || s == n));
+    const unsigned bal = __ballot_sync(0xffffffffu, cross);
+    const int last = bal ? __ffs(bal) - 1 : 31;  // lanes <= last are absorbed this round
     if (lse) {
-      const double l = M + log(S1);
-      logpl[s - 1] = l - (s - 1 == t_start ? log(P) : lse[s - 1]);
-      lse[s] = l;
+      const double l = in ? M + log(S1) : 0.0;
+      double prev = __shfl_up_sync(0xffffffffu, l, 1);
+      if (lane == 0) prev = carry;
+      if (in && lane <= last) {
+        logpl[s - 1] = l - (s - 1 == t_start ? log(P) : prev);
+        lse[s] = l;
+      }
+      carry = __shfl_sync(0xffffffffu, l, 31);
     }
-    if (t_fix >= 0 ? s == t_fix : (S1 * S1 < ess_frac * P * S2 || s == n)) {
-      ctl->s_star = s;
-      ctl->ess = S1 * S1 / S2;
+    if (bal) {
+      if (lane == last) {
+        ctl->s_star = s;
+        ctl->ess = S1 * S1 / S2;
+      }
       return;
     }
   }
+  if (lane == 0) ctl->s_star = -1;  // no crossing in this chunk
 }
 
 // lw_p := lwbuf[b*][p] (the cycle's log weights), L_p += lw_p.
