@@ -713,12 +713,24 @@ __global__ void __launch_bounds__(1024) k_resample(const double* __restrict__ lw
 }
 
 // Pooled log-ML increment from all groups' (m_j, s_j) in group order (R10).
+// One warp: lanes take the max and the exps; lane 0 adds the terms in group order.
 __global__ void k_logml_pooled(const double* __restrict__ gath_ms, int J, double P, Ctl* ctl, double* inc_out) {
-  if (threadIdx.x != 0) return;
+  const int lane = threadIdx.x;
   double M = -INFINITY;
-  for (int j = 0; j < J; ++j) M = fmax(M, gath_ms[j * 2]);
+  for (int j = lane; j < J; j += 32) M = fmax(M, gath_ms[j * 2]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) M = fmax(M, __shfl_xor_sync(0xffffffffu, M, o));
   double S = 0.0;
-  for (int j = 0; j < J; ++j) S += gath_ms[j * 2 + 1] * exp(gath_ms[j * 2] - M);
+  for (int base = 0; base < J; base += 32) {
+    const int j = base + lane;
+    const double t = j < J ? gath_ms[j * 2 + 1] * exp(gath_ms[j * 2] - M) : 0.0;
+    const int cnt = min(32, J - base);
+    for (int u = 0; u < cnt; ++u) {
+      const double v = __shfl_sync(0xffffffffu, t, u);
+      if (lane == 0) S += v;
+    }
+  }
+  if (lane != 0) return;
   ctl->logml_inc = M + log(S / P);
   if (inc_out) *inc_out = ctl->logml_inc;  // per-cycle record, read by the host when needed
 }
