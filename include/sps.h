@@ -64,7 +64,7 @@ typedef struct sps_config {
   double accept_target;    /* 0.25                                            */
   int32_t max_m_steps;     /* 1000  per M phase (R13)                                       */
   int32_t max_cycles;      /* capacity of the per-cycle trace                               */
-  int32_t n_monitors;      /* rows of `monitors`; 0 -> default test functions (R12)         */
+  int32_t n_monitors;      /* rows of `monitors`; 0 -> default (R12): C-1 block means       */
   const double* monitors;  /* host, n_monitors x d row-major; copied by sps_create          */
   int32_t pass;            /* stream pass tag (Alg. 3); 0 for a one-pass run                */
   int32_t rank, nranks;    /* group sharding; nranks = 1 for a single GPU                   */
@@ -119,11 +119,18 @@ sps_status sps_create(const sps_config* cfg, const double* X, const int32_t* y, 
  * plogit, PAPER.md:233-242 factorization), p = 0..P-1.  theta_dev: device,
  * P rows of ld >= d doubles; out_dev: device, P doubles.  Both caller-owned,
  * not retained; enqueued on the context stream (not synchronized).  Local
- * (not collective).  Errors: SPS_E_CONFIG (ranges, ld < d). */
+ * (not collective).  Errors: SPS_E_CONFIG (ranges, ld < d), returned at once;
+ * a non-finite L_p (non-finite or overflowing theta: the model's terms are
+ * finite for finite eta) is detected on the device, located
+ * there, and returned by the next sps_sync as SPS_E_NUMERIC whose
+ * sps_last_error message names the first such particle p and its first
+ * non-finite observation t (the device-side check keeps this call async). */
 sps_status sps_loglik(sps_ctx* ctx, const double* theta_dev, int64_t P, int32_t ld, int32_t t0, int32_t t1,
                       double* out_dev);
 
-/* Block the host until all work enqueued on the context stream is done. */
+/* Block the host until all work enqueued on the context stream is done.
+ * Errors: SPS_E_NUMERIC for a non-finite sps_loglik result since the last sync
+ * (message: "particle p = ..., observation t = ..."), SPS_E_CUDA. */
 sps_status sps_sync(sps_ctx* ctx);
 
 /* One C phase followed by the S phase (Algorithm 1 step 2(a)-(b),
@@ -148,8 +155,9 @@ sps_status sps_mphase(sps_ctx* ctx, int32_t R_fixed, int32_t* R, double* min_rne
  * cap_cycles + arrays, n_report + report_fns; outputs as documented above. */
 sps_status sps_run(sps_ctx* ctx, sps_report* rep);
 
-/* Accumulated log marginal likelihood and its NSE across groups (R10). */
-sps_status sps_logml(sps_ctx* ctx, double* logml, double* nse);
+/* Accumulated log marginal likelihood and its NSE across groups (R10).  Does not
+ * change the sampler state (it pulls device-side increments into a host cache). */
+sps_status sps_logml(const sps_ctx* ctx, double* logml, double* nse);
 
 /* Posterior moments of m linear functionals a_i' theta (A: host, m x d) over the
  * current particles: grand mean, sd, NSE, RNE (R2). Collective. */

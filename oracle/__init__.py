@@ -59,6 +59,9 @@ class Report(C.Structure):
         ("mean", C.POINTER(C.c_double)), ("sd", C.POINTER(C.c_double)),
         ("nse", C.POINTER(C.c_double)), ("rne", C.POINTER(C.c_double)),
         ("logpl", C.POINTER(C.c_double)),
+        ("trace_cap", C.c_int32), ("step_nacc", C.POINTER(C.c_int32)), ("step_h", C.POINTER(C.c_int32)),
+        ("step_minrne", C.POINTER(C.c_double)), ("snap_cap", C.c_int32), ("theta_snap", C.POINTER(C.c_double)),
+        ("inc_group", C.POINTER(C.c_double)), ("Lj", C.POINTER(C.c_double)),
     ]
 
 
@@ -272,7 +275,22 @@ DEFAULTS = dict(tempering=DATA, resampling=RESIDUAL, ess_frac=0.5, K_inter=0.35,
 
 
 def default_monitors(X, C_):
-    """SPEC default test functions (R12): theta_c' xbar per block + mean of all coordinates."""
+    """Default test functions g* (R12): one per coefficient block c = 1..C-1, the block's coordinate
+    mean k^-1 sum_i theta_{c,i}; the M phase stops when the RNE of every monitor reaches K.  These are
+    not the log-odds functions of interest theta_c' xbar ("The monitoring functions are not the same as
+    the log-odds ratio functions of interest"), so the reported functionals' RNE can
+    fall below K (Table 5).  A few monitors, not all d coordinates: the minimum of d noisy J-group RNE
+    estimates almost never clears 0.9 (R12)."""
+    n, k = np.asarray(X).shape
+    d = k * (C_ - 1)
+    mon = np.zeros((C_ - 1, d))
+    for c in range(C_ - 1):
+        mon[c, c * k:(c + 1) * k] = 1.0 / k
+    return mon
+
+
+def xbar_functionals(X, C_):
+    """theta_c' xbar, c = 1..C-1: the log odds at the covariate means."""
     X = np.asarray(X, dtype=np.float64)
     n, k = X.shape
     d = k * (C_ - 1)
@@ -282,21 +300,24 @@ def default_monitors(X, C_):
         a = np.zeros(d)
         a[c * k:(c + 1) * k] = xbar
         rows.append(a)
-    rows.append(np.full(d, 1.0 / d))
     return np.array(rows)
 
 
 def default_report(X, C_):
     """Reported functionals theta_c' xbar, c = 1..C-1."""
-    return default_monitors(X, C_)[: C_ - 1]
+    return xbar_functionals(X, C_)
 
 
 def run(X, y, C_, J, N, seed, prior_mean, prior_cov, monitors=None, report_fns=None, max_cycles=None,
-        return_theta=False, replay=None, record_sigma=False, **kw):
+        return_theta=False, replay=None, record_sigma=False, trace=False, snapshots=False, **kw):
     """Algorithm 2 (one pass); data tempering also returns the log predictive likelihoods
     out["logpl"][s-1] = log p(y_s | y_{1:s-1}).  replay: dict(t_cycle, phi_cycle, R_cycle, sigma) of a pass-1 run ->
     Algorithm 3 step 2 with that fixed design (pass tag kw `pass_`); record_sigma: return the
-    proposal variances Sigma_lr actually used (out["sigma"], M steps x d x d)."""
+    proposal variances Sigma_lr actually used (out["sigma"], M steps x d x d).
+    trace: per M step (global index m) the h_lr it used (out["step_h"], hundredths), its accepted
+    count (out["step_nacc"]) and the min monitor RNE after it (out["step_minrne"]), the per-group
+    log-ML increments (out["inc_group"], L x J) and cumulative L_j (out["Lj"]); snapshots: theta at
+    the start of every cycle (out["theta_snap"], L x JN x d; small runs only)."""
     X, Xp = _d(X)
     y, yp = _i(y)
     n, k = X.shape
@@ -315,7 +336,16 @@ def run(X, y, C_, J, N, seed, prior_mean, prior_cov, monitors=None, report_fns=N
                 mean=np.zeros(report_fns.shape[0]), sd=np.zeros(report_fns.shape[0]),
                 nse=np.zeros(report_fns.shape[0]), rne=np.zeros(report_fns.shape[0]),
                 logpl=np.full(n, np.nan))
+    if trace:
+        tcap = 200000
+        arrs.update(step_nacc=np.zeros(tcap, np.int32), step_h=np.zeros(tcap, np.int32),
+                    step_minrne=np.zeros(tcap), inc_group=np.zeros(max_cycles * int(J)), Lj=np.zeros(int(J)))
+    if snapshots:
+        scap = min(max_cycles, max(1, (1 << 28) // (8 * int(J) * int(N) * d)))
+        arrs["theta_snap"] = np.zeros(scap * int(J) * int(N) * d)
     rep = Report()
+    rep.trace_cap = 200000 if trace else 0
+    rep.snap_cap = scap if snapshots else 0
     for key, a in arrs.items():
         ct = C.c_int32 if a.dtype == np.int32 else C.c_double
         setattr(rep, key, a.ctypes.data_as(C.POINTER(ct)))
@@ -352,6 +382,14 @@ def run(X, y, C_, J, N, seed, prior_mean, prior_cov, monitors=None, report_fns=N
         out["logpl"] = arrs["logpl"]
     if return_theta:
         out["theta"] = theta
+    if trace:
+        M = rep.total_m_steps
+        out.update(step_nacc=arrs["step_nacc"][:M].copy(), step_h=arrs["step_h"][:M].copy(),
+                   step_minrne=arrs["step_minrne"][:M].copy(),
+                   inc_group=arrs["inc_group"][: L * int(J)].reshape(L, int(J)).copy(), Lj=arrs["Lj"].copy())
+    if snapshots:
+        Ls = min(L, rep.snap_cap)
+        out["theta_snap"] = arrs["theta_snap"][: Ls * int(J) * int(N) * d].reshape(Ls, int(J) * int(N), d).copy()
     if record_sigma:
         out["sigma"] = sigma[: rep.total_m_steps].copy()
     return out

@@ -584,6 +584,8 @@ int32_t or_run2(const or_config* cfg, const double* X, const int32_t* y, const d
       st = OR_E_CONFIG;
       goto out;
     }
+    if (rep->theta_snap && ell <= rep->snap_cap)
+      memcpy(rep->theta_snap + (int64_t)(ell - 1) * P * d, theta, sizeof(double) * P * d);
     /* ---------------- C phase ------------------------------------------ */
     if (!power) {
       /* PAPER.md:281-295 eq. (C_phase_compute) in log form, with the cycle
@@ -656,7 +658,9 @@ int32_t or_run2(const or_config* cfg, const double* X, const int32_t* y, const d
           if (lw[(int64_t)j * N + q] > mj) mj = lw[(int64_t)j * N + q];
         double sj = 0.0;
         for (int32_t q = 0; q < N; ++q) sj += exp(lw[(int64_t)j * N + q] - mj);
-        Lj[j] += mj + log(sj / (double)N);
+        const double incj = mj + log(sj / (double)N);
+        Lj[j] += incj;
+        if (rep->inc_group) rep->inc_group[(int64_t)(ell - 1) * J + j] = incj;
       }
     }
     /* ---------------- S phase, per group ------------- */
@@ -751,9 +755,14 @@ int32_t or_run2(const or_config* cfg, const double* X, const int32_t* y, const d
         st = OR_E_NUMERIC;
         goto out;
       }
-      mstep = mstep + 1;
       int64_t nacc = 0;
       for (int64_t p = 0; p < P; ++p) nacc += acc[p];
+      const int64_t m_this = mstep;
+      if (rep->step_h && m_this < rep->trace_cap) {
+        rep->step_h[m_this] = h;
+        rep->step_nacc[m_this] = (int32_t)nacc;
+      }
+      mstep = mstep + 1;
       /* ii. step-scale adaptation (R6) */
       if ((double)nacc > cfg->accept_target * (double)P)
         h = (h + cfg->h_step < cfg->h_max) ? h + cfg->h_step : cfg->h_max;
@@ -772,6 +781,7 @@ int32_t or_run2(const or_config* cfg, const double* X, const int32_t* y, const d
         or_group_stats(g, J, N, NULL, NULL, NULL, &rne);
         if (rne < minrne) minrne = rne;
       }
+      if (rep->step_minrne && m_this < rep->trace_cap) rep->step_minrne[m_this] = minrne;
       if (replay ? r == replay->R_cycle[ell - 1] : minrne >= K) break;
     }
     rep->L = ell;
@@ -802,6 +812,7 @@ int32_t or_run2(const or_config* cfg, const double* X, const int32_t* y, const d
     double s = 0.0;
     for (int32_t j = 0; j < J; ++j) s += (Lj[j] - Lbar) * (Lj[j] - Lbar);
     rep->logml_nse = sqrt(s / ((double)J * (double)(J - 1)));
+    if (rep->Lj) memcpy(rep->Lj, Lj, sizeof(double) * J);
   }
   if (theta_out) memcpy(theta_out, theta, sizeof(double) * P * d);
 

@@ -74,6 +74,16 @@ typedef struct {
    * sum_jn w_jn^(s-1)] over the particles of the cycle that absorbs s (PAPER.md:532-535,
    * 1413-1416; R18) */
   double* logpl;
+  /* Optional adaptive-control trace (test pins of PAPER.md:392-402 cycle end,
+   * 443-445 h rule, 447-451 RNE stop, 813-816 log ML); NULL / 0 to skip. */
+  int32_t trace_cap;      /* capacity in M steps of step_nacc / step_h / step_minrne */
+  int32_t* step_nacc;     /* accepted particles in M step m (global step index) */
+  int32_t* step_h;        /* h_lr (hundredths) that M step m used */
+  double* step_minrne;    /* min monitor RNE after M step m */
+  int32_t snap_cap;       /* capacity in cycles of theta_snap */
+  double* theta_snap;     /* theta at the start of cycle l (before its C phase), P x d each */
+  double* inc_group;      /* per-group log-ML increment of cycle l, capacity max_cycles x J */
+  double* Lj;             /* per-group cumulative log ML L_j, capacity J */
 } or_report;
 
 /* ---- random numbers ---------------------- */

@@ -116,7 +116,7 @@ def _declare(L):
         "sps_cphase": ([vp, C.c_int32, C.c_double, ip, dp, dp], st),
         "sps_mphase": ([vp, C.c_int32, ip, dp, ip], st),
         "sps_run": ([vp, C.POINTER(Report)], st),
-        "sps_logml": ([vp, dp, dp], st),
+        "sps_logml": ([vp, dp, dp], st),  # (const sps_ctx*)
         "sps_moments": ([vp, C.c_int32, dp, dp, dp, dp, dp], st),
         "sps_get_particles": ([vp, dp, dp, dp], st),
         "sps_shard": ([vp, C.POINTER(C.c_int64), ip, ip], st),

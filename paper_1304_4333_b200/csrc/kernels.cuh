@@ -56,17 +56,14 @@ __global__ void k_colmeans(const double* __restrict__ X, int n, int k, double* _
   xbar[i] = s / (double)n;
 }
 
-// Default monitor rows (R12): theta_c' xbar for c = 1..C-1, then 1/d each.
-__global__ void k_default_monitors(const double* __restrict__ xbar, int k, int C, double* __restrict__ mon) {
+// Default monitor rows (R12): one per coefficient block c = 1..C-1, the block's
+// coordinate mean k^-1 sum_i theta_{c,i} -- not the reported log-odds functionals
+// theta_c' xbar.
+__global__ void k_default_monitors(int k, int C, double* __restrict__ mon) {
   const int d = k * (C - 1);
-  for (int idx = threadIdx.x; idx < C * d; idx += blockDim.x) {
+  for (int idx = threadIdx.x; idx < (C - 1) * d; idx += blockDim.x) {
     const int row = idx / d, col = idx % d;
-    double v;
-    if (row < C - 1)
-      v = (col / k == row) ? xbar[col % k] : 0.0;
-    else
-      v = 1.0 / (double)d;
-    mon[idx] = v;
+    mon[idx] = (col / k == row) ? 1.0 / (double)k : 0.0;
   }
 }
 
@@ -392,7 +389,11 @@ __device__ __forceinline__ void combine3(double& M, double& S1, double& S2, doub
 }
 
 // Combine tiles in order -> this rank's (m, S1, S2) per b.
+// One block of ESS_RANK_THREADS threads, thread b = chunk observation b: the chunk size B of a C-phase
+// round never exceeds ESS_RANK_THREADS (sps_create clamps Bmax to it).
+constexpr int ESS_RANK_THREADS = 256;
 __global__ void k_ess_rank(const double* __restrict__ parts, int ntiles, int B, double* __restrict__ slice) {
+  if (B > (int)blockDim.x) __trap();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   double M = -INFINITY, S1 = 0.0, S2 = 0.0;
@@ -417,6 +418,7 @@ __global__ void k_ess_rank(const double* __restrict__ parts, int ntiles, int B, 
 // loop: the previous observation's lse comes from the neighbour lane).
 __global__ void k_ess_final(const double* __restrict__ gath, int G, int B, int s0, int n, double ess_frac, double P,
                             Ctl* ctl, int t_fix, int t_start, double* __restrict__ lse, double* __restrict__ logpl) {
+  if (blockDim.x != 32) __trap();  // one warp: lane = observation of a 32-observation round
   const int lane = threadIdx.x;
   double carry = lse && s0 != t_start ? lse[s0] : 0.0;  // lse of the observation before the round
   for (int base = 0; base < B; base += 32) {
@@ -715,6 +717,7 @@ __global__ void __launch_bounds__(1024) k_resample(const double* __restrict__ lw
 // Pooled log-ML increment from all groups' (m_j, s_j) in group order (R10).
 // One warp: lanes take the max and the exps; lane 0 adds the terms in group order.
 __global__ void k_logml_pooled(const double* __restrict__ gath_ms, int J, double P, Ctl* ctl, double* inc_out) {
+  if (blockDim.x != 32) __trap();  // one warp (full-mask shuffles)
   const int lane = threadIdx.x;
   double M = -INFINITY;
   for (int j = lane; j < J; j += 32) M = fmax(M, gath_ms[j * 2]);

@@ -670,13 +670,61 @@ __global__ void __launch_bounds__(128, MINB) k_loglik_bin_mma(LLArgs a) {
   tl_end(2);
 }
 
-// Sum chunk partials in chunk order: out[p] = sum_c part[c][p].
-__global__ void k_sum_chunks(const double* __restrict__ part, int nchunks, int64_t P, double* __restrict__ out) {
+// Sum chunk partials in chunk order: out[p] = sum_c part[c][p].  bad (may be null):
+// the smallest p whose sum is not finite (sps_loglik's error check).
+__global__ void k_sum_chunks(const double* __restrict__ part, int nchunks, int64_t P, double* __restrict__ out,
+                             int* bad = nullptr) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= P) return;
   double s = part[p];
   for (int c = 1; c < nchunks; ++c) s += part[(int64_t)c * P + p];
   out[p] = s;
+  if (bad && !isfinite(s)) atomicMin(bad, (int)(p < 0x7ffffffe ? p : 0x7ffffffe));
+}
+
+// sps_loglik error path (the log-likelihood is finite for finite theta): if
+// k_sum_chunks flagged particle *pending, find the first observation t in [t0, t1) whose term
+// log P(y_t | x_t, theta_p) is not finite (eta_c = x_t' theta_c, max-shifted log-sum-exp as in
+// K1's fallback branch, so a term is non-finite iff some eta_c is) and record (p, t) in the
+// mapped host pair rec (first error sticks until sps_sync reports it); clears *pending.
+__global__ void k_ll_locate(const double* __restrict__ theta, int ld, const double* __restrict__ X,
+                            const int32_t* __restrict__ y, int k, int C, int t0, int t1, int* pending,
+                            volatile int* rec) {
+  __shared__ int tmin;
+  const int p = *pending;
+  if (p == 0x7fffffff) return;
+  if (threadIdx.x == 0) tmin = 0x7fffffff;
+  __syncthreads();
+  const double* th = theta + (int64_t)p * ld;
+  for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+    const double* x = X + (int64_t)t * k;
+    bool bad = false;
+    double m = 0.0, ey = 0.0;
+    for (int c = 1; c < C; ++c) {
+      double e = 0.0;
+      for (int i = 0; i < k; ++i) e = fma(x[i], th[(c - 1) * k + i], e);
+      bad |= !isfinite(e);
+      m = fmax(m, e);
+      if (c == y[t]) ey = e;
+    }
+    double s = exp(-m);
+    for (int c = 1; c < C; ++c) {
+      double e = 0.0;
+      for (int i = 0; i < k; ++i) e = fma(x[i], th[(c - 1) * k + i], e);
+      s += exp(e - m);
+    }
+    const double term = ey - m - log(s);
+    if (bad || !isfinite(term)) atomicMin(&tmin, t);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (rec[0] == 0x7fffffff) {
+      rec[1] = tmin == 0x7fffffff ? -1 : tmin;
+      __threadfence_system();
+      rec[0] = p;
+    }
+    *pending = 0x7fffffff;
+  }
 }
 
 }  // namespace sps

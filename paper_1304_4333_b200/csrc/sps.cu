@@ -147,6 +147,9 @@ struct sps_ctx {
   size_t acc_smem = 0;
   Ctl* hslot = nullptr;          // 2 mapped pinned Ctl slots (pipelined M steps), written by finalize_body
   Ctl* dslot = nullptr;          // device view of hslot
+  int* llbad = nullptr;          // sps_loglik: smallest particle with a non-finite sum (device; INT_MAX = none)
+  int* hllbad = nullptr;         // mapped pinned [p, t] of the first non-finite sps_loglik term (INT_MAX = none)
+  int* dllbad = nullptr;         // device view of hllbad
   unsigned* ticket = nullptr;      // arrival counter of the fused reduce + finalize (k_mom_reduce)
   unsigned long long* trace = nullptr;  // debug (SPS_TRACE): finalize / reduce phase clocks (managed)
   unsigned long long* tl = nullptr;     // debug (SPS_TIMELINE): per-step kernel start / end clocks
@@ -936,6 +939,8 @@ void free_ctx(sps_ctx* c) {
   lap("cudaFree");
   if (c->hctl) cudaFreeHost(c->hctl);
   if (c->hslot) cudaFreeHost(c->hslot);
+  if (c->hllbad) cudaFreeHost(c->hllbad);
+  if (c->llbad) cudaFree(c->llbad);
   lap("freeHost");
   if (c->ticket) cudaFreeAsync(c->ticket, fs);
   if (c->trace) cudaFree(c->trace);  // managed
@@ -1053,7 +1058,7 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
     CU(c, cudaFuncSetAttribute(ch.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 101 * 1024 + 1024));
   }
   c->ldx = (ch.KT + 3) / 4 * 4;  // X row stride: k padded to 4 (DMMA k-step; zero columns)
-  c->nmon = cfg.n_monitors > 0 ? cfg.n_monitors : c->C;
+  c->nmon = cfg.n_monitors > 0 ? cfg.n_monitors : c->C - 1;
   if (cfg.n_monitors > 0 && !cfg_in->monitors) return fail(c, SPS_E_CONFIG, "n_monitors > 0 but monitors == NULL");
   // accept + moments layout: blocks of tp particles inside one group (tp divides N,
   // tp <= 256, staged tile tp x round_up(d, 8) doubles <= 96 KB)
@@ -1081,7 +1086,7 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
   }
   c->slice_len = c->Jl * d + d * d + 2;
   c->max_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(64, ((int64_t)1 << 26) / std::max<int64_t>(c->Pl, 1)));
-  c->Bmax = (int)std::max<int64_t>(8, std::min<int64_t>(256, ((int64_t)1 << 23) / std::max<int64_t>(c->Pl, 1)));
+  c->Bmax = (int)std::max<int64_t>(8, std::min<int64_t>(ESS_RANK_THREADS, ((int64_t)1 << 23) / std::max<int64_t>(c->Pl, 1)));
 
   {  // keep freed device memory in the default pool across contexts (once per device)
     static std::mutex mu;
@@ -1138,6 +1143,14 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
   CU(c, cudaHostAlloc((void**)&c->hslot, 2 * sizeof(Ctl), cudaHostAllocMapped));
   CU(c, cudaHostGetDevicePointer((void**)&c->dslot, c->hslot, 0));
   TRY(dalloc(c, &c->ticket, 1));
+  CU(c, cudaMalloc((void**)&c->llbad, sizeof(int)));
+  {
+    static const int none = 0x7fffffff;
+    CU(c, cudaMemcpy(c->llbad, &none, sizeof(int), cudaMemcpyHostToDevice));
+  }
+  CU(c, cudaHostAlloc((void**)&c->hllbad, 2 * sizeof(int), cudaHostAllocMapped));
+  CU(c, cudaHostGetDevicePointer((void**)&c->dllbad, c->hllbad, 0));
+  c->hllbad[0] = c->hllbad[1] = 0x7fffffff;
   if (getenv("SPS_TRACE")) CU(c, cudaMallocManaged((void**)&c->trace, 128 * sizeof(unsigned long long)));
   CU(c, cudaMemsetAsync(c->ticket, 0, sizeof(unsigned), c->stream));
   CU(c, cudaEventCreateWithFlags(&c->evs[0], cudaEventDisableTiming));
@@ -1185,6 +1198,7 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
   TRY(dalloc(c, &c->essparts, (size_t)c->Bmax * ntiles * 3));
   TRY(dalloc(c, &c->essslice, (size_t)c->Bmax * 3));
   TRY(dalloc(c, &c->grp_ms, (size_t)c->Jl * 2));
+  if (const char* e = getenv("SPS_INC_CAP")) c->inc_cap = std::max(1, atoi(e));  // (test hook: tiny capacity)
   TRY(dalloc(c, &c->inc_dev, (size_t)c->inc_cap));
   if (cfg.tempering == SPS_DATA_TEMPERING) {
     TRY(dalloc(c, &c->lse, (size_t)c->n + 1));
@@ -1239,7 +1253,7 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
     k_colmeans<<<(c->k + 127) / 128, 128, 0, c->stream>>>(c->X, c->n, c->k, c->xbar);
     CHECK_LAUNCH(c);
     if (cfg.n_monitors <= 0) {
-      k_default_monitors<<<1, 256, 0, c->stream>>>(c->xbar, c->k, c->C, c->mon);
+      k_default_monitors<<<1, 256, 0, c->stream>>>(c->k, c->C, c->mon);
       CHECK_LAUNCH(c);
     }
     const size_t smem = sizeof(double) * d * d;
@@ -1466,7 +1480,10 @@ sps_status sps_loglik(sps_ctx* c, const double* theta_dev, int64_t P, int32_t ld
   }
   int nch = 1;
   TRY(launch_loglik(c, theta_dev, ld, P, t0, t1, c->ll_scratch, max_chunks, &nch));
-  k_sum_chunks<<<(unsigned)((P + 255) / 256), 256, 0, c->stream>>>(c->ll_scratch, nch, P, out_dev);
+  k_sum_chunks<<<(unsigned)((P + 255) / 256), 256, 0, c->stream>>>(c->ll_scratch, nch, P, out_dev, c->llbad);
+  CHECK_LAUNCH(c);
+  // non-finite L_p: locate (p, t) on the device; reported by the next sps_sync (no host round trip here)
+  k_ll_locate<<<1, 256, 0, c->stream>>>(theta_dev, ld, c->X, c->y, c->k, c->C, t0, t1, c->llbad, c->dllbad);
   CHECK_LAUNCH(c);
   return SPS_OK;
 }
@@ -1477,6 +1494,11 @@ sps_status sps_sync(sps_ctx* c) {
   CU(c, cudaStreamSynchronize(c->aux));
   CU(c, cudaStreamSynchronize(c->stream));
   c->syncs += 1;
+  if (c->hllbad && c->hllbad[0] != 0x7fffffff) {
+    const int p = c->hllbad[0], t = c->hllbad[1];
+    c->hllbad[1] = c->hllbad[0] = 0x7fffffff;
+    return fail(c, SPS_E_NUMERIC, "sps_loglik: non-finite log-likelihood at particle p = %d, observation t = %d", p, t);
+  }
   return SPS_OK;
 }
 
@@ -1536,7 +1558,7 @@ sps_status sps_cphase(sps_ctx* c, int32_t t_target, double phi_target, int32_t* 
       k_ess_partials<<<dim3((unsigned)ntiles, (unsigned)Be), 256, 0, c->stream>>>(c->lwbuf, Pl, ESS_TILE,
                                                                                  c->essparts);
       CHECK_LAUNCH(c);
-      k_ess_rank<<<1, 256, 0, c->stream>>>(c->essparts, ntiles, Be, c->essslice);
+      k_ess_rank<<<1, ESS_RANK_THREADS, 0, c->stream>>>(c->essparts, ntiles, Be, c->essslice);
       CHECK_LAUNCH(c);
       TRY(gather(c, c->essslice, c->essgath, (size_t)Be * 3));
       k_ess_final<<<1, 32, 0, c->stream>>>(c->essgath, c->G, Be, s, c->n, c->cfg.ess_frac, P, c->ctl,
@@ -1605,6 +1627,8 @@ sps_status sps_cphase(sps_ctx* c, int32_t t_target, double phi_target, int32_t* 
   }
   PROF_END(c, CAT_CPHASE);
   // ---- S phase + log-ML increments (R10) ----
+  // room for this cycle's increment in inc_dev: pull the pending ones first (cycles inc_base..ell-1)
+  if (c->ell - c->inc_base >= c->inc_cap) TRY(sync_incs(c));
   c->ell += 1;
   PROF_BEGIN(c);
   {
@@ -1618,7 +1642,6 @@ sps_status sps_cphase(sps_ctx* c, int32_t t_target, double phi_target, int32_t* 
     std::swap(c->L, c->L2);
     std::swap(c->lp, c->lp2);
     TRY(gather(c, c->grp_ms, c->grp_ms_gath, (size_t)c->Jl * 2));
-    if (c->ell - 1 - c->inc_base >= c->inc_cap) TRY(sync_incs(c));  // (ell was incremented above)
     k_logml_pooled<<<1, 32, 0, c->stream>>>(c->grp_ms_gath, c->J, P, c->ctl, c->inc_dev + (c->ell - 1 - c->inc_base));
     CHECK_LAUNCH(c);
   }
@@ -2044,8 +2067,10 @@ sps_status sps_mphase(sps_ctx* c, int32_t R_fixed, int32_t* R_out, double* min_r
   return SPS_OK;
 }
 
-sps_status sps_logml(sps_ctx* c, double* logml, double* nse) {
-  if (!c) return SPS_E_CONFIG;
+sps_status sps_logml(const sps_ctx* cc, double* logml, double* nse) {
+  if (!cc) return SPS_E_CONFIG;
+  // logically const: pulls the increments still pending on the device into the host total (a cache)
+  sps_ctx* c = const_cast<sps_ctx*>(cc);
   CU(c, cudaSetDevice(c->cfg.device));
   TRY(sync_incs(c));
   if (logml) *logml = c->logml;
@@ -2128,7 +2153,6 @@ sps_status sps_run(sps_ctx* c, sps_report* rep) {
     std::vector<double> A;
     const double* fns = rep->report_fns;
     if (!fns) {  // theta_c' xbar, c = 1..C-1
-      std::vector<double> mon((size_t)c->C * c->d);
       std::vector<double> xbar(c->k);
       CU(c, cudaMemcpyAsync(xbar.data(), c->xbar, sizeof(double) * c->k, cudaMemcpyDeviceToHost, c->stream));
       CU(c, cudaStreamSynchronize(c->stream));
