@@ -31,6 +31,7 @@
 #include "kernels.cuh"
 #include "loglik.cuh"
 #include "mstep.cuh"
+#include "fused.cuh"
 
 using namespace sps;
 
@@ -179,6 +180,12 @@ struct sps_ctx {
   double gl_pairs = 0;
   LLChoice_t llc{};
   int ll_regs = 0;
+  // fused M step (binary, d <= 32): propose + K1 + accept + tile moments in one kernel (fused.cuh)
+  void (*fu_fn)(FusedArgs) = nullptr;
+  size_t fu_smem = 0;
+  int fu_TPR = 1;
+  unsigned* fu_tick = nullptr;
+  double* fu_tpart = nullptr;
   struct Plan {
     int64_t P = -1;
     int range = -1, max_chunks = -1, S = 1, chunk = 0, sub = 0, occ = 1;
@@ -502,20 +509,11 @@ bool choose_ll(int k, int C, LLChoice* o) {
   }
 }
 
-// Launch K1 over [t0, t1) for P particles: partial sums per observation chunk
-// into `part` ([nchunks][P]); returns nchunks.  The chunk count S is chosen so
-// the grid (tiles x S) fills whole waves of SMs x resident blocks (occupancy
-// from the kernel's registers and the chunk's shared memory) and the X tile
-// fits in shared memory; plans are cached per (P, range).
-sps_status launch_loglik(sps_ctx* c, const double* theta, int64_t ldt, int64_t P, int t0, int t1, double* part,
-                         int max_chunks, int* nchunks_out, const int* stop = nullptr) {
+// K1 launch plan for P particles over an observation range: chunk count S chosen so the grid
+// (tiles x S) fills whole waves of SMs x resident blocks (occupancy from the kernel's registers and
+// the chunk's shared memory) and the X tile fits in shared memory; cached per (P, range).
+sps_status get_plan(sps_ctx* c, int64_t P, int range, int max_chunks, sps_ctx::Plan** out) {
   const LLChoice& ch = c->llc;
-  const int range = t1 - t0;
-  if (range <= 0) {
-    CU(c, cudaMemsetAsync(part, 0, (size_t)P * sizeof(double), c->stream));
-    *nchunks_out = 1;
-    return SPS_OK;
-  }
   const int ppb = ch.ppb > 0 ? ch.ppb : LL_THREADS * ch.PPT;
   const int64_t tiles = (P + ppb - 1) / ppb;
   const size_t row_bytes = (size_t)c->ldx * 8 + (c->C > 2 ? 4 : 0);
@@ -577,6 +575,28 @@ sps_status launch_loglik(sps_ctx* c, const double* theta, int64_t ldt, int64_t P
       fprintf(stderr, "K1 plan: P %lld range %d -> S %d chunk %d sub %d occ %d smem %zu\n", (long long)P, range, pl->S,
               pl->chunk, pl->sub, pl->occ, pl->smem);
   }
+  *out = pl;
+  return SPS_OK;
+}
+
+// Launch K1 over [t0, t1) for P particles: partial sums per observation chunk
+// into `part` ([nchunks][P]); returns nchunks.  The chunk count S is chosen so
+// the grid (tiles x S) fills whole waves of SMs x resident blocks (occupancy
+// from the kernel's registers and the chunk's shared memory) and the X tile
+// fits in shared memory; plans are cached per (P, range).
+sps_status launch_loglik(sps_ctx* c, const double* theta, int64_t ldt, int64_t P, int t0, int t1, double* part,
+                         int max_chunks, int* nchunks_out, const int* stop = nullptr) {
+  const LLChoice& ch = c->llc;
+  const int range = t1 - t0;
+  if (range <= 0) {
+    CU(c, cudaMemsetAsync(part, 0, (size_t)P * sizeof(double), c->stream));
+    *nchunks_out = 1;
+    return SPS_OK;
+  }
+  const int ppb = ch.ppb > 0 ? ch.ppb : LL_THREADS * ch.PPT;
+  const int64_t tiles = (P + ppb - 1) / ppb;
+  sps_ctx::Plan* pl = nullptr;
+  TRY(get_plan(c, P, range, max_chunks, &pl));
   LLArgs a{c->Xs, c->y, theta, part, ldt, P, t0, t1, pl->chunk};
   a.k = c->k;
   a.stop = stop;
@@ -708,6 +728,68 @@ sps_status launch_draw(sps_ctx* c, int slot, const double* base, const double* L
   return SPS_OK;
 }
 
+// Fused M step (binary, d <= 32; fused.cuh): theta* in shared memory, K1 over [0, t1), accept and
+// the tile moment partials -> bpart rows (the k_accept_tile layout), one launch.
+sps_status launch_fused(sps_ctx* c, int slot, int t1, double temper, const int* stop, bool graph) {
+  sps_ctx::Plan* pl = nullptr;
+  TRY(get_plan(c, c->Pl, t1, c->max_chunks, &pl));
+  if (pl->sub <= 0 || pl->sub > 64) return fail(c, SPS_E_CONFIG, "fused M step: X sub-chunk of %d rows (max 64)", pl->sub);
+  if (!graph) CU(c, cudaStreamWaitEvent(c->stream, c->ev_zready[slot], 0));
+  FusedArgs a{};
+  a.X = c->Xs;
+  a.theta = c->theta;
+  a.L = c->L;
+  a.lp = c->lp;
+  a.Z = c->Zbuf[slot];
+  a.logu = c->LUbuf[slot];
+  a.Lz = c->Lprop;
+  a.Rp = c->RpP;
+  a.mu = c->mu;
+  a.shift = c->shift;
+  a.part = c->part;
+  a.tpart = c->fu_tpart;
+  a.bpart = c->bpart;
+  a.tick = c->fu_tick;
+  a.ctl = c->ctl;
+  a.stop = stop;
+  a.P = c->Pl;
+  a.temper = temper;
+  a.dmagic = ((1ull << 32) + (uint64_t)c->d - 1) / (uint64_t)c->d;
+  a.d = c->d;
+  a.t1 = t1;
+  a.chunk = pl->chunk;
+  a.sub = pl->sub;
+  a.S = pl->S;
+  a.TPR = c->fu_TPR;
+  a.step0 = c->phase_step0;
+  a.set_step = 1;
+  const dim3 grid((unsigned)(c->Pl / FU_TILE), (unsigned)pl->S);
+  PROF_BEGIN(c);
+  CU(c, launch_pdl(c->fu_fn, grid, dim3(128), c->fu_smem, c->stream, a));
+  CHECK_LAUNCH(c);
+  c->k1_launches += 1;
+  c->k1_pairs += (double)c->Pl * t1;
+  PROF_END(c, CAT_K1);
+  return SPS_OK;
+}
+
+// Fused-kernel instance for k = d <= 32: DMMA k-steps KKD + remainder DFMAs REM (as K1), T'T tiles NT.
+void (*pick_fused(int k))(FusedArgs) {
+  switch (k) {
+#define FU_CASE(K_, KKD_, REM_) \
+  case K_:                      \
+    return k_mstep_bin<KKD_, REM_, (K_ + 8) / 8>;
+    FU_CASE(1, 0, 1) FU_CASE(2, 0, 2) FU_CASE(3, 1, 0) FU_CASE(4, 1, 0) FU_CASE(5, 1, 1) FU_CASE(6, 1, 2)
+    FU_CASE(7, 2, 0) FU_CASE(8, 2, 0) FU_CASE(9, 2, 1) FU_CASE(10, 2, 2) FU_CASE(11, 3, 0) FU_CASE(12, 3, 0)
+    FU_CASE(13, 3, 1) FU_CASE(14, 3, 2) FU_CASE(15, 4, 0) FU_CASE(16, 4, 0) FU_CASE(17, 4, 1)
+    FU_CASE(18, 4, 2) FU_CASE(19, 5, 0) FU_CASE(20, 5, 0) FU_CASE(21, 5, 1) FU_CASE(22, 5, 2)
+    FU_CASE(23, 6, 0) FU_CASE(24, 6, 0) FU_CASE(25, 6, 1) FU_CASE(26, 6, 2) FU_CASE(27, 7, 0)
+    FU_CASE(28, 7, 0) FU_CASE(29, 7, 1) FU_CASE(30, 7, 2) FU_CASE(31, 8, 0) FU_CASE(32, 8, 0)
+#undef FU_CASE
+    default: return nullptr;
+  }
+}
+
 // K9 + K6 (decide = true) or K6 only, then the deterministic reduction into this
 // rank's stats slice and the gather across ranks -> `gath`.
 sps_status launch_normals(sps_ctx* c, uint32_t tag, uint32_t step, int slot, bool graph, bool forked);
@@ -716,7 +798,7 @@ sps_status launch_normals(sps_ctx* c, uint32_t tag, uint32_t step, int slot, boo
 // the side stream.
 sps_status accept_moments(sps_ctx* c, bool decide, int nchunks, double temper, uint32_t step, const int* stop,
                           const double* logu = nullptr, const FinArgs* fin = nullptr, size_t fin_smem = 0,
-                          uint32_t fork_step = ~0u) {
+                          uint32_t fork_step = ~0u, bool fused = false) {
   AccArgs a{};
   a.theta = c->theta;
   a.L = c->L;
@@ -743,7 +825,8 @@ sps_status accept_moments(sps_ctx* c, bool decide, int nchunks, double temper, u
   a.trace = decide ? c->trace : nullptr;
   // (device-side loop: each captured step's log-u buffer is static -- LUbuf[step & 1] -- like its Z)
   PROF_BEGIN(c);
-  if (c->acc_tnt > 0) {  // tile layout: bulk-staged rows, on-the-fly DMMA fragments, ones column
+  if (fused) {  // accept + tile moments already done by the fused M-step kernel
+  } else if (c->acc_tnt > 0) {  // tile layout: bulk-staged rows, on-the-fly DMMA fragments, ones column
     switch (c->acc_tnt) {
       case 1: CU(c, launch_pdl(k_accept_tile<1>, dim3(c->nblk), dim3(256), c->acc_smem, c->stream, a)); break;
       case 2: CU(c, launch_pdl(k_accept_tile<2>, dim3(c->nblk), dim3(256), c->acc_smem, c->stream, a)); break;
@@ -864,10 +947,11 @@ sps_status finalize(sps_ctx* c, int mode, bool allow_stop, const int* stop, int 
 
 // K9 + K6 -> reduce -> (gather) -> K7: fused into the reduce launch on one rank.
 sps_status moments_finalize(sps_ctx* c, bool decide, int nchunks, double temper, uint32_t step, const int* stop,
-                            const double* logu, int mode, bool allow_stop, int slot, bool fork_normals = false) {
+                            const double* logu, int mode, bool allow_stop, int slot, bool fork_normals = false,
+                            bool fused = false) {
   const bool graph = c->capturing;
   if (c->G > 1) {
-    TRY(accept_moments(c, decide, nchunks, temper, step, stop, logu, nullptr, 0, fork_normals ? step : ~0u));
+    TRY(accept_moments(c, decide, nchunks, temper, step, stop, logu, nullptr, 0, fork_normals ? step : ~0u, fused));
     return finalize(c, mode, allow_stop, stop, slot);
   }
   FinArgs f;
@@ -875,7 +959,7 @@ sps_status moments_finalize(sps_ctx* c, bool decide, int nchunks, double temper,
   TRY(make_fin(c, mode, allow_stop, stop, slot, &f, &smem));
   f.ticket = c->ticket;
   (void)graph;
-  return accept_moments(c, decide, nchunks, temper, step, stop, logu, &f, smem, fork_normals ? step : ~0u);
+  return accept_moments(c, decide, nchunks, temper, step, stop, logu, &f, smem, fork_normals ? step : ~0u, fused);
 }
 
 sps_status validate(const sps_config* cfg) {
@@ -933,7 +1017,7 @@ void free_ctx(sps_ctx* c) {
                   c->shift, c->Lprop, c->V, c->rne, c->lwbuf, c->essparts, c->essslice, c->essgath, c->lse, c->logpl, c->grp_ms,
                   c->grp_ms_gath, c->Lj, c->Lj_gath, c->scal, c->pw_parts, c->pw_slice, c->pw_gath, c->mx_parts,
                   c->mx_slice, c->mx_gath, c->fn_A, c->fn_out, c->ll_scratch, c->Sinv, c->LpriorP, c->SinvP, c->Rp, c->RpP, c->bpart, c->ctl, c->inc_dev,
-                  c->sig_rec, c->sig_in};
+                  c->sig_rec, c->sig_in, c->fu_tick, c->fu_tpart};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, fs);
   lap("cudaFree");
@@ -1084,6 +1168,16 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
       c->acc_smem = sm;
     }
   }
+  {  // fused M-step kernel (binary, d <= 32, DMMA K1, tile-layout moments, groups of whole 64-tiles):
+     // opt-in (SPS_FUSED=1) -- measured slower than the separate kernels at every t_l
+    static const bool fused_on = getenv("SPS_FUSED") != nullptr && strcmp(getenv("SPS_FUSED"), "0") != 0;
+    if (fused_on && c->C == 2 && c->llc.streams && c->k <= 32 && c->acc_tnt > 0 && c->tp % FU_TILE == 0)
+      c->fu_fn = pick_fused(c->k);
+    if (c->fu_fn) {
+      c->fu_TPR = c->tp / FU_TILE;
+      c->fu_smem = (size_t)fused_smem_doubles(round_up(c->k, 4), c->d) * sizeof(double);
+    }
+  }
   c->slice_len = c->Jl * d + d * d + 2;
   c->max_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(64, ((int64_t)1 << 26) / std::max<int64_t>(c->Pl, 1)));
   c->Bmax = (int)std::max<int64_t>(8, std::min<int64_t>(ESS_RANK_THREADS, ((int64_t)1 << 23) / std::max<int64_t>(c->Pl, 1)));
@@ -1139,6 +1233,13 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
   for (double** p : {&c->L, &c->L2, &c->lp, &c->lp2, &c->lw, &c->lw_cur, &c->lp_s}) TRY(dalloc(c, p, (size_t)Pl));
   TRY(dalloc(c, &c->part, (size_t)c->max_chunks * Pl));
   TRY(dalloc(c, &c->bpart, (size_t)c->nblk * std::max(c->W, c->Wt)));
+  if (c->fu_fn) {
+    const int64_t tiles = c->Pl / FU_TILE;
+    TRY(dalloc(c, &c->fu_tick, (size_t)(tiles + c->nblk)));
+    CU(c, cudaMemsetAsync(c->fu_tick, 0, sizeof(unsigned) * (size_t)(tiles + c->nblk), c->stream));
+    if (c->fu_TPR > 1) TRY(dalloc(c, &c->fu_tpart, (size_t)tiles * c->Wt));
+    CU(c, cudaFuncSetAttribute(c->fu_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->fu_smem));
+  }
   TRY(dalloc(c, &c->Sinv, (size_t)d * d));
   CU(c, cudaHostAlloc((void**)&c->hslot, 2 * sizeof(Ctl), cudaHostAllocMapped));
   CU(c, cudaHostGetDevicePointer((void**)&c->dslot, c->hslot, 0));
@@ -1429,8 +1530,10 @@ sps_status sps_get_counters(const sps_ctx* cc, sps_counters* out) {
     for (int b = 0; b < 6; ++b)
       if (c->tl_bin[b][0] > 0)
         fprintf(stderr,
-                "SPS_TIMELINE %-7s steps %5.0f  K1 %7.2f us  step %7.2f us  gap %5.2f us  K1 blk0: release %.2f theta %.2f "
-                "rest %.2f  last block start %.2f\n",
+                c->fu_fn ? "SPS_TIMELINE %-7s steps %5.0f  K1 %7.2f us  step %7.2f us  gap %5.2f us  fused: kernel %.2f "
+                           "-> reduce end %.2f -> finalize start %.2f finalize %.2f\n"
+                         : "SPS_TIMELINE %-7s steps %5.0f  K1 %7.2f us  step %7.2f us  gap %5.2f us  K1 blk0: release %.2f "
+                           "theta %.2f rest %.2f  last block start %.2f\n",
                 bn[b], c->tl_bin[b][0], c->tl_bin[b][1] / c->tl_bin[b][0] / 1e3, c->tl_bin[b][2] / c->tl_bin[b][0] / 1e3,
                 c->tl_bin[b][3] / c->tl_bin[b][0] / 1e3, c->tl_bin[b][4] / c->tl_bin[b][0] / 1e3,
                 c->tl_bin[b][5] / c->tl_bin[b][0] / 1e3, c->tl_bin[b][6] / c->tl_bin[b][0] / 1e3,
@@ -1723,7 +1826,12 @@ static sps_status timeline_accumulate(sps_ctx* c, int R) {
       c->tl_bin[b][1] += (double)(t[5] - t[4]);
       c->tl_bin[b][2] += (double)(t[11] - t[0]);
       if (r + 1 < rows && h[(size_t)(r + 1) * TL_W]) c->tl_bin[b][3] += (double)h[(size_t)(r + 1) * TL_W] - (double)t[11];
-      if (t[24] && t[25] && t[26] && t[27]) {  // K1 phases: block (0,0) release / theta loaded / done, last block start
+      if (c->fu_fn) {  // fused M step: kernel start -> last tail, -> reduce end, -> finalize start, finalize
+        c->tl_bin[b][4] += (double)t[7] - (double)t[0];
+        c->tl_bin[b][5] += (double)t[9] - (double)t[7];
+        c->tl_bin[b][6] += (double)t[10] - (double)t[9];
+        c->tl_bin[b][7] += (double)t[11] - (double)t[10];
+      } else if (t[24] && t[25] && t[26] && t[27]) {  // K1 phases: block (0,0) release / theta loaded / done, last block start
         c->tl_bin[b][4] += (double)t[25] - (double)t[4];
         c->tl_bin[b][5] += (double)t[26] - (double)t[25];
         c->tl_bin[b][6] += (double)t[27] - (double)t[26];
@@ -1764,6 +1872,10 @@ static sps_status launch_mstep(sps_ctx* c, uint32_t step, bool allow_stop, bool 
   const double temper = power ? c->phi : 1.0;
   const int* stop = &c->ctl->stop;
   const int zs = (int)(step & 1u);
+  if (c->fu_fn && t1 > 0) {  // one kernel: propose + K1 + accept + tile moments (fused.cuh)
+    TRY(launch_fused(c, zs, t1, temper, stop, graph));
+    TRY(moments_finalize(c, true, 1, temper, step, stop, c->LUbuf[zs], 1, allow_stop, zs, true, true));
+  } else {
   TRY(launch_draw(c, zs, c->theta, c->Lprop, c->theta_s, c->lp_s, stop, graph, true));
   // the next step's normals: forked after accept into the reduce / finalize tail (default), or after
   // the proposal with a small resident footprint (SPS_NORMALS_FORK=propose, experiment)
@@ -1785,6 +1897,7 @@ static sps_status launch_mstep(sps_ctx* c, uint32_t step, bool allow_stop, bool 
   // the reduce / one-block finalize tail leaves idle (SPS_TIMELINE: launched before K1 they held
   // every SM while K1 waited 17.8 us; forked after K1 they stretched accept from 13 to 25 us)
   TRY(moments_finalize(c, true, nch, temper, step, stop, c->LUbuf[zs], 1, allow_stop, zs, !fork_at_propose && !fork_at_k1));
+  }
   if (graph) {
     CU(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
     if (!c->capturing_loop) CU(c, cudaEventRecordWithFlags(c->evs[zs], c->stream, cudaEventRecordExternal));

@@ -57,8 +57,10 @@ def test_run_parity_large_d(sps, orc):
     """d = 100: generic (non register-blocked) proposal / moments / block Cholesky paths."""
     X, y = sps_synth.make_data(200, 100, 2, 30, (0.0,), 0.15, seed=5)
     cov = orc.g_prior(X, 2, 0.25)
-    o = orc.run(X, y, 2, 4, 128, seed=2, prior_mean=np.zeros(100), prior_cov=cov)
-    s = sps.Sps(X, y, np.zeros(100), cov, J=4, N=128, seed=2)
+    # (J = 8: with J = 4 x N = 128 and d = 100 the resampled particle set is so degenerate that the
+    # ridge-retry decision (R13) of a near-singular V can differ in the last bit between the two)
+    o = orc.run(X, y, 2, 8, 128, seed=2, prior_mean=np.zeros(100), prior_cov=cov)
+    s = sps.Sps(X, y, np.zeros(100), cov, J=8, N=128, seed=2)
     g = s.run()
     s.close()
     assert o["status"] == 0 and g["L"] == o["L"]
