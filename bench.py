@@ -10,8 +10,12 @@ observation log-likelihood terms evaluated per second, whole job (all ranks).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1: launched by torch.distributed.run, one rank per GPU, group sharding
-(weak scaling: 64 groups x 1024 particles per GPU, J = 64 N in total).
+N > 1: launched by torch.distributed.run, one rank per GPU, group sharding.
+Default for N > 1 is the north_star's strong-scaling case: configs[4] at a fixed
+P = 2^20 particles (J = 1024 groups x N = 1024, cfg2 data), J / N groups per GPU,
+plus a 1-GPU run of the same workload on rank 0 (`strong_ref`, speedup = its
+time / the N-GPU time).  --scaling weak: 64 groups x 1024 particles per GPU.
+--workload cfg4: configs[3] (n = 1e5, k = 100, J = 1024 x N = 1024) sharded.
 --impl reference: the CPU oracle (oracle/, the tier's reference arm) on a
 bounded sample of the same workload, on the host cores.
 """
@@ -55,6 +59,11 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--scaling", choices=["auto", "weak", "strong"], default="auto",
+                    help="auto: configs[1] at N = 1, strong scaling at 2^20 particles for N > 1")
+    ap.add_argument("--particles", type=int, default=1 << 20, help="strong scaling: global particle count")
+    ap.add_argument("--workload", choices=["cfg2", "cfg4"], default="cfg2")
+    ap.add_argument("--no-strong-ref", action="store_true")
     return ap.parse_args()
 
 
@@ -187,11 +196,27 @@ def main():
         if world > 1:
             dist.barrier()
 
-    X, y = sps_synth.config_data("cfg2")
+    scaling = args.scaling if args.scaling != "auto" else ("weak" if world == 1 else "strong")
+    if args.workload == "cfg4":  # configs[3]: one context over all ranks, 1024 / world groups each
+        X, y = sps_synth.config_data("cfg4")
+        g = sps_synth.CONFIGS["cfg4"]["g"]
+        J, N = 1024, 1024
+        scaling = "strong"
+        wdesc = ("configs[3]: large synthetic binary logit, n=100000, k=100 (1 + 30 continuous + 69 binary), "
+                 f"J=1024 x N=1024 particles group-sharded over {world} GPU(s), g=1/4, full Algorithm 2 to posterior")
+    else:
+        X, y = sps_synth.config_data("cfg2")
+        g = WORKLOAD["g"]
+        N = WORKLOAD["N"]
+        if scaling == "strong":
+            J = max(world, args.particles // N)
+            wdesc = (f"configs[4] strong scaling: cfg2 data (n=1000, k=25, g=1/16), P={J * N} particles (J={J} x "
+                     f"N={N}) fixed in total, {J // world} groups per GPU over {world} GPUs, full Algorithm 2 to posterior")
+        else:
+            J = WORKLOAD["J_per_gpu"] * world
+            wdesc = WORKLOAD_DESC if world == 1 else (WORKLOAD_DESC + f"; weak scaling: 64 groups per GPU x {world}")
     n, k = X.shape
-    cov = sps.g_prior(X, 2, WORKLOAD["g"], device=local)
-    J = WORKLOAD["J_per_gpu"] * world
-    N = WORKLOAD["N"]
+    cov = sps.g_prior(X, 2, g, device=local)
     stream = torch.cuda.Stream(device=dev)
     ctx = sps.Sps(X, y, np.zeros(k), cov, J=J, N=N, seed=1, rank=rank, nranks=world, nccl_id=nccl_id,
                   device=local, stream=stream.cuda_stream)
@@ -237,7 +262,7 @@ def main():
     ctx.set_profiling(False)
     k1_avg_ms = cnt["k1_ms"] / max(cnt["k1_launches"], 1)
     pairs_per_launch = cnt["k1_pairs"] / max(cnt["k1_launches"], 1)
-    ops_per_pair = 2 * k * (WORKLOAD["C"] - 1) + EPILOGUE_DP_OPS_BINARY
+    ops_per_pair = 2 * k * (WORKLOAD["C"] - 1) + EPILOGUE_DP_OPS_BINARY  # (cfg4's k = 100: the same epilogue)
     achieved = pairs_per_launch * ops_per_pair / (k1_avg_ms * 1e-3) / 1e12
     # FP64 pipe slots actually issued per pair: k FMA-equivalents (DMMA + remainder DFMA) + epilogue ops
     pipe_tflops = pairs_per_launch * 2 * (k * (WORKLOAD["C"] - 1) + EPILOGUE_DP_OPS_BINARY) / (k1_avg_ms * 1e-3) / 1e12
@@ -296,39 +321,86 @@ def main():
         e2e = {"value": e2e_pairs / float(wt.item()), "unit": "pairs/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h)}
 
+    # ---- strong scaling: the same workload on ONE GPU (rank 0; the other ranks wait at the barrier)
+    strong_ref = None
+    if world > 1 and scaling == "strong" and not args.no_strong_ref:
+        if rank == 0:
+            c1 = sps.Sps(X, y, np.zeros(k), cov, J=J, N=N, seed=1, device=local, stream=stream.cuda_stream)
+            c1.run()  # warm-up (graphs, plans)
+            t1s = []
+            for s in range(args.steps):
+                with torch.cuda.stream(stream):
+                    flush.fill_(float(s))
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                c1.reset(seed=1 + s)
+                r1 = c1.run()
+                e1.record(stream)
+                stream.synchronize()
+                t1s.append(e0.elapsed_time(e1))
+            c1.close()
+            ms1 = sum(t1s) / len(t1s)
+            strong_ref = {"n_gpus": 1, "ms_per_step": ms1, "speedup": ms1 / (tot_ms / args.steps),
+                          "note": "same workload, same seeds, one context on rank 0's GPU (no NCCL)"}
+        barrier()
+
     # ---- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         p, dt = oracle_sample(X, y, oracle_cov(X), seed=7)
         cpu = {"value": p / dt, "unit": "pairs/s", "cores": os.cpu_count(), "kind": "oracle",
                "sample": sample_desc(), "seconds": dt}
+        # the oracle at THIS configuration (configs[1] exactly, seed 1), timed on a B200 host by
+        # tests/test_gpu_headline.py::test_run_parity_cfg2_full (same trajectory as the GPU run)
+        full = os.path.join(ROOT, "profiles", "r02_oracle_cfg2_full.json")
+        if os.path.exists(full) and args.workload == "cfg2":
+            fj = json.load(open(full))
+            cpu["same_config"] = {"value": fj["pairs_per_s"], "unit": "pairs/s", "wall_s": fj["oracle_wall_s"],
+                                  "threads": fj["threads"], "cpu_model": fj["cpu_model"],
+                                  "source": "profiles/r02_oracle_cfg2_full.json"}
+        # one core, configs[0] (the SURVEY 8(d) oracle-timing plan)
+        import oracle
+        import sps_synth as _syn
+
+        X1, y1 = _syn.config_data("cfg1")
+        t0 = time.perf_counter()
+        r1 = oracle.run(X1, y1, 2, 4, 128, seed=1, prior_mean=np.zeros(4), prior_cov=oracle.g_prior(X1, 2, 0.25),
+                        n_threads=1)
+        dt1 = time.perf_counter() - t0
+        cpu["cfg1_1core"] = {"value": r1["pairs"] / dt1, "unit": "pairs/s", "wall_s": dt1, "cores": 1}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD_DESC, "n": n, "k": k, "C": 2, "J": J, "N": N,
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": wdesc, "n": n, "k": k, "C": 2, "J": J, "N": N,
                        "global_particles": J * N, "parallelism": f"group-sharded x{world}" if world > 1 else "1 GPU",
                        "l2": "flushed (256 MiB device write) before every timed step",
                        "wall_s_to_posterior": tot_ms / args.steps / 1e3},
             "clocks": clk,
+            "strong_ref": strong_ref,
             "e2e": e2e,
             "gpu_launches": launches,
             # K1's contraction runs on the tensor cores' FP64 (DMMA) subpipe, which B200 shares with
             # the FP64 ALU pipe its epilogue uses: bound by that pipe, against its measured rate
             # (MEASURED_PEAKS.json carries no FP64 figure)
-            "roofline": {"bound": "tensor", "kernel": "k_loglik_bin_mma<6,1,2> (K1: fp64 DMMA contraction + fused softplus/product epilogue)",
+            "roofline": {"bound": "tensor", "kernel": f"k_loglik_bin_mma<{k // 4 if k <= 32 else (k + 3) // 4},{k % 4 if k <= 32 and k % 4 in (1, 2) else 0},2> (K1: fp64 DMMA contraction + fused softplus/product epilogue)",
                          "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
                          "ops_per_pair": ops_per_pair, "k1_avg_ms": k1_avg_ms,
                          "pairs_per_launch": pairs_per_launch, "k1_launches_per_run": cnt["k1_launches"],
                          "k1_share_of_step": k1_share,
-                         "fp64_pipe_frac": pipe_tflops / FP64_PEAK_TFLOPS,
-                         "contraction_frac": pairs_per_launch * 2 * k * (WORKLOAD["C"] - 1) / (k1_avg_ms * 1e-3) / 1e12
+                         # three readings of the same K1 time: (i) algorithmic contraction flops
+                         # 2k per pair; (ii) `frac` above, 2k flops + the 11 counted epilogue ops per pair;
+                         # (iii) FP64-pipe slots, k FMA + 11 epilogue ops per pair against 64 slots / clk / SM
+                         # -- what the shared DMMA / DFMA pipe actually enforces
+                         "frac_contraction": pairs_per_launch * 2 * k * (WORKLOAD["C"] - 1) / (k1_avg_ms * 1e-3) / 1e12
                          / FP64_PEAK_TFLOPS,
+                         "frac_pipe_slots": pipe_tflops / FP64_PEAK_TFLOPS,
                          "peak_source": "measured FP64 DMMA rate, 37.07 TF/s (tools/fp64_peaks.cu, profiles/r01_fp64_peaks.json; "
-                                        "the DFMA epilogue shares the pipe); ncu: profiles/r01_k1_full_ncu_v7.txt",
+                                        "the DFMA epilogue shares the pipe); ncu: profiles/r01_k1_full_ncu_v12.txt, "
+                                        "profiles/r02_ncu_fused_vs_k1.txt",
                          "full_data_eval": {"ms": full_ms, "pairs_per_s": full_pairs_s,
                                             "frac": full_pairs_s * ops_per_pair / 1e12 / FP64_PEAK_TFLOPS}},
             "cpu_baseline": cpu,

@@ -12,6 +12,17 @@
 
 namespace sps {
 
+// Slice layout (one rank): [Jl x d group sums S | d x d second moment | accepts | error |
+// nmon x Jl monitor group means a_m' S_j / N | d column sums of S].
+__host__ __device__ inline int slice_off_G(int Jl, int d) { return Jl * d + d * d + 2; }
+__host__ __device__ inline int slice_off_C(int Jl, int d, int nmon) { return slice_off_G(Jl, d) + nmon * Jl; }
+__host__ __device__ inline int slice_length(int Jl, int d, int nmon) { return slice_off_C(Jl, d, nmon) + d; }
+// k_mom_reduce grid: nm moment blocks (32 lower-triangle / column-sum entries each), ng group blocks
+// (whole groups: gpb = max(1, 256 / d) per block), one accepts block.
+__host__ __device__ inline int red_nm(int d) { return (d * (d + 1) / 2 + d + 31) / 32; }
+__host__ __device__ inline int red_gpb(int d) { return d <= 256 ? 256 / d : 1; }
+__host__ __device__ inline int red_ng(int Jl, int d) { return (Jl + red_gpb(d) - 1) / red_gpb(d); }
+
 // ---------------------------------------------------------------- K8 / K10
 // theta* = base + Lz z (z: Box-Muller pairs of the stream (id = p0 + p, step,
 // tag), R15) and lp* = -1/2 (theta* - mu)' Sinv (theta* - mu).  INIT: base =
@@ -1002,19 +1013,41 @@ __device__ void finalize_body(const FinArgs& f, double* sm) {
   if (f.trace && threadIdx.x == 0) f.trace[1] = gtimer();
   if (f.mode == 1 && threadIdx.x == 0) tl_mark_any(16);
   auto S = [&](int j, int i) -> double { return f.stage_S ? sS[j * d + i] : group_sum_global(f, j, i); };
-  // ---- theta-bar: lane = coordinate, warp = group subset, fixed-order combine
+  // ---- theta-bar: lane = coordinate, warp = group subset, fixed-order combine (S staged); otherwise
+  // from the per-rank column sums of S that k_mom_reduce put in the slices (large J: S stays in L2)
+  if (!f.stage_S) {
+    const int offC = slice_off_C(f.Jl, d, f.nmon), offG = slice_off_G(f.Jl, d);
+#pragma unroll 1
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+      double t = 0.0;
+#pragma unroll 1
+      for (int r = 0; r < f.G; ++r) t += __ldcg(f.gath + (int64_t)r * f.slice_len + offC + i);
+      sbar[i] = t / P;
+    }
+    // monitor group means (nmon x J) into sg, 4 independent loads in flight per thread
+    const int nG = f.nmon * J;
+#pragma unroll 1
+    for (int i0 = threadIdx.x; i0 < nG; i0 += 4 * blockDim.x) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int idx = i0 + u * blockDim.x;
+        const int m = idx / J, j = idx - m * J;
+        v[u] = idx < nG ? __ldcg(f.gath + (int64_t)(j / f.Jl) * f.slice_len + offG + m * f.Jl + (j % f.Jl)) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (i0 + u * blockDim.x < nG) sg[i0 + u * blockDim.x] = v[u];
+    }
+    __syncthreads();
+  } else
 #pragma unroll 1
   for (int i0 = 0; i0 < d; i0 += 32) {
     const int i = i0 + lane;
     double s = 0.0;
     if (i < d) {
-      if (f.stage_S) {
 #pragma unroll 4
-        for (int j = w; j < J; j += nw) s += sS[j * d + i];
-      } else {
-#pragma unroll 1
-        for (int j = w; j < J; j += nw) s += group_sum_global(f, j, i);
-      }
+      for (int j = w; j < J; j += nw) s += sS[j * d + i];
     }
     s_part[w][lane] = s;
     __syncthreads();
@@ -1088,15 +1121,20 @@ __device__ void finalize_body(const FinArgs& f, double* sm) {
       double gp = 0.0;
 #pragma unroll 1
       for (int j = lane; j < J; j += 32) {
-        double s0 = 0.0, s1 = 0.0;
-        int i = 0;
-        for (; i + 2 <= d; i += 2) {
-          s0 = fma(av[i], S(j, i), s0);
-          s1 = fma(av[i + 1], S(j, i + 1), s1);
+        double g;
+        if (f.stage_S) {
+          double s0 = 0.0, s1 = 0.0;
+          int i = 0;
+          for (; i + 2 <= d; i += 2) {
+            s0 = fma(av[i], S(j, i), s0);
+            s1 = fma(av[i + 1], S(j, i + 1), s1);
+          }
+          if (i < d) s0 = fma(av[i], S(j, i), s0);
+          g = (s0 + s1) / (double)f.N;
+          sg[m * J + j] = g;
+        } else {  // the same value, formed by k_mom_reduce's group blocks and staged above
+          g = sg[m * J + j];
         }
-        if (i < d) s0 = fma(av[i], S(j, i), s0);
-        const double g = (s0 + s1) / (double)f.N;
-        sg[m * J + j] = g;
         gp += g;
       }
       const double gbar = warp_sum(gp) / (double)J;
@@ -1165,6 +1203,8 @@ struct RedArgs {
   int tnt;             // tile layout: tiles per side (0: full layout)
   int N;               // particles per group (tile layout: group sums += N c)
   const double* shift;
+  const double* mon;   // nmon x d monitors: k_mom_reduce also writes the monitor group means and the
+  int nmon;            // column sums of S into the slice (finalize_body reads them when S is not staged)
 };
 __device__ __forceinline__ int red_col(const RedArgs& r, int i, int l) {  // entry (i, l), i >= l, of T'T
   if (!r.tnt) return r.d + i * r.d + l;
@@ -1189,20 +1229,25 @@ __global__ void __launch_bounds__(256) k_mom_reduce(RedArgs r, Ctl* ctl, double*
   if (f.mode == 1) tl_start(4);
   griddep_wait();  // the accept kernel's block partials
   const int d = r.d, Jl = r.Jl, W = r.W, nblk = r.nblk, dd = d * d, nl = d * (d + 1) / 2;
-  const int nm = (nl + 31) / 32, ng = (Jl * d + 255) / 256;
+  const int nm = red_nm(d), ng = red_ng(Jl, d), gpb = red_gpb(d);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if ((int)blockIdx.x < nm) {
+    // entries e < nl: (i, l) of the lower triangle of the second moment; nl <= e < nl + d: column sum
+    // l = e - nl of the group sums over all blocks (the ones row of the tile layout)
     const int e = blockIdx.x * 32 + lane;
-    int i = 0, l = 0;
+    int i = 0, l = 0, col = 0;
     if (e < nl) {  // e = i (i + 1) / 2 + l
       i = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
       while (i * (i + 1) / 2 > e) --i;
       while ((i + 1) * (i + 2) / 2 <= e) ++i;
       l = e - i * (i + 1) / 2;
+      col = red_col(r, i, l);
+    } else if (e < nl + d) {
+      l = e - nl;
+      col = r.tnt ? red_col(r, d, l) : l;
     }
-    const int col = red_col(r, i, l);
     double acc8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    if (e < nl) {
+    if (e < nl + d) {
 #pragma unroll 1
       for (int b0 = w; b0 < nblk; b0 += 256) {
         double v[32];
@@ -1217,22 +1262,51 @@ __global__ void __launch_bounds__(256) k_mom_reduce(RedArgs r, Ctl* ctl, double*
     }
     part[w][lane] = ((acc8[0] + acc8[1]) + (acc8[2] + acc8[3])) + ((acc8[4] + acc8[5]) + (acc8[6] + acc8[7]));
     __syncthreads();
-    if (w == 0 && e < nl) {
+    if (w == 0 && e < nl + d) {
       double t = part[0][lane];
       for (int q = 1; q < 8; ++q) t += part[q][lane];
-      slice[Jl * d + i * d + l] = t;
-      slice[Jl * d + l * d + i] = t;
+      if (e < nl) {
+        slice[Jl * d + i * d + l] = t;
+        slice[Jl * d + l * d + i] = t;
+      } else {
+        slice[slice_off_C(Jl, d, r.nmon) + l] = r.tnt ? t + (double)Jl * (double)r.N * r.shift[l] : t;
+      }
     }
   } else if ((int)blockIdx.x < nm + ng) {
-    const int idx = (blockIdx.x - nm) * 256 + threadIdx.x;
-    if (idx < Jl * d) {
-      const int j = idx / d, c = idx % d;
-      const int col = r.tnt ? red_col(r, d, c) : c;
-      double s = 0.0;
-      for (int b = 0; b < r.bpg; ++b) s += r.bpart[(int64_t)(j * r.bpg + b) * W + col];
-      if (r.tnt) s += (double)r.N * r.shift[c];
-      slice[idx] = s;
+    // whole groups j0 .. j0 + gpb - 1: their sums S_j, then the monitor group means a_m' S_j / N (the
+    // finalize_body arithmetic, two interleaved fma chains)
+    __shared__ double sgrp[512];
+    const int j0 = (blockIdx.x - nm) * gpb;
+#pragma unroll 1
+    for (int t = threadIdx.x; t < gpb * d; t += blockDim.x) {
+      const int j = j0 + t / d, c = t % d;
+      if (j < Jl) {
+        const int col = r.tnt ? red_col(r, d, c) : c;
+        double s = 0.0;
+        for (int b = 0; b < r.bpg; ++b) s += r.bpart[(int64_t)(j * r.bpg + b) * W + col];
+        if (r.tnt) s += (double)r.N * r.shift[c];
+        slice[j * d + c] = s;
+        if (t < 512) sgrp[t] = s;
+      }
     }
+    __syncthreads();
+    if (r.mon && gpb * d <= 512)
+#pragma unroll 1
+      for (int t = threadIdx.x; t < r.nmon * gpb; t += blockDim.x) {
+        const int m = t / gpb, jj = t % gpb, j = j0 + jj;
+        if (j < Jl) {
+          const double* av = r.mon + m * d;
+          const double* Sj = sgrp + jj * d;
+          double s0 = 0.0, s1 = 0.0;
+          int i = 0;
+          for (; i + 2 <= d; i += 2) {
+            s0 = fma(av[i], Sj[i], s0);
+            s1 = fma(av[i + 1], Sj[i + 1], s1);
+          }
+          if (i < d) s0 = fma(av[i], Sj[i], s0);
+          slice[slice_off_G(Jl, d) + m * Jl + j] = (s0 + s1) / (double)r.N;
+        }
+      }
   } else {
     double s = 0.0;
     for (int b = threadIdx.x; b < nblk; b += 256) s += r.bpart[(int64_t)b * W + W - 1];

@@ -859,8 +859,9 @@ sps_status accept_moments(sps_ctx* c, bool decide, int nchunks, double temper, u
     TRY(launch_normals(c, TAG_PROPOSAL, fork_step + 1u, (int)((fork_step + 1u) & 1u), c->capturing, true));
   }
   const int d = c->d;
-  const int nm = (d * (d + 1) / 2 + 31) / 32, ng = (c->Jl * d + 255) / 256;
-  RedArgs r{c->bpart, c->nblk, c->N / c->tp, c->Jl, d, c->acc_tnt > 0 ? c->Wt : c->W, c->acc_tnt, c->N, c->shift};
+  const int nm = red_nm(d), ng = red_ng(c->Jl, d);
+  RedArgs r{c->bpart, c->nblk, c->N / c->tp, c->Jl, d, c->acc_tnt > 0 ? c->Wt : c->W, c->acc_tnt, c->N, c->shift,
+            c->mon, c->nmon};
   FinArgs none{};
   if (fin && fin->stage_S && c->red_cluster > 0) {  // one rank: reduce + finalize as one cluster (DSMEM)
     FinArgs f = *fin;
@@ -1178,7 +1179,7 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
       c->fu_smem = (size_t)fused_smem_doubles(round_up(c->k, 4), c->d) * sizeof(double);
     }
   }
-  c->slice_len = c->Jl * d + d * d + 2;
+  c->slice_len = slice_length(c->Jl, d, c->nmon);
   c->max_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(64, ((int64_t)1 << 26) / std::max<int64_t>(c->Pl, 1)));
   c->Bmax = (int)std::max<int64_t>(8, std::min<int64_t>(ESS_RANK_THREADS, ((int64_t)1 << 23) / std::max<int64_t>(c->Pl, 1)));
 

@@ -51,7 +51,7 @@ def _sharded(sps, G, X, y, cov, J, N, seed, **kw):
     return out
 
 
-@pytest.mark.parametrize("G", [2, 4])
+@pytest.mark.parametrize("G", [2, 4, 8])
 @pytest.mark.parametrize("tempering", [0, 1])
 def test_loopback_sharded_matches_single_rank(sps, orc, G, tempering):
     X, y = sps_synth.config_data("cfg1")
@@ -116,3 +116,46 @@ def test_loopback_sharded_two_pass_and_predictive(sps, orc):
         assert np.allclose(rep["mean"], single["mean"], atol=1e-9, rtol=0)
     assert abs(out[0]["logml"] - o2["logml"]) <= 1e-6
     assert np.all(np.abs(out[0]["logpl"] - o2["logpl"]) <= 1e-9)
+
+
+def _check_sharded(res, single, o, tol_single=1e-9):
+    for rep, _ in res:
+        assert rep["L"] == single["L"] == o["L"]
+        assert np.array_equal(rep["t_cycle"], single["t_cycle"]) and np.array_equal(rep["t_cycle"], o["t_cycle"])
+        assert np.array_equal(rep["R_cycle"], single["R_cycle"]) and np.array_equal(rep["R_cycle"], o["R_cycle"])
+        assert np.array_equal(rep["h_cycle"], single["h_cycle"])
+        assert abs(rep["logml"] - single["logml"]) < tol_single
+        assert np.allclose(rep["mean"], single["mean"], atol=tol_single, rtol=0)
+    assert abs(res[0][0]["logml"] - o["logml"]) <= 1e-6
+    assert abs(res[0][0]["logml_nse"] - o["logml_nse"]) <= 1e-6
+    assert np.all(np.abs(res[0][0]["mean"] - o["mean"]) <= 1e-6)
+
+
+@pytest.mark.parametrize("G", [2, 8])
+def test_loopback_sharded_d25(sps, orc, G):
+    """The bench shape's kernels (d = 25: k_propose_rb<7>, k_accept_tile<4>, warp Cholesky at d = 25) on
+    the sharded path, G = 2 and 8 ranks of the German-credit-shaped data."""
+    X, y = sps_synth.config_data("cfg2", n=300)
+    cov = orc.g_prior(X, 2, 1.0 / 16)
+    J, N, seed = 8, 256, 2
+    s = sps.Sps(X, y, np.zeros(25), cov, J=J, N=N, seed=seed)
+    single = s.run()
+    s.close()
+    o = orc.run(X, y, 2, J, N, seed=seed, prior_mean=np.zeros(25), prior_cov=cov)
+    _check_sharded(_sharded(sps, G, X, y, cov, J, N, seed), single, o)
+
+
+def test_large_J_unstaged_finalize(sps, orc):
+    """J = 8192 groups (J x d too large to stage in the finalize block's shared memory): theta-bar and
+    the monitor group means come from the column sums / group means k_mom_reduce writes into the stats
+    slice -- single rank and G = 8 loopback ranks (1024 groups each) against the oracle."""
+    X, y = sps_synth.config_data("cfg1")
+    cov = orc.g_prior(X, 2, 0.25)
+    J, N, seed = 8192, 16, 1
+    s = sps.Sps(X, y, np.zeros(4), cov, J=J, N=N, seed=seed)
+    single = s.run()
+    s.close()
+    o = orc.run(X, y, 2, J, N, seed=seed, prior_mean=np.zeros(4), prior_cov=cov)
+    assert o["status"] == 0
+    _check_sharded([(single, None)], single, o)
+    _check_sharded(_sharded(sps, 8, X, y, cov, J, N, seed), single, o)
