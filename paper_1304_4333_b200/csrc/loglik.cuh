@@ -670,6 +670,205 @@ __global__ void __launch_bounds__(128, MINB) k_loglik_bin_mma(LLArgs a) {
   tl_end(2);
 }
 
+// ---------------------------------------------------------------------------
+// Multinomial (C = CM1 + 1 >= 3), contraction on DMMA (mma.sync m8n8k4 f64): each warp owns
+// NTW x 8 particles; class c = 1..C-1 of those particles is its own n-tile (B = theta_c
+// fragments in registers), so one A fragment of X (8 observations x 4 covariates, from shared
+// memory) feeds NTW x CM1 DMMAs and lane (ar, ac) ends with eta_c of observation ar and
+// particles 2 ac, 2 ac + 1 of every n-tile, for all classes at once.  k = 4 KKD + REM: the
+// last REM (<= 2) covariates are DFMAs on the accumulators (as in the binary kernel).
+// Epilogue per (observation, particle): log p = eta_y - log(1 + sum_c e^eta_c), the logs deferred
+// into a running product (renormalised every observation: 1 + sum e^eta can reach C e^704), the
+// max-shifted form only when some |eta_c| >= 704 (R17).  X streams through two shared-memory
+// sub-chunk buffers by TMA bulk copies; the labels of a sub-chunk ride along in a small array.
+template <int KKD, int REM, int CM1, int NTW = 2, int MINB = 4>
+__global__ void __launch_bounds__(128, MINB) k_loglik_mnl_mma(LLArgs a) {
+  constexpr int KP = 4 * KKD + (REM ? 4 : 0);
+  extern __shared__ __align__(16) double smem[];
+  double* sT = smem;        // 64: exp table 2^(i/64) (256 reserved)
+  double* sX = smem + 256;  // 2 x SR x KP
+  __shared__ int sY[2][64];
+  __shared__ __align__(8) uint64_t xbar[2];
+  const double tv = threadIdx.x < 64 ? __ldg(c_exp2tab + threadIdx.x) : 0.0;
+  if (a.stop && *a.stop) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, ar = lane >> 2, ac = lane & 3;
+  const int tile = blockIdx.x, cy = blockIdx.y;
+  const int c0 = a.t0 + cy * a.chunk;
+  const int c1 = min(c0 + a.chunk, a.t1);
+  const int ntot = max(c1 - c0, 0);
+  const int sub = a.sub > 0 ? a.sub : ntot;
+  const int SR = (sub + 15) & ~15;
+  if (threadIdx.x < 64) sT[threadIdx.x] = tv;
+  if (threadIdx.x == 0) {
+    mbar_init(&xbar[0], 1);
+    mbar_init(&xbar[1], 1);
+  }
+  auto issue = [&](int cs, int buf) {
+    const unsigned bytes = (unsigned)(min(sub, ntot - cs) * KP * 8);
+    mbar_arrive_expect_tx(&xbar[buf], bytes);
+    bulk_g2s(sX + buf * SR * KP, a.X + (int64_t)(c0 + cs) * KP, bytes, &xbar[buf]);
+  };
+  if (threadIdx.x < 64 && threadIdx.x < ntot && threadIdx.x < sub) sY[0][threadIdx.x] = __ldg(a.y + c0 + threadIdx.x);
+  __syncthreads();
+  if (threadIdx.x == 0 && ntot > 0) issue(0, 0);  // X does not depend on the predecessor
+  griddep_wait();  // theta (the proposal kernel's output) from here on
+  const int64_t pw = ((int64_t)tile * 4 + w) * (NTW * 8);
+  double b[NTW][CM1][KKD > 0 ? KKD : 1];
+  double tr[NTW][CM1][2][REM > 0 ? REM : 1];
+#pragma unroll
+  for (int nt = 0; nt < NTW; ++nt) {
+    const int64_t p = pw + nt * 8 + ar;
+    const double* row = a.theta + (p < a.P ? p : 0) * a.ldt;
+#pragma unroll
+    for (int c = 0; c < CM1; ++c)
+#pragma unroll
+      for (int kk = 0; kk < KKD; ++kk) {
+        const int k = kk * 4 + ac;
+        b[nt][c][kk] = (p < a.P && k < a.k) ? __ldg(row + c * a.k + k) : 0.0;
+      }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int64_t q = pw + nt * 8 + 2 * ac + e;
+      const double* rq = a.theta + (q < a.P ? q : 0) * a.ldt;
+#pragma unroll
+      for (int c = 0; c < CM1; ++c)
+#pragma unroll
+        for (int r = 0; r < REM; ++r) tr[nt][c][e][r] = q < a.P ? __ldg(rq + c * a.k + 4 * KKD + r) : 0.0;
+    }
+  }
+  double D[NTW][2], Pp[NTW][2];
+  int E[NTW][2];
+#pragma unroll
+  for (int nt = 0; nt < NTW; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      D[nt][e] = 0.0;
+      Pp[nt][e] = 1.0;
+      E[nt][e] = 0;
+    }
+  int it = 0;
+  for (int cs = 0; cs < ntot; cs += sub) {
+    const int nobs = min(sub, ntot - cs);
+    const int buf = it & 1;
+    if (cs + sub < ntot) {
+      if (threadIdx.x == 0) issue(cs + sub, buf ^ 1);  // buf ^ 1 released by the barrier below
+      const int nn = min(sub, ntot - cs - sub);
+      if (threadIdx.x < nn) sY[buf ^ 1][threadIdx.x] = __ldg(a.y + c0 + cs + sub + threadIdx.x);
+    }
+    mbar_wait(&xbar[buf], (unsigned)(it >> 1) & 1u);
+    ++it;
+    const double* sXb = sX + buf * SR * KP;
+    for (int t0 = 0; t0 < nobs; t0 += 8) {
+      double acc[NTW][CM1][2];
+#pragma unroll
+      for (int nt = 0; nt < NTW; ++nt)
+#pragma unroll
+        for (int c = 0; c < CM1; ++c) acc[nt][c][0] = acc[nt][c][1] = 0.0;
+      const double* xr = sXb + (t0 + ar) * KP;
+#pragma unroll
+      for (int kk = 0; kk < KKD; ++kk) {
+        const double av = xr[kk * 4 + ac];
+#pragma unroll
+        for (int nt = 0; nt < NTW; ++nt)
+#pragma unroll
+          for (int c = 0; c < CM1; ++c) dmma884(acc[nt][c][0], acc[nt][c][1], av, b[nt][c][kk]);
+      }
+#pragma unroll
+      for (int r = 0; r < REM; ++r) {
+        const double xv = xr[4 * KKD + r];
+#pragma unroll
+        for (int nt = 0; nt < NTW; ++nt)
+#pragma unroll
+          for (int c = 0; c < CM1; ++c) {
+            acc[nt][c][0] = fma(xv, tr[nt][c][0][r], acc[nt][c][0]);
+            acc[nt][c][1] = fma(xv, tr[nt][c][1][r], acc[nt][c][1]);
+          }
+      }
+      if (t0 + ar < nobs) {  // rows past the sub-chunk hold stale data
+        const int yt = sY[buf][t0 + ar];
+#pragma unroll
+        for (int nt = 0; nt < NTW; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            // unshifted 1 + sum_c e^eta_c (reference class: e^0 = 1), C - 1 exps, no max
+            double ey = 0.0, v = 1.0;
+            int big = 0;
+#pragma unroll
+            for (int c = 0; c < CM1; ++c) {
+              const double eta = acc[nt][c][e];
+              ey = (yt == c + 1) ? eta : ey;
+              big |= (__double2hiint(eta) & 0x7fffffff) >= 0x40860000;  // |eta| >= 704, inf, nan
+              v += exp_neg(-eta, sT);
+            }
+            D[nt][e] -= ey;
+            if (big) {
+              double m = 0.0;
+#pragma unroll
+              for (int c = 0; c < CM1; ++c) m = fmax(m, acc[nt][c][e]);
+              v = exp_neg(abs_clamp708(m), sT);
+#pragma unroll
+              for (int c = 0; c < CM1; ++c) v += exp_neg(abs_clamp708(m - acc[nt][c][e]), sT);
+              D[nt][e] += m;
+            }
+            Pp[nt][e] *= v;
+            renorm(Pp[nt][e], E[nt][e]);
+          }
+      }
+    }
+    __syncthreads();  // every warp is done with buffer `buf` (and its labels) before they are refilled
+  }
+  {  // combine the 8 lanes of each particle column (the binary kernel's reduce-scatter)
+    constexpr int V = 2 * NTW;
+    double m[V], pp[V];
+    int ex[V];
+#pragma unroll
+    for (int nt = 0; nt < NTW; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        renorm(Pp[nt][e], E[nt][e]);
+        m[nt * 2 + e] = D[nt][e];
+        pp[nt * 2 + e] = Pp[nt][e];
+        ex[nt * 2 + e] = E[nt][e];
+      }
+    int jsel = 0, cnt = V;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int o = 4 << r;
+      const int bit = (ar >> r) & 1;
+      if (cnt > 1) {
+        const int h = cnt / 2;
+#pragma unroll
+        for (int q = 0; q < V / 2; ++q) {
+          if (q < h) {
+            const double sm = bit ? m[q] : m[q + h], sp = bit ? pp[q] : pp[q + h];
+            const int se = bit ? ex[q] : ex[q + h];
+            const double km = bit ? m[q + h] : m[q], kp = bit ? pp[q + h] : pp[q];
+            const int ke = bit ? ex[q + h] : ex[q];
+            m[q] = km + __shfl_xor_sync(0xffffffffu, sm, o);
+            pp[q] = kp * __shfl_xor_sync(0xffffffffu, sp, o);  // 8 factors in [1,2): < 2^8
+            ex[q] = ke + __shfl_xor_sync(0xffffffffu, se, o);
+          }
+        }
+        jsel += bit * h;
+        cnt = h;
+      } else {
+        m[0] += __shfl_xor_sync(0xffffffffu, m[0], o);
+        pp[0] *= __shfl_xor_sync(0xffffffffu, pp[0], o);
+        ex[0] += __shfl_xor_sync(0xffffffffu, ex[0], o);
+      }
+    }
+    const int rest = ar >> (V == 8 ? 3 : V == 4 ? 2 : 1);
+    const int64_t p = pw + (jsel >> 1) * 8 + 2 * ac + (jsel & 1);
+    if (rest == 0 && p < a.P) {
+      double pv = pp[0];
+      int xv = ex[0];
+      renorm(pv, xv);
+      a.part[(int64_t)cy * a.P + p] = -(m[0] + (log(pv) + (double)xv * 0x1.62e42fefa39efp-1));
+    }
+  }
+  griddep_launch();
+}
+
 // Sum chunk partials in chunk order: out[p] = sum_c part[c][p].  bad (may be null):
 // the smallest p whose sum is not finite (sps_loglik's error check).
 __global__ void k_sum_chunks(const double* __restrict__ part, int nchunks, int64_t P, double* __restrict__ out,

@@ -1,0 +1,286 @@
+// ozaki.cuh -- K1 for the binary model with 64 <= k <= 128 (configs[3]: k = 100) on the 5th-generation
+// tensor cores: the FP64 contraction eta_tp = x~_t' theta_p is reproduced from INT8 tcgen05 MMAs with
+// int32 accumulators in TMEM (Ozaki-style splitting), then the same deferred-log
+// softplus epilogue as the DMMA kernels.  PAPER.md:129-131 asks for the likelihood "to machine
+// accuracy": the split below keeps the contraction error ~1e-13 relative (bar 1e-10 on L_p).
+//
+// Splitting (exact FP64 steps: scaling by powers of two and subtracting integers):
+//   row scale sigma = 2^e, e = ilogb(max_i |v_i|) + 1, so |v_i| / sigma < 1;
+//   r = v / sigma; V_0 = rint(64 r), r = 64 r - V_0; V_a = rint(128 r), r = 128 r - V_a (a >= 1)
+//   => v = sigma * sum_{a < S} V_a 2^(-6 - 7a) + O(sigma 2^(-6 - 7S)),  |V_a| <= 64 (int8).
+// Product: eta = sigma_t tau_p sum_{a,b} X_a T_b 2^(-12 - 7(a + b)); the int8 GEMMs of one level
+// L = a + b share a TMEM accumulator (|C_L| <= 7 * 128 * 64^2 < 2^22); levels L > LMAX = S - 1 are
+// dropped (their weight <= 2^(-12 - 7 S) k); the epilogue folds the levels exactly in int64,
+// acc = sum_L C_L 2^(7 (LMAX - L)) (< 2^62), eta = (double) acc * sigma_t * tau_p * 2^(-12 - 7 LMAX).
+//
+// Operand images (built by k_oz_slice: one thread per row, 16-byte stores, coalesced) are the UMMA
+// K-major SWIZZLE_NONE canonical layout -- core matrices of 8 rows x 16 bytes, row groups at SBO =
+// 128 B, 16-byte K chunks at LBO -- so one 1-D bulk copy lands a tile in shared memory ready for
+// the MMA descriptors:
+//   particle tile (M = 128 rows): [128 doubles tau][S slices][2 KB chunks][16 groups][8][16 B]
+//   observation tile (N = 32 rows): [32 doubles sigma][S slices][2 KB chunks][4 groups][8][16 B]
+// Kernel (one CTA per 128-particle tile x observation chunk, 6 warps, warp-specialised):
+//   warp 0: producer -- bulk copies of observation tiles through a 3-stage ring;
+//   warp 1: TMEM owner + MMA issuer -- per observation tile, KB x S(S+1)/2 tcgen05.mma.kind::i8
+//           (M = 128 particles, N = 32 observations, K = 32) into the level accumulators of one of
+//           two TMEM buffers (2 x S x 32 columns);
+//   warps 2-5: epilogue -- tcgen05.ld of the S levels (thread = particle = TMEM lane), int64 fold,
+//           scale, softplus into the per-particle deferred-log product, release the buffer.
+#pragma once
+#include "loglik.cuh"
+
+namespace sps {
+
+constexpr int OZ_S = 7;              // slices per operand
+constexpr int OZ_LMAX = OZ_S - 1;    // highest level kept
+constexpr int OZ_MT = 128;           // particles per tile (MMA M, TMEM lanes)
+constexpr int OZ_NT = 32;            // observations per tile (MMA N)
+constexpr int OZ_STAGES = 3;
+constexpr int OZ_NPAIR = OZ_S * (OZ_S + 1) / 2;
+
+__host__ __device__ constexpr int oz_slice_bytes(int rows, int KB) { return rows * KB * 32; }
+__host__ __device__ constexpr int oz_tile_bytes(int rows, int KB) { return rows * 8 + OZ_S * oz_slice_bytes(rows, KB); }
+
+// Split `rows` rows of v (row stride ld, k used columns) into tile images (rows per tile R = 128 or 32).
+__global__ void k_oz_slice(const double* __restrict__ v, int64_t rows, int64_t ld, int k, int KB, int R,
+                           int64_t row0, uint8_t* __restrict__ out, const int* stop) {
+  if (stop && *stop) return;  // speculative M step after the stop
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // image row (row0 + r is the data row)
+  const int64_t ntile = (rows + R - 1) / R;
+  if (r >= ntile * R) return;
+  const int64_t tile = r / R;
+  const int rr = (int)(r % R);
+  const int64_t drow = row0 + r;
+  const bool valid = r < rows;
+  const double* src = v + (valid ? drow : 0) * ld;
+  double mx = 0.0;
+  if (valid)
+    for (int i = 0; i < k; ++i) mx = fmax(mx, fabs(src[i]));
+  const int e = mx > 0.0 ? ilogb(mx) + 1 : 0;
+  uint8_t* tb = out + tile * (int64_t)oz_tile_bytes(R, KB);
+  reinterpret_cast<double*>(tb)[rr] = ldexp(1.0, e);
+  const int ngrp = R / 8, nch = 2 * KB;
+  double rem[16];
+  for (int c = 0; c < nch; ++c) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int i = c * 16 + j;
+      rem[j] = (valid && i < k) ? ldexp(src[i], -e) : 0.0;
+    }
+#pragma unroll 1
+    for (int a = 0; a < OZ_S; ++a) {
+      uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const double s = rem[j] * (a == 0 ? 64.0 : 128.0);
+        const double q = rint(s);
+        rem[j] = s - q;
+        w[j >> 2] |= (uint32_t)(uint8_t)(int8_t)(int)q << (8 * (j & 3));
+      }
+      uint8_t* dst = tb + R * 8 + (int64_t)a * oz_slice_bytes(R, KB) + ((int64_t)c * ngrp + rr / 8) * 128 + (rr % 8) * 16;
+      *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+}
+
+// UMMA shared-memory descriptor, K-major SWIZZLE_NONE (version 1, base offset 0).
+__device__ __forceinline__ uint64_t oz_desc(const void* smem, uint32_t lbo, uint32_t sbo) {
+  const uint64_t a = (uint64_t)(smem_u32(smem) >> 4) & 0x3fffull;
+  return a | ((uint64_t)((lbo >> 4) & 0x3fff) << 16) | ((uint64_t)((sbo >> 4) & 0x3fff) << 32) | (1ull << 46);
+}
+// Instruction descriptor: kind::i8, D = S32, A = B = signed int8, both K-major, M = 128, N = 32.
+constexpr uint32_t OZ_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ_NT >> 3) << 17) |
+                              ((uint32_t)(OZ_MT >> 4) << 24);
+
+__device__ __forceinline__ void oz_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(OZ_IDESC), "r"(accumulate), "r"(0u), "r"(0u), "r"(0u), "r"(0u));
+}
+__device__ __forceinline__ void oz_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void oz_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void oz_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar)) : "memory");
+}
+// 32 consecutive TMEM columns of this thread's lane (32x32b shape, x32)
+// (the registers of tcgen05.ld are defined only after tcgen05.wait::ld: one asm statement, so no use
+// of them can be scheduled in between)
+__device__ __forceinline__ void oz_tmem_ld32_wait(uint32_t taddr, int32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n\t"
+      "tcgen05.wait::ld.sync.aligned;\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr)
+      : "memory");
+}
+// mbarrier wait that traps instead of hanging (a descriptor or protocol error must fail the launch,
+// not wedge the GPU): ~2^31 polls, seconds
+__device__ __forceinline__ void oz_wait(uint64_t* bar, unsigned phase) {
+  uint32_t done = 0;
+  for (uint32_t n = 0;; ++n) {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(done)
+                 : "r"(smem_u32(bar)), "r"(phase)
+                 : "memory");
+    if (done) return;
+    if (n > (1u << 31)) __trap();
+  }
+}
+
+struct OzArgs {
+  const uint8_t* Ti;   // particle tile images (this launch's theta)
+  const uint8_t* Xi;   // observation tile images (X, static)
+  double* part;        // [S][P] chunk partials
+  int64_t P;
+  int32_t t0, t1, chunk;
+  const int* stop;
+};
+
+template <int KB>
+__host__ __device__ constexpr int oz_smem_bytes() {
+  return oz_tile_bytes(OZ_MT, KB) + OZ_STAGES * oz_tile_bytes(OZ_NT, KB);
+}
+
+template <int KB>
+__global__ void __launch_bounds__(192, 1) k_oz_loglik(OzArgs a) {
+  constexpr int TA = oz_tile_bytes(OZ_MT, KB), TB = oz_tile_bytes(OZ_NT, KB);
+  constexpr int SA = oz_slice_bytes(OZ_MT, KB), SB = oz_slice_bytes(OZ_NT, KB);
+  constexpr uint32_t LBO_A = (OZ_MT / 8) * 128, LBO_B = (OZ_NT / 8) * 128, SBO = 128;
+  extern __shared__ __align__(1024) uint8_t ozs[];
+  uint8_t* sA = ozs;
+  uint8_t* sB = ozs + TA;
+  __shared__ __align__(8) uint64_t a_full, full[OZ_STAGES], empty[OZ_STAGES], tfull[2], tempty[2];
+  __shared__ uint32_t s_tmem;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (a.stop && *a.stop) return;
+  griddep_wait();  // theta images of this launch
+  const int tile = blockIdx.x, cy = blockIdx.y;
+  const int c0 = a.t0 + cy * a.chunk;
+  const int c1 = min(c0 + a.chunk, a.t1);
+  const int ob0 = c0 / OZ_NT, ob1 = (c1 + OZ_NT - 1) / OZ_NT;  // observation tiles [ob0, ob1)
+  const int nob = c1 > c0 ? ob1 - ob0 : 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&a_full, 1);
+    for (int s = 0; s < OZ_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1 + 4);  // the MMA commit + the 4 epilogue warps (they read the scales)
+    }
+    for (int u = 0; u < 2; ++u) {
+      mbar_init(&tfull[u], 1);
+      mbar_init(&tempty[u], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {  // TMEM: 2 buffers x OZ_S levels x 32 columns (<= 512)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&s_tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  oz_fence_before();
+  __syncthreads();
+  oz_fence_after();
+  const uint32_t tmem = s_tmem;
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&a_full, (unsigned)TA);
+      bulk_g2s(sA, a.Ti + (int64_t)tile * TA, (unsigned)TA, &a_full);
+      for (int i = 0; i < nob; ++i) {
+        const int s = i % OZ_STAGES;
+        if (i >= OZ_STAGES) oz_wait(&empty[s], (unsigned)((i / OZ_STAGES) - 1) & 1u);
+        mbar_arrive_expect_tx(&full[s], (unsigned)TB);
+        bulk_g2s(sB + s * TB, a.Xi + (int64_t)(ob0 + i) * TB, (unsigned)TB, &full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      oz_wait(&a_full, 0u);
+      for (int i = 0; i < nob; ++i) {
+        const int s = i % OZ_STAGES, u = i & 1;
+        oz_wait(&full[s], (unsigned)(i / OZ_STAGES) & 1u);
+        if (i >= 2) oz_wait(&tempty[u], (unsigned)((i >> 1) - 1) & 1u);
+        oz_fence_after();
+        const uint8_t* bb = sB + s * TB + OZ_NT * 8;
+        const uint32_t dbase = tmem + (uint32_t)(u * OZ_S * OZ_NT);
+#pragma unroll
+        for (int kb = 0; kb < KB; ++kb)
+#pragma unroll
+          for (int xa = 0; xa < OZ_S; ++xa)
+#pragma unroll
+            for (int tb = 0; tb + xa <= OZ_LMAX; ++tb) {
+              const uint64_t ad = oz_desc(sA + OZ_MT * 8 + tb * SA + 2 * kb * LBO_A, LBO_A, SBO);
+              const uint64_t bd = oz_desc(bb + xa * SB + 2 * kb * LBO_B, LBO_B, SBO);
+              oz_mma(dbase + (uint32_t)((xa + tb) * OZ_NT), ad, bd, (kb > 0 || xa > 0) ? 1u : 0u);
+            }
+        oz_commit(&empty[s]);  // the stage's operands are consumed once these MMAs complete
+        oz_commit(&tfull[u]);  // the accumulators of buffer u are ready
+      }
+    }
+  } else {  // epilogue: warp w accesses TMEM lanes 32 (w % 4) .. 32 (w % 4) + 31
+    const int q = warp & 3;
+    const int pl = 32 * q + lane;  // particle of the tile = TMEM lane
+    const int64_t p = (int64_t)tile * OZ_MT + pl;
+    oz_wait(&a_full, 0u);
+    const double wp = reinterpret_cast<const double*>(sA)[pl] * 0x1p-54;  // tau_p 2^(-12 - 7 LMAX)
+    __shared__ double sT[64];
+    if (warp == 2) {
+      sT[lane] = __ldg(c_exp2tab + lane);
+      sT[lane + 32] = __ldg(c_exp2tab + lane + 32);
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps
+    double M = 0.0, Pp = 1.0;
+    int E = 0;
+    for (int i = 0; i < nob; ++i) {
+      const int s = i % OZ_STAGES, u = i & 1;
+      oz_wait(&tfull[u], (unsigned)(i >> 1) & 1u);
+      oz_fence_after();
+      long long acc[OZ_NT];
+#pragma unroll
+      for (int j = 0; j < OZ_NT; ++j) acc[j] = 0;
+      const uint32_t tb = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(u * OZ_S * OZ_NT);
+#pragma unroll
+      for (int L = 0; L < OZ_S; ++L) {
+        int32_t v[32];
+        oz_tmem_ld32_wait(tb + (uint32_t)(L * OZ_NT), v);
+#pragma unroll
+        for (int j = 0; j < OZ_NT; ++j) acc[j] += (long long)v[j] << (7 * (OZ_LMAX - L));
+      }
+      oz_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[u]);  // buffer u may take the next tile's MMAs
+      const double* sc = reinterpret_cast<const double*>(sB + s * TB);  // sigma_t of the tile's observations
+      const int tb0 = (ob0 + i) * OZ_NT;
+#pragma unroll
+      for (int j = 0; j < OZ_NT; ++j) {
+        const int t = tb0 + j;
+        if (t >= c0 && t < c1) {
+          const double s_ = (double)acc[j] * (wp * sc[j]);  // eta (sign-flipped rows: log p = -softplus)
+          M += relu_bits(s_);
+          const double ex = exp_neg(abs_clamp708(s_), sT);
+          Pp = fma(Pp, ex, Pp);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);  // (with the MMA commit) the stage may be refilled
+      renorm(Pp, E);
+    }
+    if (p < a.P) a.part[(int64_t)cy * a.P + p] = -(M + (log(Pp) + (double)E * 0x1.62e42fefa39efp-1));
+  }
+  oz_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    oz_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+  griddep_launch();
+}
+
+}  // namespace sps

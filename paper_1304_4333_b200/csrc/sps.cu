@@ -32,6 +32,7 @@
 #include "loglik.cuh"
 #include "mstep.cuh"
 #include "fused.cuh"
+#include "ozaki.cuh"
 
 using namespace sps;
 
@@ -186,6 +187,11 @@ struct sps_ctx {
   int fu_TPR = 1;
   unsigned* fu_tick = nullptr;
   double* fu_tpart = nullptr;
+  // K1 on INT8 tensor cores (binary, 64 <= k <= 128; ozaki.cuh): K-blocks of 32, operand images
+  int oz_KB = 0;
+  uint8_t* oz_X = nullptr;  // observation tile images (built once at create)
+  uint8_t* oz_T = nullptr;  // particle tile images of the theta of the current launch
+  size_t oz_T_cap = 0;
   struct Plan {
     int64_t P = -1;
     int range = -1, max_chunks = -1, S = 1, chunk = 0, sub = 0, occ = 1;
@@ -485,6 +491,46 @@ bool choose_ll(int k, int C, LLChoice* o) {
     if (k <= 64) { *o = {ll_ptr<64, 1, 1>(), 64, 1}; return true; }
     return false;
   }
+  // multinomial contraction on DMMA (k_loglik_mnl_mma): classes as n-tiles, 64 particles per block
+  // (C - 1 <= 3) / 32 (C - 1 <= 7); SPS_MNL_DFMA: the DFMA kernel below (A/B)
+  static const bool mnl_dfma = getenv("SPS_MNL_DFMA") != nullptr;
+  if (cm1 >= 2 && cm1 <= 3 && k <= 16 && !mnl_dfma) {
+    // C - 1 = 3 with 2 remainder covariates: k padded to the next multiple of 4 (DMMA) -- the
+    // remainder's 2 x 2 x 3 x 2 theta registers would push the kernel past 128 registers (spills)
+    static const char* var = getenv("SPS_MNL_VAR");  // A/B: "rem" (keep the remainder DFMAs), "ntw1"
+    const bool keep_rem = var && !strcmp(var, "rem"), ntw1 = var && !strcmp(var, "ntw1");
+#define MNL_CASE(K_, KKD_, REM_)                                                                              \
+  case K_:                                                                                                    \
+    if (cm1 == 2)                                                                                             \
+      *o = LLChoice{k_loglik_mnl_mma<KKD_, REM_, 2>, 4 * KKD_ + (REM_ ? 4 : 0), 1, 64, true, 256};             \
+    else if (ntw1)                                                                                            \
+      *o = LLChoice{k_loglik_mnl_mma<KKD_, REM_, 3, 1>, 4 * KKD_ + (REM_ ? 4 : 0), 1, 32, true, 256};          \
+    else if (REM_ == 2 && !keep_rem)                                                                          \
+      *o = LLChoice{k_loglik_mnl_mma<KKD_ + 1, 0, 3>, 4 * KKD_ + 4, 1, 64, true, 256};                          \
+    else                                                                                                      \
+      *o = LLChoice{k_loglik_mnl_mma<KKD_, REM_, 3>, 4 * KKD_ + (REM_ ? 4 : 0), 1, 64, true, 256};             \
+    return true;
+    switch (k) {
+      MNL_CASE(1, 0, 1) MNL_CASE(2, 0, 2) MNL_CASE(3, 1, 0) MNL_CASE(4, 1, 0) MNL_CASE(5, 1, 1) MNL_CASE(6, 1, 2)
+      MNL_CASE(7, 2, 0) MNL_CASE(8, 2, 0) MNL_CASE(9, 2, 1) MNL_CASE(10, 2, 2) MNL_CASE(11, 3, 0) MNL_CASE(12, 3, 0)
+      MNL_CASE(13, 3, 1) MNL_CASE(14, 3, 2) MNL_CASE(15, 4, 0) MNL_CASE(16, 4, 0)
+      default: break;
+    }
+#undef MNL_CASE
+  }
+  if (cm1 >= 4 && cm1 <= 7 && k <= 8 && !mnl_dfma) {
+    const bool k4 = k <= 4;
+    switch (cm1) {
+#define MNL_W(C_)                                                                                          \
+  case C_:                                                                                                 \
+    *o = k4 ? LLChoice{k_loglik_mnl_mma<1, 0, C_, 1>, 4, 1, 32, true, 256}                                  \
+            : LLChoice{k_loglik_mnl_mma<2, 0, C_, 1>, 8, 1, 32, true, 256};                                 \
+    return true;
+      MNL_W(4) MNL_W(5) MNL_W(6) MNL_W(7)
+#undef MNL_W
+      default: break;
+    }
+  }
   if (cm1 == 2) {
     if (k <= 12) return pick_exact<2, 2>(k, o, std::make_integer_sequence<int, 12>{});
     if (k <= 16) return pick_exact<2, 1>(k, o, std::make_integer_sequence<int, 16>{});
@@ -579,6 +625,61 @@ sps_status get_plan(sps_ctx* c, int64_t P, int range, int max_chunks, sps_ctx::P
   return SPS_OK;
 }
 
+// K1 on the INT8 tensor cores (ozaki.cuh): slice this launch's theta into particle tile images,
+// then one CTA (1 per SM: ~200 KB shared memory, 512 TMEM columns) per (128-particle tile,
+// observation chunk); S chosen to fill whole waves of SMs.
+template <int KB>
+sps_status launch_oz(sps_ctx* c, const double* theta, int64_t ldt, int64_t P, int t0, int t1, double* part,
+                     int max_chunks, int* nchunks_out, const int* stop) {
+  const int range = t1 - t0;
+  const int64_t tiles = (P + OZ_MT - 1) / OZ_MT;
+  const size_t need = (size_t)tiles * oz_tile_bytes(OZ_MT, KB);
+  if (need > c->oz_T_cap) {
+    if (c->oz_T) cudaFreeAsync(c->oz_T, c->stream);
+    c->oz_T = nullptr;
+    c->oz_T_cap = 0;
+    TRY(dalloc(c, &c->oz_T, need));
+    c->oz_T_cap = need;
+  }
+  PROF_BEGIN(c);
+  k_oz_slice<<<(unsigned)((tiles * OZ_MT + 127) / 128), 128, 0, c->stream>>>(theta, P, ldt, c->k, KB, OZ_MT, 0,
+                                                                               c->oz_T, stop);
+  CHECK_LAUNCH(c);
+  PROF_END(c, CAT_OTHER);
+  const int nsm = num_sms();
+  int best = 1;
+  double best_cost = 1e300;
+  for (int S = 1; S <= std::max(1, std::min(max_chunks, range / OZ_NT)); ++S) {
+    const int chunk = (range + S - 1) / S;
+    const double cost = std::ceil((double)tiles * S / nsm) * ((chunk + OZ_NT - 1) / OZ_NT + 2.0);
+    if (cost < best_cost * 0.995) {
+      best_cost = cost;
+      best = S;
+    }
+  }
+  const int chunk = ((range + best - 1) / best + OZ_NT - 1) / OZ_NT * OZ_NT;
+  const int S = (range + chunk - 1) / chunk;
+  OzArgs a{c->oz_T, c->oz_X, part, P, t0, t1, chunk, stop};
+  PROF_BEGIN(c);
+  CU(c, launch_pdl(k_oz_loglik<KB>, dim3((unsigned)tiles, (unsigned)S), dim3(192), (size_t)oz_smem_bytes<KB>(), c->stream,
+                   a));
+  CHECK_LAUNCH(c);
+  c->k1_launches += 1;
+  c->k1_pairs += (double)P * range;
+  PROF_END(c, CAT_K1);
+  *nchunks_out = S;
+  return SPS_OK;
+}
+
+sps_status launch_loglik_oz(sps_ctx* c, const double* theta, int64_t ldt, int64_t P, int t0, int t1, double* part,
+                            int max_chunks, int* nchunks_out, const int* stop) {
+  switch (c->oz_KB) {
+    case 2: return launch_oz<2>(c, theta, ldt, P, t0, t1, part, max_chunks, nchunks_out, stop);
+    case 3: return launch_oz<3>(c, theta, ldt, P, t0, t1, part, max_chunks, nchunks_out, stop);
+    default: return launch_oz<4>(c, theta, ldt, P, t0, t1, part, max_chunks, nchunks_out, stop);
+  }
+}
+
 // Launch K1 over [t0, t1) for P particles: partial sums per observation chunk
 // into `part` ([nchunks][P]); returns nchunks.  The chunk count S is chosen so
 // the grid (tiles x S) fills whole waves of SMs x resident blocks (occupancy
@@ -593,6 +694,7 @@ sps_status launch_loglik(sps_ctx* c, const double* theta, int64_t ldt, int64_t P
     *nchunks_out = 1;
     return SPS_OK;
   }
+  if (c->oz_KB > 0) return launch_loglik_oz(c, theta, ldt, P, t0, t1, part, max_chunks, nchunks_out, stop);
   const int ppb = ch.ppb > 0 ? ch.ppb : LL_THREADS * ch.PPT;
   const int64_t tiles = (P + ppb - 1) / ppb;
   sps_ctx::Plan* pl = nullptr;
@@ -1018,7 +1120,7 @@ void free_ctx(sps_ctx* c) {
                   c->shift, c->Lprop, c->V, c->rne, c->lwbuf, c->essparts, c->essslice, c->essgath, c->lse, c->logpl, c->grp_ms,
                   c->grp_ms_gath, c->Lj, c->Lj_gath, c->scal, c->pw_parts, c->pw_slice, c->pw_gath, c->mx_parts,
                   c->mx_slice, c->mx_gath, c->fn_A, c->fn_out, c->ll_scratch, c->Sinv, c->LpriorP, c->SinvP, c->Rp, c->RpP, c->bpart, c->ctl, c->inc_dev,
-                  c->sig_rec, c->sig_in, c->fu_tick, c->fu_tpart};
+                  c->sig_rec, c->sig_in, c->fu_tick, c->fu_tpart, c->oz_X, c->oz_T};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, fs);
   lap("cudaFree");
@@ -1136,6 +1238,10 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
   c->KT = ch.KT;
   c->PPT = ch.PPT;
   c->llc = ch;
+  {  // binary 64 <= k <= 128: K1 on the INT8 tensor cores (ozaki.cuh); SPS_NO_OZAKI: the DMMA kernel
+    static const bool no_oz = getenv("SPS_NO_OZAKI") != nullptr;
+    if (!no_oz && c->C == 2 && c->k >= 64 && c->k <= 128) c->oz_KB = (c->k + 31) / 32;
+  }
   {
     cudaFuncAttributes fa{};
     CU(c, cudaFuncGetAttributes(&fa, ch.fn));
@@ -1352,6 +1458,16 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
                                                                      c->ctl);
     CHECK_LAUNCH(c);
     CU(c, cudaMemsetAsync(c->Xs + tot, 0, 2 * sizeof(double), c->stream));
+    if (c->oz_KB > 0) {  // observation tile images of the sign-flipped X (ozaki.cuh)
+      const int64_t ot = (c->n + OZ_NT - 1) / OZ_NT;
+      TRY(dalloc(c, &c->oz_X, (size_t)ot * oz_tile_bytes(OZ_NT, c->oz_KB)));
+      k_oz_slice<<<(unsigned)((ot * OZ_NT + 127) / 128), 128, 0, c->stream>>>(c->Xs, c->n, c->ldx, c->k, c->oz_KB, OZ_NT,
+                                                                                0, c->oz_X, nullptr);
+      CHECK_LAUNCH(c);
+      const int ob = c->oz_KB == 2 ? oz_smem_bytes<2>() : c->oz_KB == 3 ? oz_smem_bytes<3>() : oz_smem_bytes<4>();
+      auto fn = c->oz_KB == 2 ? k_oz_loglik<2> : c->oz_KB == 3 ? k_oz_loglik<3> : k_oz_loglik<4>;
+      CU(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, ob));
+    }
     k_colmeans<<<(c->k + 127) / 128, 128, 0, c->stream>>>(c->X, c->n, c->k, c->xbar);
     CHECK_LAUNCH(c);
     if (cfg.n_monitors <= 0) {

@@ -1,0 +1,83 @@
+"""K1 on the INT8 tensor cores (ozaki.cuh): binary model, 64 <= k <= 128, the
+contraction x~_t' theta_p rebuilt from 7 x 7 int8 slices (levels a + b <= 6) accumulated in TMEM by
+tcgen05.mma.kind::i8.  Bar: the north_star's 1e-10 relative per-particle log-likelihood against the
+oracle ("evaluate to machine accuracy"), on ragged particle and observation tiles,
+single-observation and empty ranges, chunk starts that are not tile aligned, wide dynamic ranges of
+X and theta, and the extreme |eta| paths of the epilogue."""
+import math
+
+import numpy as np
+import pytest
+
+import sps_synth
+
+pytestmark = pytest.mark.gpu
+LL_RTOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def sps():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_1304_4333_b200 as pkg
+
+    pkg.build()
+    return pkg
+
+
+def _case(sps, orc, X, y, theta, t0, t1):
+    import torch
+
+    n, k = X.shape
+    s = sps.Sps(X, y, np.zeros(k), np.eye(k), J=2, N=4, seed=1)
+    got = s.loglik_tensor(torch.tensor(theta, device="cuda"), t0, t1).cpu().numpy()
+    s.close()
+    want = orc.loglik_range(theta, X, y, 2, t0, t1)
+    err = np.abs(got - want)
+    assert np.all(err <= LL_RTOL * np.abs(want) + 1e-300), (err / np.maximum(np.abs(want), 1e-300)).max()
+    return got
+
+
+@pytest.mark.parametrize("k", [64, 65, 80, 100, 120])
+def test_ozaki_loglik_shapes(sps, orc, k):
+    rng = np.random.default_rng(900 + k)
+    n = 333  # 11 observation tiles of 32, ragged
+    X = np.column_stack([np.ones(n), rng.normal(size=(n, 30)), (rng.uniform(size=(n, k - 31)) < 0.3)])
+    y = rng.integers(0, 2, n).astype(np.int32)
+    P = 1000 + 37  # ragged particle tiles of 128
+    theta = rng.normal(0, 0.15, (P, k))
+    _case(sps, orc, X, y, theta, 0, n)
+    _case(sps, orc, X, y, theta, 17, 301)   # chunk bounds inside observation tiles
+    _case(sps, orc, X, y, theta[:5], 40, 41)  # one observation
+    got = _case(sps, orc, X, y, theta[:200], 100, 100)  # empty range
+    assert np.all(got == 0.0)
+
+
+def test_ozaki_dynamic_range_and_extremes(sps, orc):
+    rng = np.random.default_rng(11)
+    n, k = 257, 100
+    X = np.column_stack([np.ones(n), rng.normal(size=(n, k - 1)) * np.exp(rng.uniform(-6, 6, k - 1))])
+    y = rng.integers(0, 2, n).astype(np.int32)
+    theta = np.concatenate([rng.normal(0, 1e-3, (128, k)) * np.exp(rng.uniform(-4, 4, k)),
+                            rng.normal(0, 5.0, (64, k)),       # |eta| >> 708: clamp path
+                            np.zeros((8, k))])                 # theta = 0 -> -n log 2
+    got = _case(sps, orc, X, y, theta, 0, n)
+    assert np.allclose(got[-8:], -n * math.log(2), rtol=1e-14)
+
+
+def test_ozaki_cfg4_shard_full_data(sps, orc):
+    """configs[3] shape: n = 1e5, k = 100, one GPU's shard of 128 x 1024 particles; full-data L_p on
+    64 sampled particles against the oracle."""
+    import torch
+
+    X, y = sps_synth.config_data("cfg4")
+    P = 131072
+    theta = sps_synth.particles(P, 100, scale=0.05, seed=4)
+    s = sps.Sps(X, y, np.zeros(100), np.eye(100), J=2, N=4, seed=1)
+    got = s.loglik_tensor(torch.tensor(theta, device="cuda")).cpu().numpy()
+    s.close()
+    idx = np.random.default_rng(3).choice(P, 64, replace=False)
+    want = orc.loglik_range(theta[idx], X, y, 2)
+    assert np.all(np.abs(got[idx] - want) <= LL_RTOL * np.abs(want))
