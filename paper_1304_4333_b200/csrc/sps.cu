@@ -497,8 +497,11 @@ bool choose_ll(int k, int C, LLChoice* o) {
   if (cm1 >= 2 && cm1 <= 3 && k <= 16 && !mnl_dfma) {
     // C - 1 = 3 with 2 remainder covariates: k padded to the next multiple of 4 (DMMA) -- the
     // remainder's 2 x 2 x 3 x 2 theta registers would push the kernel past 128 registers (spills)
-    static const char* var = getenv("SPS_MNL_VAR");  // A/B: "rem" (keep the remainder DFMAs), "ntw1"
-    const bool keep_rem = var && !strcmp(var, "rem"), ntw1 = var && !strcmp(var, "ntw1");
+    // C - 1 = 3: one n-tile group (8 particles) per warp, 32 per block -- measured fastest on configs[2]
+    // (full-data K1 3.16 ms vs 3.32 ms padded 2-group, 3.40 ms with remainder DFMAs, 3.45 ms DFMA kernel;
+    // tools/k1_mnl_ab.py); SPS_MNL_VAR = "pad" / "rem": the 64-particle variants (A/B)
+    static const char* var = getenv("SPS_MNL_VAR");
+    const bool keep_rem = var && !strcmp(var, "rem"), ntw1 = !var || !strcmp(var, "ntw1");
 #define MNL_CASE(K_, KKD_, REM_)                                                                              \
   case K_:                                                                                                    \
     if (cm1 == 2)                                                                                             \
@@ -642,7 +645,7 @@ sps_status launch_oz(sps_ctx* c, const double* theta, int64_t ldt, int64_t P, in
     c->oz_T_cap = need;
   }
   PROF_BEGIN(c);
-  k_oz_slice<<<(unsigned)((tiles * OZ_MT + 127) / 128), 128, 0, c->stream>>>(theta, P, ldt, c->k, KB, OZ_MT, 0,
+  k_oz_slice<<<(unsigned)((tiles * OZ_MT + 127) / 128), 128, 0, c->stream>>>(theta, P, ldt, c->k, KB, OZ_MT, 0, 0,
                                                                                c->oz_T, stop);
   CHECK_LAUNCH(c);
   PROF_END(c, CAT_OTHER);
@@ -660,9 +663,11 @@ sps_status launch_oz(sps_ctx* c, const double* theta, int64_t ldt, int64_t P, in
   const int chunk = ((range + best - 1) / best + OZ_NT - 1) / OZ_NT * OZ_NT;
   const int S = (range + chunk - 1) / chunk;
   OzArgs a{c->oz_T, c->oz_X, part, P, t0, t1, chunk, stop};
+  static const int dbg = getenv("SPS_OZ_DBG") ? atoi(getenv("SPS_OZ_DBG")) : 0;  // timing experiments only
+  auto fn = dbg == 1 ? k_oz_loglik<KB, 1> : dbg == 2 ? k_oz_loglik<KB, 2> : k_oz_loglik<KB>;
+  if (dbg) CU(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, oz_smem_bytes<KB>()));
   PROF_BEGIN(c);
-  CU(c, launch_pdl(k_oz_loglik<KB>, dim3((unsigned)tiles, (unsigned)S), dim3(192), (size_t)oz_smem_bytes<KB>(), c->stream,
-                   a));
+  CU(c, launch_pdl(fn, dim3((unsigned)tiles, (unsigned)S), dim3(OZ_THREADS), (size_t)oz_smem_bytes<KB>(), c->stream, a));
   CHECK_LAUNCH(c);
   c->k1_launches += 1;
   c->k1_pairs += (double)P * range;
@@ -1462,7 +1467,7 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
       const int64_t ot = (c->n + OZ_NT - 1) / OZ_NT;
       TRY(dalloc(c, &c->oz_X, (size_t)ot * oz_tile_bytes(OZ_NT, c->oz_KB)));
       k_oz_slice<<<(unsigned)((ot * OZ_NT + 127) / 128), 128, 0, c->stream>>>(c->Xs, c->n, c->ldx, c->k, c->oz_KB, OZ_NT,
-                                                                                0, c->oz_X, nullptr);
+                                                                                1, 0, c->oz_X, nullptr);
       CHECK_LAUNCH(c);
       const int ob = c->oz_KB == 2 ? oz_smem_bytes<2>() : c->oz_KB == 3 ? oz_smem_bytes<3>() : oz_smem_bytes<4>();
       auto fn = c->oz_KB == 2 ? k_oz_loglik<2> : c->oz_KB == 3 ? k_oz_loglik<3> : k_oz_loglik<4>;
