@@ -637,6 +637,8 @@ sps_status launch_oz(sps_ctx* c, const double* theta, int64_t ldt, int64_t P, in
   const int range = t1 - t0;
   const int64_t tiles = (P + OZ_MT - 1) / OZ_MT;
   const size_t need = (size_t)tiles * oz_tile_bytes(OZ_MT, KB);
+  if (need > c->oz_T_cap && c->capturing)  // (sized for P_local at create: no allocation inside a graph)
+    return fail(c, SPS_E_STATE, "ozaki: particle images not allocated before graph capture");
   if (need > c->oz_T_cap) {
     if (c->oz_T) cudaFreeAsync(c->oz_T, c->stream);
     c->oz_T = nullptr;
@@ -1472,6 +1474,9 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
       const int ob = c->oz_KB == 2 ? oz_smem_bytes<2>() : c->oz_KB == 3 ? oz_smem_bytes<3>() : oz_smem_bytes<4>();
       auto fn = c->oz_KB == 2 ? k_oz_loglik<2> : c->oz_KB == 3 ? k_oz_loglik<3> : k_oz_loglik<4>;
       CU(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, ob));
+      // particle images for this rank's P_local (the M steps' launches, captured into graphs)
+      c->oz_T_cap = (size_t)((c->Pl + OZ_MT - 1) / OZ_MT) * oz_tile_bytes(OZ_MT, c->oz_KB);
+      TRY(dalloc(c, &c->oz_T, c->oz_T_cap));
     }
     k_colmeans<<<(c->k + 127) / 128, 128, 0, c->stream>>>(c->X, c->n, c->k, c->xbar);
     CHECK_LAUNCH(c);

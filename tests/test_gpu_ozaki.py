@@ -81,3 +81,40 @@ def test_ozaki_cfg4_shard_full_data(sps, orc):
     idx = np.random.default_rng(3).choice(P, 64, replace=False)
     want = orc.loglik_range(theta[idx], X, y, 2)
     assert np.all(np.abs(got[idx] - want) <= LL_RTOL * np.abs(want))
+
+
+_RUN = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, {root!r})
+import paper_1304_4333_b200 as sps, sps_synth
+X, y = sps_synth.make_data(200, 100, 2, 30, (0.0,), 0.15, seed=5)
+s = sps.Sps(X, y, np.zeros(100), sps.g_prior(X, 2, 0.25), J=8, N=128, seed=2)
+r = s.run()
+s.close()
+print("RESULT" + json.dumps(dict(L=r["L"], R=[int(v) for v in r["R_cycle"]], logml=r["logml"], mean=list(r["mean"]))))
+"""
+
+
+def test_ozaki_whole_run_engine_modes():
+    """A d = 100 run (K1 on the INT8 tensor cores inside the M-step graphs: the particle images are
+    allocated at create, never inside a capture) gives the same result bit for bit under the device
+    loop, per-step graph replays and plain launches, and the FP64 DMMA kernel's schedule and log ML."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for tag, env in (("loop", {}), ("noloop", {"SPS_NO_LOOP": "1"}), ("nograph", {"SPS_NO_GRAPH": "1"}),
+                     ("dmma", {"SPS_NO_OZAKI": "1"})):
+        e = dict(os.environ)
+        e.update(env)
+        p = subprocess.run([sys.executable, "-c", _RUN.format(root=root)], env=e, capture_output=True, text=True,
+                           timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        out[tag] = json.loads([ln for ln in p.stdout.splitlines() if ln.startswith("RESULT")][-1][6:])
+    assert out["loop"] == out["noloop"] == out["nograph"]
+    assert out["dmma"]["L"] == out["loop"]["L"] and out["dmma"]["R"] == out["loop"]["R"]
+    assert abs(out["dmma"]["logml"] - out["loop"]["logml"]) <= 1e-9
