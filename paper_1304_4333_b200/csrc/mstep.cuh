@@ -201,10 +201,16 @@ template <int KK, int TILE>  // TILE particles per tile = TILE / 8 warps of 8 ro
 __global__ void __launch_bounds__(4 * TILE, TILE == 32 ? 5 : 3) k_propose_rb(DrawArgs a) {
   constexpr int KP = 4 * KK, NT = (KP + 7) / 8, NP = 8 * NT;
   extern __shared__ __align__(16) double sm[];
-  // with a static Z buffer (a.Zalt null) the first tile's loads are issued before the stop flag
-  // and the step counter are read (two dependent global loads off the critical path)
+  // Launched with programmatic dependent launch after the previous step's reduce + finalize, which
+  // triggers once the accept kernel is complete: theta (base rows) and Z (side stream, a full graph
+  // edge) may be loaded before griddep_wait; Lz, Rp, the stop flag and the step counter (written by
+  // the finalize) only after it.  With a static Z buffer (a.Zalt null) the first tile's Z / theta
+  // loads are issued before that wait.
   const bool early = a.Zalt == nullptr;
-  if (!early && a.stop && *a.stop) return;
+  if (!early) {
+    griddep_wait();
+    if (a.stop && *a.stop) return;
+  }
   const double* Zsrc = a.Z;
   if (a.Zalt && ((a.step0 + (uint32_t)a.ctl->steps_done) & 1u)) Zsrc = a.Zalt;
   const int d = a.d, BS = round_up(TILE * d, 2);
@@ -214,37 +220,41 @@ __global__ void __launch_bounds__(4 * TILE, TILE == 32 ? 5 : 3) k_propose_rb(Dra
   double* smu = Bs0 + 2 * BS;           // KP
   double* sL = smu + KP;                // NP x KP
   double* sS = sL + NP * KP;            // NP x KP (Rp)
-  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ __align__(8) uint64_t bar[2], barL;
   const int64_t ntl = (a.P + TILE - 1) / TILE;
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
+    mbar_init(&barL, 1);
   }
   for (int i = threadIdx.x; i < KP; i += blockDim.x) smu[i] = i < d ? a.mu[i] : 0.0;
   __syncthreads();
-  // thread 0: TMA loads of `tile` into buffer `buf` (+ Lz, Sinv with the first)
-  auto issue = [&](int64_t tile, int buf, bool first) {
+  // thread 0: TMA loads of `tile` into buffer `buf`
+  auto issue = [&](int64_t tile, int buf) {
     const int64_t pb = tile * TILE;
     const int cnt = (int)min((int64_t)TILE, a.P - pb);
     const unsigned zb = (unsigned)(TILE * KP * 8);
     const unsigned bb = a.base ? (unsigned)(round_up(cnt * d, 2) * 8) : 0u;
-    const unsigned mb = first ? (unsigned)(NP * KP * 8) : 0u;
-    mbar_arrive_expect_tx(&bar[buf], zb + bb + 2 * mb);
+    mbar_arrive_expect_tx(&bar[buf], zb + bb);
     bulk_g2s(Zs0 + buf * TILE * KP, Zsrc + pb * KP, zb, &bar[buf]);
     if (a.base) bulk_g2s(Bs0 + buf * BS, a.base + pb * d, bb, &bar[buf]);
-    if (mb) {
-      bulk_g2s(sL, a.Lz, mb, &bar[buf]);
-      bulk_g2s(sS, a.Rp, mb, &bar[buf]);
-    }
   };
-  if (threadIdx.x == 0 && (int64_t)blockIdx.x < ntl) issue(blockIdx.x, 0, true);
+  if (threadIdx.x == 0 && (int64_t)blockIdx.x < ntl) issue(blockIdx.x, 0);
+  griddep_wait();  // the previous step's finalize: Lz, the stop flag, the step counter
   if (early && a.stop && *a.stop) {  // speculative step after the stop: drain the loads, exit
     if (threadIdx.x == 0 && (int64_t)blockIdx.x < ntl) mbar_wait(&bar[0], 0u);
     return;
   }
+  if (threadIdx.x == 0) {  // Lz, Rp (padded NP x KP) under their own barrier
+    const unsigned mb = (unsigned)(NP * KP * 8);
+    mbar_arrive_expect_tx(&barL, 2 * mb);
+    bulk_g2s(sL, a.Lz, mb, &barL);
+    bulk_g2s(sS, a.Rp, mb, &barL);
+  }
   if (a.set_step && blockIdx.x == 0 && threadIdx.x == 0) a.ctl->step_cur = a.step0 + (uint32_t)a.ctl->steps_done;
   if (a.set_step) tl_start(0);
   griddep_launch();  // persistent grid (all CTAs resident): K1's CTAs may start their prologue
+  mbar_wait(&barL, 0u);
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < ntl; tile += gridDim.x, ++it) {
     const int buf = it & 1;
@@ -252,7 +262,7 @@ __global__ void __launch_bounds__(4 * TILE, TILE == 32 ? 5 : 3) k_propose_rb(Dra
     const int cnt = (int)min((int64_t)TILE, a.P - pb);
     if (threadIdx.x == 0 && tile + gridDim.x < ntl) {
       bulk_wait_read();  // the bulk store of iteration it-1 has read buffer buf^1
-      issue(tile + gridDim.x, buf ^ 1, false);
+      issue(tile + gridDim.x, buf ^ 1);
     }
     mbar_wait(&bar[buf], (unsigned)(it >> 1) & 1u);
     double* Zs = Zs0 + buf * TILE * KP;
@@ -1227,7 +1237,8 @@ __global__ void __launch_bounds__(256) k_mom_reduce(RedArgs r, Ctl* ctl, double*
   if (f.trace && threadIdx.x == 0) f.trace[8 + blockIdx.x] = gtimer();
   if (stop && *stop) return;
   if (f.mode == 1) tl_start(4);
-  griddep_wait();  // the accept kernel's block partials
+  griddep_wait();    // the accept kernel's block partials
+  griddep_launch();  // the next step's proposal may start its launch and theta / Z loads (accept is done)
   const int d = r.d, Jl = r.Jl, W = r.W, nblk = r.nblk, dd = d * d, nl = d * (d + 1) / 2;
   const int nm = red_nm(d), ng = red_ng(Jl, d), gpb = red_gpb(d);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1350,7 +1361,8 @@ __global__ void __launch_bounds__(256) k_mom_reduce_cl(RedArgs r, Ctl* ctl, cons
   const int rank = (int)cl.block_rank(), ncta = (int)cl.num_blocks();
   if (stop && *stop) return;  // uniform over the cluster
   if (f.mode == 1 && rank == 0) tl_start(4);
-  griddep_wait();  // the accept kernel's block partials
+  griddep_wait();    // the accept kernel's block partials
+  griddep_launch();  // the next step's proposal may start its launch and theta / Z loads (accept is done)
   const int d = r.d, Jl = r.Jl, W = r.W, nblk = r.nblk, nl = d * (d + 1) / 2, nm = (nl + 31) / 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   double* sS0 = cl.map_shared_rank(fin_sm, 0);  // CTA 0's finalize layout: [S (J x d) | M (d x d) | ...]

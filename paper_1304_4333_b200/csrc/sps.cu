@@ -813,12 +813,12 @@ sps_status launch_draw(sps_ctx* c, int slot, const double* base, const double* L
     const int64_t ntlT = (c->Pl + T - 1) / T;
     const unsigned grid = (unsigned)std::min<int64_t>(ntlT, (T == 32 ? 5 : 3) * (int64_t)num_sms());
     const unsigned thr = (unsigned)(4 * T);
-#define PRB(KK_)                                                                      \
-  case KK_:                                                                           \
-    if (T == 32)                                                                      \
-      k_propose_rb<KK_, 32><<<grid, thr, sm, c->stream>>>(a);                         \
-    else                                                                              \
-      k_propose_rb<KK_, 64><<<grid, thr, sm, c->stream>>>(a);                         \
+#define PRB(KK_)                                                                                \
+  case KK_:                                                                                     \
+    if (T == 32)                                                                                \
+      CU(c, launch_pdl(k_propose_rb<KK_, 32>, dim3(grid), dim3(thr), sm, c->stream, a));        \
+    else                                                                                        \
+      CU(c, launch_pdl(k_propose_rb<KK_, 64>, dim3(grid), dim3(thr), sm, c->stream, a));        \
     break;
     switch (KK) {
       PRB(1) PRB(2) PRB(3) PRB(4) PRB(5) PRB(6) PRB(7)
