@@ -65,18 +65,24 @@ __global__ void k_oz_slice(const double* __restrict__ v, int64_t rows, int64_t l
   const bool valid = r < rows;
   const double* src = v + (valid ? drow : 0) * ld;
   double mx = 0.0;
+  bool finite = true;
   if (valid)
-    for (int i = 0; i < k; ++i) mx = fmax(mx, fabs(src[i]));
+    for (int i = 0; i < k; ++i) {
+      mx = fmax(mx, fabs(src[i]));
+      finite = finite && isfinite(src[i]);
+    }
   const int e = mx > 0.0 ? ilogb(mx) + 1 : 0;
   uint8_t* tb = out + tile * (int64_t)oz_tile_bytes(R, KB);
-  reinterpret_cast<double*>(tb)[rr] = ldexp(1.0, e);
+  // a non-finite entry makes the row's scale NaN, so every eta of the row -- and L_p -- is NaN, as in
+  // the FP64 kernels (sps_loglik's non-finite check, the M phase's numerical-failure flag)
+  reinterpret_cast<double*>(tb)[rr] = finite ? ldexp(1.0, e) : __longlong_as_double(0x7ff8000000000000ll);
   const int ngrp = R / 8, nch = 2 * KB;
   double rem[16];
   for (int c = 0; c < nch; ++c) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       const int i = c * 16 + j;
-      rem[j] = (valid && i < k) ? ldexp(src[i], -e) : 0.0;
+      rem[j] = (valid && i < k && finite) ? ldexp(src[i], -e) : 0.0;
     }
 #pragma unroll 1
     for (int a = 0; a < OZ_S; ++a) {

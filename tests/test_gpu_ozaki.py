@@ -118,3 +118,21 @@ def test_ozaki_whole_run_engine_modes():
     assert out["loop"] == out["noloop"] == out["nograph"]
     assert out["dmma"]["L"] == out["loop"]["L"] and out["dmma"]["R"] == out["loop"]["R"]
     assert abs(out["dmma"]["logml"] - out["loop"]["logml"]) <= 1e-9
+
+
+def test_ozaki_nonfinite_theta_reported(sps):
+    """A NaN in theta makes L_p NaN on the INT8 path too (the row scale carries it), so sps_sync reports
+    SPS_E_NUMERIC naming the particle."""
+    import torch
+
+    X, y = sps_synth.config_data("cfg4", n=300)
+    s = sps.Sps(X, y, np.zeros(100), np.eye(100), J=2, N=4, seed=1)
+    th = torch.tensor(sps_synth.particles(500, 100, scale=0.05), device="cuda")
+    th[321, 57] = float("nan")
+    out = torch.empty(500, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    s.loglik(th.data_ptr(), 500, 100, 0, 300, out.data_ptr())
+    with pytest.raises(sps.SpsError) as e:
+        s.sync()
+    assert e.value.status == 4 and "p = 321" in str(e.value) and "t = 0" in str(e.value)
+    s.close()
