@@ -56,7 +56,8 @@ struct DrawArgs {
 // With `sctl` (M steps replayed from a CUDA graph) the step is device-resident:
 // step = sctl->step_cur + 1, written by the proposal kernel of the running step.
 // Zalt / logualt (device-side loop): the outputs of odd steps (Z / logu: even steps).
-__global__ void __launch_bounds__(256) k_normals(int64_t P, int64_t p0, int np, int ldz, uint64_t seed, uint32_t step,
+__global__ void __launch_bounds__(256) k_normals(int64_t P, int64_t p0, int np, uint64_t npmagic, int ldz, uint64_t seed,
+                                                 uint32_t step,
                                                  uint32_t tag, uint32_t pass, double* __restrict__ Z,
                                                  double* __restrict__ logu, const Ctl* sctl, const int* stop,
                                                  double* Zalt, double* logualt) {
@@ -71,8 +72,10 @@ __global__ void __launch_bounds__(256) k_normals(int64_t P, int64_t p0, int np, 
   }
   const int64_t ntask = P * np;
   const int64_t gstride = (int64_t)gridDim.x * blockDim.x, g0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // t / np as the high half of t * npmagic, npmagic = floor(2^64 / np) + 1 (exact for every t < 2^64 / np;
+  // computed on the host): the 64-bit division was a subroutine call per normal pair
   for (int64_t t = g0; t < ntask; t += gstride) {
-    const int64_t p = t / np;
+    const int64_t p = np == 1 ? t : (int64_t)__umul64hi((uint64_t)t, npmagic);
     const int pr = (int)(t - p * np);
     double z0, z1;
     normal_pair(seed, (uint32_t)pr, (uint32_t)(p0 + p), step, tag, pass, &z0, &z1);

@@ -762,7 +762,9 @@ sps_status launch_normals(sps_ctx* c, uint32_t tag, uint32_t step, int slot, boo
     at[0].val.priority = lo;
     lc.attrs = at;
     lc.numAttrs = 1;
-    CU(c, cudaLaunchKernelEx(&lc, k_normals, (int64_t)c->Pl, (int64_t)c->p0, np, round_up(c->d, 4), (uint64_t)c->cfg.seed,
+    const uint64_t npmagic = np > 1 ? ~0ull / (uint64_t)np + 1ull : 0ull;  // floor(2^64 / np) + 1 (np = 1: unused)
+    CU(c, cudaLaunchKernelEx(&lc, k_normals, (int64_t)c->Pl, (int64_t)c->p0, np, npmagic,
+                             round_up(c->d, 4), (uint64_t)c->cfg.seed,
                              step, tag, (uint32_t)c->cfg.pass, c->capturing_loop ? c->Zbuf[0] : c->Zbuf[slot],
                              tag == TAG_PROPOSAL ? (c->capturing_loop ? c->LUbuf[0] : c->LUbuf[slot]) : (double*)nullptr,
                              graph ? (const Ctl*)c->ctl : nullptr, graph ? (const int*)&c->ctl->stop : nullptr,
