@@ -389,33 +389,43 @@ __device__ __forceinline__ void combine3(double& M, double& S1, double& S2, doub
 }
 
 // Combine tiles in order -> this rank's (m, S1, S2) per b.
-// One block of ESS_RANK_THREADS threads, thread b = chunk observation b: the chunk size B of a C-phase
-// round never exceeds ESS_RANK_THREADS (sps_create clamps Bmax to it).
+// One warp per chunk observation b (8 per block): lane l combines tiles l, l + 32, ... in order, then a
+// fixed 5-round shuffle tree (deterministic; was one thread looping over all tiles: ~18 us per chunk
+// in the launch list, a chain of dependent exps).  ESS_RANK_THREADS still caps the chunk size B.
 constexpr int ESS_RANK_THREADS = 256;
-__global__ void k_ess_rank(const double* __restrict__ parts, int ntiles, int B, double* __restrict__ slice) {
-  if (B > (int)blockDim.x) __trap();
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
+__global__ void __launch_bounds__(256) k_ess_rank(const double* __restrict__ parts, int ntiles, int B,
+                                                  double* __restrict__ slice) {
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (b >= B) return;  // (warp-uniform)
   double M = -INFINITY, S1 = 0.0, S2 = 0.0;
-  for (int t = 0; t < ntiles; ++t) {
+  for (int t = lane; t < ntiles; t += 32) {
     const double* o = parts + ((int64_t)b * ntiles + t) * 3;
     combine3(M, S1, S2, o[0], o[1], o[2]);
   }
-  slice[b * 3 + 0] = M;
-  slice[b * 3 + 1] = S1;
-  slice[b * 3 + 2] = S2;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const double m = __shfl_xor_sync(0xffffffffu, M, off);
+    const double s1 = __shfl_xor_sync(0xffffffffu, S1, off);
+    const double s2 = __shfl_xor_sync(0xffffffffu, S2, off);
+    // both partners combine the same pair in the same order (lower lane first): identical results
+    if (lane & off) {
+      double mm = m, a1 = s1, a2 = s2;
+      combine3(mm, a1, a2, M, S1, S2);
+      M = mm;
+      S1 = a1;
+      S2 = a2;
+    } else {
+      combine3(M, S1, S2, m, s1, s2);
+    }
+  }
+  if (lane == 0) {
+    slice[b * 3 + 0] = M;
+    slice[b * 3 + 1] = S1;
+    slice[b * 3 + 2] = S2;
+  }
 }
 
-// K3 (Algorithm 2 step 1; R3, R4): combine ranks in rank order;
-// s* = first s in the chunk with S1^2 < ess_frac P S2, or s == n (ends the cycle);
-// with t_fix >= 0 (fixed schedule) s* = t_fix.  Also the log predictive likelihood of
-// every absorbed observation (R18): lse[s] = log sum_p w_p^(s) =
-// M + log S1, logpl[s-1] = lse[s] - lse[s-1], with lse[t_start] = log P (the weights
-// are all 1 after the last S phase).
-// One warp: lane i takes observation base + i of each 32-observation round (the rank
-// combine, the log and the ESS test in parallel); the first crossing is the lowest
-// set lane of a ballot; lse / logpl are written up to it (same values as a serial
-// loop: the previous observation's lse comes from the neighbour lane).
 __global__ void k_ess_final(const double* __restrict__ gath, int G, int B, int s0, int n, double ess_frac, double P,
                             Ctl* ctl, int t_fix, int t_start, double* __restrict__ lse, double* __restrict__ logpl) {
   if (blockDim.x != 32) __trap();  // one warp: lane = observation of a 32-observation round

@@ -1790,7 +1790,7 @@ sps_status sps_cphase(sps_ctx* c, int32_t t_target, double phi_target, int32_t* 
       k_ess_partials<<<dim3((unsigned)ntiles, (unsigned)Be), 256, 0, c->stream>>>(c->lwbuf, Pl, ESS_TILE,
                                                                                  c->essparts);
       CHECK_LAUNCH(c);
-      k_ess_rank<<<1, ESS_RANK_THREADS, 0, c->stream>>>(c->essparts, ntiles, Be, c->essslice);
+      k_ess_rank<<<(unsigned)((Be + 7) / 8), 256, 0, c->stream>>>(c->essparts, ntiles, Be, c->essslice);
       CHECK_LAUNCH(c);
       TRY(gather(c, c->essslice, c->essgath, (size_t)Be * 3));
       k_ess_final<<<1, 32, 0, c->stream>>>(c->essgath, c->G, Be, s, c->n, c->cfg.ess_frac, P, c->ctl,
