@@ -136,3 +136,20 @@ def test_ozaki_nonfinite_theta_reported(sps):
         s.sync()
     assert e.value.status == 4 and "p = 321" in str(e.value) and "t = 0" in str(e.value)
     s.close()
+
+
+def test_ozaki_run_parity_power_vs_oracle(sps, orc):
+    """A whole Algorithm 2 run with K1 on the INT8 tensor cores (d = 100) under power tempering -- every
+    M step evaluates the full-data likelihood of theta* -- against the oracle (data tempering at d = 100:
+    tests/test_gpu_large.py::test_run_parity_large_d, which takes the same K1 path)."""
+    X, y = sps_synth.make_data(150, 100, 2, 30, (0.0,), 0.15, seed=7)
+    cov = orc.g_prior(X, 2, 0.25)
+    o = orc.run(X, y, 2, 8, 128, seed=3, prior_mean=np.zeros(100), prior_cov=cov, tempering=orc.POWER)
+    s = sps.Sps(X, y, np.zeros(100), cov, J=8, N=128, seed=3, tempering=1)
+    g = s.run()
+    s.close()
+    assert o["status"] == 0 and g["L"] == o["L"]
+    assert np.array_equal(g["R_cycle"], o["R_cycle"])
+    assert np.allclose(g["phi_cycle"], o["phi_cycle"], rtol=0, atol=1e-12)
+    assert abs(g["logml"] - o["logml"]) <= 1e-6
+    assert np.all(np.abs(g["mean"] - o["mean"]) <= 1e-6)
