@@ -11,8 +11,8 @@
 // Product: eta = sigma_t tau_p sum_{a,b} X_a T_b 2^(-12 - 7(a + b)); the int8 GEMMs of one level
 // L = a + b share a TMEM accumulator (|C_L| <= 7 * 128 * 64^2 < 2^22); levels L > LMAX = S - 1 are
 // dropped (their weight <= 2^(-12 - 7 S) k); the epilogue folds adjacent levels in int32
-// (C_l 2^7 + C_{l+1} < 2^29) and those in FP64, V = sum_L C_L 2^(-7L) (one rounding per add),
-// eta = V * sigma_t * tau_p * 2^-12.
+// (C_l 2^7 + C_{l+1} < 2^29) and those exactly in int64 (< 2^62), one rounding to double:
+// eta = (double)(sum_L C_L 2^(7 (6 - L))) * sigma_t * tau_p * 2^-54.
 //
 // Operand images (built by k_oz_slice: one thread per row, 16-byte stores, coalesced) are the UMMA
 // K-major SWIZZLE_NONE canonical layout -- core matrices of 8 rows x 16 bytes, row groups at SBO =
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_oz_loglik(OzArgs a) {
     const int pl = 32 * q + lane;  // particle of the tile = TMEM lane
     const int64_t p = (int64_t)tile * OZ_MT + pl;
     oz_wait(&a_full, 0u);
-    const double wp = reinterpret_cast<const double*>(sA)[pl] * 0x1p-12;  // tau_p 2^-12
+    const double wp = reinterpret_cast<const double*>(sA)[pl] * 0x1p-54;  // tau_p 2^-12 2^-42
     __shared__ double sT[64];
     if (warp == 2) {
       sT[lane] = __ldg(c_exp2tab + lane);
@@ -287,24 +287,26 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_oz_loglik(OzArgs a) {
       const int s = i % OZ_STAGES, u = i & 1;
       oz_wait(&tfull[u], (unsigned)(i >> 1) & 1u);
       oz_fence_after();
-      // levels folded in pairs in int32 (|C_L| < 7 * 2^19: C_l 2^7 + C_{l+1} < 2^29), then in FP64:
-      // V = C_0 + 2^-14 (C_1 2^7 + C_2) + 2^-28 (C_3 2^7 + C_4) + 2^-42 (C_5 2^7 + C_6) = sum_L C_L 2^-7L
+      // levels folded in pairs in int32 (|C_L| < 7 * 2^19: C_l 2^7 + C_{l+1} < 2^29), the pairs in int64 on
+      // the ALU (A 2^42 + B 2^28 + C 2^14 + D < 2^62), one conversion: V 2^42 = sum_L C_L 2^(7 (6 - L))
+      // (the FP64 pipe is shared with the INT8 MMAs: fold work stays off it)
       const uint32_t tb = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(u * OZ_S * OZ_NT + 16 * h);
       double V[16];
       {
         int32_t c0v[16], c1v[16], c2v[16];
+        long long acc[16];
         oz_tmem_ld16_wait(tb, c0v);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) V[j] = (double)c0v[j];
+        for (int j = 0; j < 16; ++j) acc[j] = (long long)c0v[j];
         oz_tmem_ld16x2_wait(tb + 1 * OZ_NT, tb + 2 * OZ_NT, c1v, c2v);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) V[j] = fma((double)(c1v[j] * 128 + c2v[j]), 0x1p-14, V[j]);
+        for (int j = 0; j < 16; ++j) acc[j] = acc[j] * 16384 + (long long)(c1v[j] * 128 + c2v[j]);
         oz_tmem_ld16x2_wait(tb + 3 * OZ_NT, tb + 4 * OZ_NT, c1v, c2v);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) V[j] = fma((double)(c1v[j] * 128 + c2v[j]), 0x1p-28, V[j]);
+        for (int j = 0; j < 16; ++j) acc[j] = acc[j] * 16384 + (long long)(c1v[j] * 128 + c2v[j]);
         oz_tmem_ld16x2_wait(tb + 5 * OZ_NT, tb + 6 * OZ_NT, c1v, c2v);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) V[j] = fma((double)(c1v[j] * 128 + c2v[j]), 0x1p-42, V[j]);
+        for (int j = 0; j < 16; ++j) V[j] = (double)(acc[j] * 16384 + (long long)(c1v[j] * 128 + c2v[j]));
       }
       oz_fence_before();
       __syncwarp();
