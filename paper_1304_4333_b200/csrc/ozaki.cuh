@@ -53,8 +53,10 @@ __host__ __device__ constexpr int oz_tile_bytes(int rows, int KB) { return rows 
 // inter = 0 (particle tiles, the A operand): [slice][chunk][row group]; inter = 1 (observation tiles,
 // the B operand): [chunk][slice][row group], so that for one K chunk the row groups of slices
 // 0 .. m-1 are consecutive (SBO apart) and ONE MMA with N = 32 m covers all of them.
+// amax (may be null, X only): per K block, the highest slice index with a nonzero entry in any row
+// (atomicMax; zero-initialised by the caller) -- 0/1 covariate columns are exact in slice 0.
 __global__ void k_oz_slice(const double* __restrict__ v, int64_t rows, int64_t ld, int k, int KB, int R, int inter,
-                           int64_t row0, uint8_t* __restrict__ out, const int* stop) {
+                           int64_t row0, uint8_t* __restrict__ out, const int* stop, int* amax = nullptr) {
   if (stop && *stop) return;  // speculative M step after the stop
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // image row (row0 + r is the data row)
   const int64_t ntile = (rows + R - 1) / R;
@@ -84,6 +86,7 @@ __global__ void k_oz_slice(const double* __restrict__ v, int64_t rows, int64_t l
       const int i = c * 16 + j;
       rem[j] = (valid && i < k && finite) ? ldexp(src[i], -e) : 0.0;
     }
+    int anz = 0;  // highest slice of this chunk with a nonzero entry
 #pragma unroll 1
     for (int a = 0; a < OZ_S; ++a) {
       uint32_t w[4] = {0u, 0u, 0u, 0u};
@@ -94,11 +97,13 @@ __global__ void k_oz_slice(const double* __restrict__ v, int64_t rows, int64_t l
         rem[j] = s - q;
         w[j >> 2] |= (uint32_t)(uint8_t)(int8_t)(int)q << (8 * (j & 3));
       }
+      if (w[0] | w[1] | w[2] | w[3]) anz = a;
       const int64_t grp = inter ? ((int64_t)c * OZ_S + a) * ngrp + rr / 8
                                 : (int64_t)a * nch * ngrp + (int64_t)c * ngrp + rr / 8;
       uint8_t* dst = tb + R * 8 + grp * 128 + (rr % 8) * 16;
       *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
     }
+    if (amax && anz > 0) atomicMax(&amax[c >> 1], anz);
   }
 }
 
@@ -182,6 +187,7 @@ __device__ __forceinline__ void oz_wait(uint64_t* bar, unsigned phase) {
 struct OzArgs {
   const uint8_t* Ti;   // particle tile images (this launch's theta)
   const uint8_t* Xi;   // observation tile images (X, static)
+  const int* xamax;    // [KB] highest nonzero X slice per K block (k_oz_slice); K block 0 always takes all
   double* part;        // [S][P] chunk partials
   int64_t P;
   int32_t t0, t1, chunk;
@@ -204,6 +210,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_oz_loglik(OzArgs a) {
   uint8_t* sB = ozs + TA;
   __shared__ __align__(8) uint64_t a_full, full[OZ_STAGES], empty[OZ_STAGES], tfull[2], tempty[2];
   __shared__ uint32_t s_tmem;
+  __shared__ int s_amax[8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (a.stop && *a.stop) return;
   griddep_wait();  // theta images of this launch
@@ -212,6 +219,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_oz_loglik(OzArgs a) {
   const int c1 = min(c0 + a.chunk, a.t1);
   const int ob0 = c0 / OZ_NT, ob1 = (c1 + OZ_NT - 1) / OZ_NT;  // observation tiles [ob0, ob1)
   const int nob = c1 > c0 ? ob1 - ob0 : 0;
+  if (threadIdx.x < KB) s_amax[threadIdx.x] = a.xamax ? a.xamax[threadIdx.x] : OZ_S - 1;
   if (threadIdx.x == 0) {
     mbar_init(&a_full, 1);
     for (int s = 0; s < OZ_STAGES; ++s) {
@@ -255,16 +263,20 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_oz_loglik(OzArgs a) {
         const uint32_t dbase = tmem + (uint32_t)(u * OZ_S * OZ_NT);
         // theta slice tb against X slices 0 .. LMAX - tb in ONE MMA (N = 32 (LMAX + 1 - tb)): its D starts
         // at column 32 tb, so X_a T_tb lands in the column block of level a + tb; the first MMA of a tile
-        // (kb = 0, tb = 0) spans all levels and overwrites, every later one accumulates
+        // (kb = 0, tb = 0) spans all levels and overwrites, every later one accumulates.  K blocks whose X
+        // slices above nx - 1 are all zero (0/1 covariates are exact in slice 0) stop there.
 #pragma unroll
-        for (int kb = 0; kb < KB; ++kb)
+        for (int kb = 0; kb < KB; ++kb) {
+          const int nx = kb == 0 ? OZ_S : s_amax[kb] + 1;
 #pragma unroll
           for (int tb = 0; tb <= OZ_LMAX; ++tb) {
+            const int na = min(OZ_LMAX + 1 - tb, nx);
             const uint64_t ad = oz_desc(sA + OZ_MT * 8 + tb * SA + 2 * kb * LBO_A, LBO_A, SBO);
             const uint64_t bd = oz_desc(bb + 2 * kb * LBO_B, LBO_B, SBO);
-            const uint32_t idesc = OZ_IDESC_BASE | ((uint32_t)((OZ_NT * (OZ_LMAX + 1 - tb)) >> 3) << 17);
+            const uint32_t idesc = OZ_IDESC_BASE | ((uint32_t)((OZ_NT * na) >> 3) << 17);
             if (DBG != 2) oz_mma(dbase + (uint32_t)(tb * OZ_NT), ad, bd, idesc, (kb > 0 || tb > 0) ? 1u : 0u);
           }
+        }
         oz_commit(&empty[s]);  // the stage's operands are consumed once these MMAs complete
         oz_commit(&tfull[u]);  // the accumulators of buffer u are ready
       }

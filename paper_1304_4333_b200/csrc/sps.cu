@@ -190,6 +190,7 @@ struct sps_ctx {
   // K1 on INT8 tensor cores (binary, 64 <= k <= 128; ozaki.cuh): K-blocks of 32, operand images
   int oz_KB = 0;
   uint8_t* oz_X = nullptr;  // observation tile images (built once at create)
+  int* oz_xamax = nullptr;  // [KB] highest nonzero X slice per K block
   uint8_t* oz_T = nullptr;  // particle tile images of the theta of the current launch
   size_t oz_T_cap = 0;
   struct Plan {
@@ -664,7 +665,7 @@ sps_status launch_oz(sps_ctx* c, const double* theta, int64_t ldt, int64_t P, in
   }
   const int chunk = ((range + best - 1) / best + OZ_NT - 1) / OZ_NT * OZ_NT;
   const int S = (range + chunk - 1) / chunk;
-  OzArgs a{c->oz_T, c->oz_X, part, P, t0, t1, chunk, stop};
+  OzArgs a{c->oz_T, c->oz_X, c->oz_xamax, part, P, t0, t1, chunk, stop};
   static const int dbg = getenv("SPS_OZ_DBG") ? atoi(getenv("SPS_OZ_DBG")) : 0;  // timing experiments only
   auto fn = dbg == 1 ? k_oz_loglik<KB, 1> : dbg == 2 ? k_oz_loglik<KB, 2> : k_oz_loglik<KB>;
   if (dbg) CU(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, oz_smem_bytes<KB>()));
@@ -1129,7 +1130,7 @@ void free_ctx(sps_ctx* c) {
                   c->shift, c->Lprop, c->V, c->rne, c->lwbuf, c->essparts, c->essslice, c->essgath, c->lse, c->logpl, c->grp_ms,
                   c->grp_ms_gath, c->Lj, c->Lj_gath, c->scal, c->pw_parts, c->pw_slice, c->pw_gath, c->mx_parts,
                   c->mx_slice, c->mx_gath, c->fn_A, c->fn_out, c->ll_scratch, c->Sinv, c->LpriorP, c->SinvP, c->Rp, c->RpP, c->bpart, c->ctl, c->inc_dev,
-                  c->sig_rec, c->sig_in, c->fu_tick, c->fu_tpart, c->oz_X, c->oz_T};
+                  c->sig_rec, c->sig_in, c->fu_tick, c->fu_tpart, c->oz_X, c->oz_T, c->oz_xamax};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, fs);
   lap("cudaFree");
@@ -1470,8 +1471,10 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
     if (c->oz_KB > 0) {  // observation tile images of the sign-flipped X (ozaki.cuh)
       const int64_t ot = (c->n + OZ_NT - 1) / OZ_NT;
       TRY(dalloc(c, &c->oz_X, (size_t)ot * oz_tile_bytes(OZ_NT, c->oz_KB)));
+      TRY(dalloc(c, &c->oz_xamax, 8));
+      CU(c, cudaMemsetAsync(c->oz_xamax, 0, 8 * sizeof(int), c->stream));
       k_oz_slice<<<(unsigned)((ot * OZ_NT + 127) / 128), 128, 0, c->stream>>>(c->Xs, c->n, c->ldx, c->k, c->oz_KB, OZ_NT,
-                                                                                1, 0, c->oz_X, nullptr);
+                                                                                1, 0, c->oz_X, nullptr, c->oz_xamax);
       CHECK_LAUNCH(c);
       const int ob = c->oz_KB == 2 ? oz_smem_bytes<2>() : c->oz_KB == 3 ? oz_smem_bytes<3>() : oz_smem_bytes<4>();
       auto fn = c->oz_KB == 2 ? k_oz_loglik<2> : c->oz_KB == 3 ? k_oz_loglik<3> : k_oz_loglik<4>;
