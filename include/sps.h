@@ -8,7 +8,11 @@
  *    (when there is one) keeps a message readable with sps_last_error().
  *  - Threading: a context is single-owner and not thread-safe.
  *  - Precision: fp64 end to end ("easy to evaluate to
- *    machine accuracy").
+ *    machine accuracy").  For binary models with 64 <= k <= 128 the K1
+ *    contraction runs on the INT8 tensor cores as an exact-to-~1e-16 split
+ *    (7 x 7 int8 slices with power-of-two row scales, int32 accumulation,
+ *    an exact int64 fold); its results agree with the
+ *    FP64 DMMA kernel's to rounding (SPS_NO_OZAKI=1 selects the latter).
  *  - Labels: y[t] in [0, C); label 0 is the paper's reference category C
  *    (theta_C = 0).  theta = [theta_1 .. theta_{C-1}]
  *    stacked in blocks of k, d = k (C-1).
