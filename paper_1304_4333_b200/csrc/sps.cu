@@ -188,7 +188,7 @@ struct sps_ctx {
   unsigned* fu_tick = nullptr;
   double* fu_tpart = nullptr;
   // K1 on INT8 tensor cores (binary, 64 <= k <= 128; ozaki.cuh): K-blocks of 32, operand images
-  int oz_KB = 0;
+  int oz_KB = 0, oz_min_range = 512;
   uint8_t* oz_X = nullptr;  // observation tile images (built once at create)
   int* oz_xamax = nullptr;  // [KB] highest nonzero X slice per K block
   uint8_t* oz_T = nullptr;  // particle tile images of the theta of the current launch
@@ -702,7 +702,8 @@ sps_status launch_loglik(sps_ctx* c, const double* theta, int64_t ldt, int64_t P
     *nchunks_out = 1;
     return SPS_OK;
   }
-  if (c->oz_KB > 0) return launch_loglik_oz(c, theta, ldt, P, t0, t1, part, max_chunks, nchunks_out, stop);
+  if (c->oz_KB > 0 && range >= c->oz_min_range)
+    return launch_loglik_oz(c, theta, ldt, P, t0, t1, part, max_chunks, nchunks_out, stop);
   const int ppb = ch.ppb > 0 ? ch.ppb : LL_THREADS * ch.PPT;
   const int64_t tiles = (P + ppb - 1) / ppb;
   sps_ctx::Plan* pl = nullptr;
@@ -1249,8 +1250,13 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
   c->PPT = ch.PPT;
   c->llc = ch;
   {  // binary 64 <= k <= 128: K1 on the INT8 tensor cores (ozaki.cuh); SPS_NO_OZAKI: the DMMA kernel
-    static const bool no_oz = getenv("SPS_NO_OZAKI") != nullptr;
-    if (!no_oz && c->C == 2 && c->k >= 64 && c->k <= 128) c->oz_KB = (c->k + 31) / 32;
+    // per launch, only for observation ranges >= oz_min_range: below that the FP64 DMMA kernel is faster
+    // (measured crossover ~384-512 observations at P = 65536, k = 56 and 100: the INT8 path pays the
+    // theta slicing and a TMEM / operand-image setup per CTA); SPS_OZ_MINK / SPS_OZ_MINRANGE: A/B, tests
+    const bool no_oz = getenv("SPS_NO_OZAKI") != nullptr;
+    const int oz_mink = getenv("SPS_OZ_MINK") ? std::max(33, atoi(getenv("SPS_OZ_MINK"))) : 33;
+    c->oz_min_range = getenv("SPS_OZ_MINRANGE") ? std::max(1, atoi(getenv("SPS_OZ_MINRANGE"))) : 512;
+    if (!no_oz && c->C == 2 && c->k >= oz_mink && c->k <= 128) c->oz_KB = (c->k + 31) / 32;
   }
   {
     cudaFuncAttributes fa{};

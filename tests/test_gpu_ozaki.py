@@ -27,6 +27,13 @@ def sps():
     return pkg
 
 
+@pytest.fixture(autouse=True)
+def _int8_path_for_every_range(monkeypatch):
+    """The engine takes the INT8 path only for ranges >= 512 observations (below, the FP64 DMMA kernel
+    is faster); these tests exercise it on short ranges too (read at sps_create)."""
+    monkeypatch.setenv("SPS_OZ_MINRANGE", "1")
+
+
 def _case(sps, orc, X, y, theta, t0, t1):
     import torch
 
@@ -151,5 +158,22 @@ def test_ozaki_run_parity_power_vs_oracle(sps, orc):
     assert o["status"] == 0 and g["L"] == o["L"]
     assert np.array_equal(g["R_cycle"], o["R_cycle"])
     assert np.allclose(g["phi_cycle"], o["phi_cycle"], rtol=0, atol=1e-12)
+    assert abs(g["logml"] - o["logml"]) <= 1e-6
+    assert np.all(np.abs(g["mean"] - o["mean"]) <= 1e-6)
+
+
+def test_ozaki_switch_within_run_vs_oracle(sps, orc, monkeypatch):
+    """Default switch (INT8 path for ranges >= 512 observations, FP64 DMMA below) inside one run: k = 40,
+    n = 600, the late cycles' M steps cross 512 -- the schedule, log ML and means match the oracle."""
+    monkeypatch.delenv("SPS_OZ_MINRANGE", raising=False)
+    X, y = sps_synth.make_data(600, 40, 2, 12, (-0.5,), 0.3, seed=21)
+    cov = orc.g_prior(X, 2, 0.25)
+    o = orc.run(X, y, 2, 8, 128, seed=4, prior_mean=np.zeros(40), prior_cov=cov)
+    s = sps.Sps(X, y, np.zeros(40), cov, J=8, N=128, seed=4)
+    g = s.run()
+    s.close()
+    assert o["status"] == 0 and o["t_cycle"][-2] >= 512  # the last cycles run K1 on the INT8 path
+    assert g["L"] == o["L"] and np.array_equal(g["t_cycle"], o["t_cycle"])
+    assert np.array_equal(g["R_cycle"], o["R_cycle"])
     assert abs(g["logml"] - o["logml"]) <= 1e-6
     assert np.all(np.abs(g["mean"] - o["mean"]) <= 1e-6)

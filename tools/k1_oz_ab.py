@@ -21,8 +21,12 @@ import sps_synth  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=100000)
 ap.add_argument("--P", type=int, default=131072)
+ap.add_argument("--k", type=int, default=100, help="covariates (configs[3] recipe with k columns)")
 a = ap.parse_args()
-X, y = sps_synth.config_data("cfg4", n=a.n)
+if a.k == 100:
+    X, y = sps_synth.config_data("cfg4", n=a.n)
+else:  # the configs[3] recipe at another k: ~30% continuous columns, the rest 0/1
+    X, y = sps_synth.make_data(a.n, a.k, 2, max(1, (3 * a.k) // 10), (0.0,), 0.15)
 n, k = X.shape
 ctx = sps.Sps(X, y, np.zeros(k), np.eye(k), J=2, N=4, seed=1)
 th = torch.tensor(sps_synth.particles(a.P, k, scale=0.05, seed=4), device="cuda")
@@ -41,7 +45,7 @@ e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / reps
 pairs = a.P * n / (ms * 1e-3)
-oz = os.environ.get("SPS_NO_OZAKI") is None
+oz = os.environ.get("SPS_NO_OZAKI") is None and k >= int(os.environ.get("SPS_OZ_MINK", "64"))
 KB = (k + 31) // 32
 print(json.dumps({"kernel": "int8 tcgen05 (ozaki)" if oz else "fp64 DMMA", "n": n, "k": k, "P": a.P, "ms": ms,
                   "pairs_per_s": pairs, "fp64_equiv_frac": pairs * (2 * k + 11) / 1e12 / 37.07,
