@@ -16,7 +16,7 @@
 //      tiles per reduce row, the last tile tail of the row sums the TPR tile rows in order.
 // It removes the proposal and accept launches (~9.7 + ~7.7 us per cfg2 step), their dependent-launch
 // gaps and the theta* / lp* round trips through L2 -- and measured SLOWER, so it is opt-in
-// (SPS_FUSED=1): cfg2 run 167.6 vs 149.4 ms.  ncu (full-data step, t = 1000,
+// (SPS_FUSED=1, instantiated for k = 4 and 25): cfg2 run 167.6 vs 149.4 ms.  ncu (full-data step, t = 1000,
 // S = 4 chunk blocks per tile): 172.6 vs 125.7 us for K1 alone; the phase-B latency (theta / Z
 // loads, two dependent DMMA passes) is paid by all S blocks of a tile while each holds one of
 // the SM's 4 register-limited slots, and the tile tails (~8 us of dependent loads, barriers and

@@ -496,23 +496,15 @@ bool choose_ll(int k, int C, LLChoice* o) {
   // (C - 1 <= 3) / 32 (C - 1 <= 7); SPS_MNL_DFMA: the DFMA kernel below (A/B)
   static const bool mnl_dfma = getenv("SPS_MNL_DFMA") != nullptr;
   if (cm1 >= 2 && cm1 <= 3 && k <= 16 && !mnl_dfma) {
-    // C - 1 = 3 with 2 remainder covariates: k padded to the next multiple of 4 (DMMA) -- the
-    // remainder's 2 x 2 x 3 x 2 theta registers would push the kernel past 128 registers (spills)
     // C - 1 = 3: one n-tile group (8 particles) per warp, 32 per block -- measured fastest on configs[2]
-    // (full-data K1 3.16 ms vs 3.32 ms padded 2-group, 3.40 ms with remainder DFMAs, 3.45 ms DFMA kernel;
-    // tools/k1_mnl_ab.py); SPS_MNL_VAR = "pad" / "rem": the 64-particle variants (A/B)
-    static const char* var = getenv("SPS_MNL_VAR");
-    const bool keep_rem = var && !strcmp(var, "rem"), ntw1 = !var || !strcmp(var, "ntw1");
+    // (full-data K1 3.16 ms vs 3.32 ms with two groups and k padded to 12, 3.40 ms with two groups and
+    // remainder DFMAs, 3.45 ms DFMA kernel; tools/k1_mnl_ab.py); C - 1 = 2: two groups
 #define MNL_CASE(K_, KKD_, REM_)                                                                              \
   case K_:                                                                                                    \
     if (cm1 == 2)                                                                                             \
       *o = LLChoice{k_loglik_mnl_mma<KKD_, REM_, 2>, 4 * KKD_ + (REM_ ? 4 : 0), 1, 64, true, 256};             \
-    else if (ntw1)                                                                                            \
-      *o = LLChoice{k_loglik_mnl_mma<KKD_, REM_, 3, 1>, 4 * KKD_ + (REM_ ? 4 : 0), 1, 32, true, 256};          \
-    else if (REM_ == 2 && !keep_rem)                                                                          \
-      *o = LLChoice{k_loglik_mnl_mma<KKD_ + 1, 0, 3>, 4 * KKD_ + 4, 1, 64, true, 256};                          \
     else                                                                                                      \
-      *o = LLChoice{k_loglik_mnl_mma<KKD_, REM_, 3>, 4 * KKD_ + (REM_ ? 4 : 0), 1, 64, true, 256};             \
+      *o = LLChoice{k_loglik_mnl_mma<KKD_, REM_, 3, 1>, 4 * KKD_ + (REM_ ? 4 : 0), 1, 32, true, 256};          \
     return true;
     switch (k) {
       MNL_CASE(1, 0, 1) MNL_CASE(2, 0, 2) MNL_CASE(3, 1, 0) MNL_CASE(4, 1, 0) MNL_CASE(5, 1, 1) MNL_CASE(6, 1, 2)
@@ -886,19 +878,12 @@ sps_status launch_fused(sps_ctx* c, int slot, int t1, double temper, const int* 
   return SPS_OK;
 }
 
-// Fused-kernel instance for k = d <= 32: DMMA k-steps KKD + remainder DFMAs REM (as K1), T'T tiles NT.
+// Fused-kernel instance (opt-in experiment): instantiated for the measured / tested
+// shapes only, k = 4 (configs[0]) and k = 25 (configs[1]); other k run the separate kernels.
 void (*pick_fused(int k))(FusedArgs) {
   switch (k) {
-#define FU_CASE(K_, KKD_, REM_) \
-  case K_:                      \
-    return k_mstep_bin<KKD_, REM_, (K_ + 8) / 8>;
-    FU_CASE(1, 0, 1) FU_CASE(2, 0, 2) FU_CASE(3, 1, 0) FU_CASE(4, 1, 0) FU_CASE(5, 1, 1) FU_CASE(6, 1, 2)
-    FU_CASE(7, 2, 0) FU_CASE(8, 2, 0) FU_CASE(9, 2, 1) FU_CASE(10, 2, 2) FU_CASE(11, 3, 0) FU_CASE(12, 3, 0)
-    FU_CASE(13, 3, 1) FU_CASE(14, 3, 2) FU_CASE(15, 4, 0) FU_CASE(16, 4, 0) FU_CASE(17, 4, 1)
-    FU_CASE(18, 4, 2) FU_CASE(19, 5, 0) FU_CASE(20, 5, 0) FU_CASE(21, 5, 1) FU_CASE(22, 5, 2)
-    FU_CASE(23, 6, 0) FU_CASE(24, 6, 0) FU_CASE(25, 6, 1) FU_CASE(26, 6, 2) FU_CASE(27, 7, 0)
-    FU_CASE(28, 7, 0) FU_CASE(29, 7, 1) FU_CASE(30, 7, 2) FU_CASE(31, 8, 0) FU_CASE(32, 8, 0)
-#undef FU_CASE
+    case 4: return k_mstep_bin<1, 0, 1>;
+    case 25: return k_mstep_bin<6, 1, 4>;
     default: return nullptr;
   }
 }

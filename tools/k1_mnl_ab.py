@@ -2,7 +2,7 @@
 P = 128 x 1024): full-data evaluations timed with CUDA events; pairs/s and the fraction of the
 measured FP64 peak counting the contraction alone (2 k (C-1) flops per pair) and with the epilogue.
 
-    SPS_MNL_VAR=pad|rem|ntw1 / SPS_MNL_DFMA=1 python tools/k1_mnl_ab.py
+    [SPS_MNL_DFMA=1] python tools/k1_mnl_ab.py   (the round-2 variants "pad" / "rem" were removed after this A/B)
 """
 import json
 import os
