@@ -165,3 +165,20 @@ def test_logml_many_cycles_small_increment_buffer(sps, orc, monkeypatch):
     s.close()
     assert o["L"] > 3
     _compare(g, o)
+
+
+def test_reset_rerun_bit_identical_cfg2(sps):
+    """Back-to-back runs on one context (the bench's timed loop): sps_reset(seed) restores every piece of
+    device state a run reads, so the same seed reproduces the run bit for bit after another seed's run
+    (no state carried from the previous run's last M step, cycle or increment buffer)."""
+    X, y = sps_synth.config_data("cfg2")
+    cov = sps.g_prior(X, 2, 1.0 / 16)
+    s = sps.Sps(X, y, np.zeros(25), cov, J=64, N=1024, seed=1)
+    res = []
+    for seed in (5, 6, 5, 5):
+        s.reset(seed)
+        r = s.run()
+        res.append((r["logml"], r["L"], r["total_m_steps"], r["mean"].tobytes()))
+    s.close()
+    assert res[0] == res[2] == res[3]
+    assert res[1] != res[0]
