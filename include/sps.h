@@ -42,7 +42,8 @@ typedef enum {
   SPS_E_MIXING = 5,  /* M phase exceeded max_m_steps (R13)                      */
   SPS_E_CUDA = 6,    /* CUDA runtime error / no device                          */
   SPS_E_NCCL = 7,    /* NCCL error                                              */
-  SPS_E_STATE = 8    /* call out of order (e.g. sps_mphase before any C phase)  */
+  SPS_E_STATE = 8,   /* call out of order (e.g. sps_mphase before any C phase)  */
+  SPS_E_GUARD = 9    /* debug: a device buffer's guard zone was overwritten     */
 } sps_status;
 
 enum { SPS_DATA_TEMPERING = 0, SPS_POWER_TEMPERING = 1 };
@@ -239,6 +240,17 @@ sps_status sps_get_counters(const sps_ctx* ctx, sps_counters* out);
 
 /* Local particle count and first global group of this rank. */
 sps_status sps_shard(const sps_ctx* ctx, int64_t* P_local, int32_t* group0, int32_t* J_local);
+
+/* Debug memory check (the pool this was built on runs no compute-sanitizer).  With the
+ * environment variable SPS_GUARD=1 at sps_create, every device buffer of the context is
+ * allocated between two 256-byte guard zones filled with 0xA5; an out-of-bounds write by any
+ * kernel (or copy) lands in a zone.  sps_check_guards synchronizes the context's streams and
+ * reads every zone back.  *n_corrupt (may be NULL) = overwritten guard bytes.  Returns SPS_OK,
+ * SPS_E_GUARD (the last-error message names the first buffer and the byte offset relative to
+ * its start: negative = before it, >= its size = past its end), or SPS_E_CONFIG if the context
+ * was created without SPS_GUARD=1.  Test hook: SPS_GUARD_POKE=<buffer name, e.g. &c->theta>
+ * writes 8 bytes past that buffer at create. */
+sps_status sps_check_guards(sps_ctx* ctx, int64_t* n_corrupt);
 
 void sps_destroy(sps_ctx* ctx);
 const char* sps_last_error(const sps_ctx* ctx);

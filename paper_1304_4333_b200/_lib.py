@@ -68,7 +68,7 @@ EXPORTED = [
     "sps_moments", "sps_get_particles", "sps_shard", "sps_destroy", "sps_last_error", "sps_nccl_unique_id",
     "sps_g_prior", "sps_test_philox", "sps_test_normals", "sps_test_portable", "sps_test_resample_int",
     "sps_test_resample_group", "sps_test_accept", "sps_reset", "sps_set_profiling", "sps_get_counters", "sps_sync", "sps_loopback_unique_id",
-    "sps_record_sigma", "sps_get_sigma", "sps_set_design", "sps_predictive",
+    "sps_record_sigma", "sps_get_sigma", "sps_set_design", "sps_predictive", "sps_check_guards",
 ]
 
 
@@ -120,6 +120,7 @@ def _declare(L):
         "sps_moments": ([vp, C.c_int32, dp, dp, dp, dp, dp], st),
         "sps_get_particles": ([vp, dp, dp, dp], st),
         "sps_shard": ([vp, C.POINTER(C.c_int64), ip, ip], st),
+        "sps_check_guards": ([vp, C.POINTER(C.c_int64)], st),
         "sps_destroy": ([vp], None),
         "sps_last_error": ([vp], C.c_char_p),
         "sps_nccl_unique_id": ([vp], st),

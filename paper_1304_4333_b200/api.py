@@ -211,6 +211,13 @@ class Sps:
                     syncs=c.syncs, cat_ms={k: c.cat_ms[i] for i, k in enumerate(cats)},
                     cat_n={k: c.cat_n[i] for i, k in enumerate(cats)})
 
+    def check_guards(self):
+        """Debug memory check (context created with SPS_GUARD=1): raises SpsError (status 9) naming the
+        first buffer whose guard zone a kernel overwrote; returns 0."""
+        n = C.c_int64()
+        _check(lib().sps_check_guards(self.ctx, C.byref(n)), self.ctx)
+        return n.value
+
     def logml(self):
         v, nse = C.c_double(), C.c_double()
         _check(lib().sps_logml(self.ctx, C.byref(v), C.byref(nse)), self.ctx)

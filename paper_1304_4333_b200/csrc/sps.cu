@@ -201,6 +201,14 @@ struct sps_ctx {
   int plan_next = 0;
   Ctl* ctl = nullptr;
   Ctl* hctl = nullptr;  // pinned mirror
+  // debug memory check (SPS_GUARD=1 at create): every device buffer between two guard zones
+  struct Guard {
+    char* base;
+    size_t bytes;  // user bytes (the buffer is [base + GUARD_BYTES, base + GUARD_BYTES + bytes))
+    const char* name;
+  };
+  bool guarded = false;
+  std::vector<Guard> guards;
   int slice_len = 0;
   // host state (Algorithm 2)
   int t = 0;            // observations absorbed
@@ -327,12 +335,42 @@ cudaError_t launch_cluster_pdl(void (*kern)(KArgs...), int cl, dim3 block, size_
   return cudaLaunchKernelEx(&lc, kern, args...);
 }
 
+constexpr size_t GUARD_BYTES = 256;   // guard zone before and after each buffer (SPS_GUARD=1)
+constexpr unsigned char GUARD_FILL = 0xA5;
+
 template <typename T>
-sps_status dalloc(sps_ctx* c, T** p, size_t count) {
+sps_status dalloc(sps_ctx* c, T** p, size_t count, const char* name = "?") {
   // stream-ordered allocation from the device's default pool (release threshold raised once per
   // device): a new context reuses memory cached by earlier ones instead of driver allocations
-  CU(c, cudaMallocAsync((void**)p, std::max<size_t>(count, 1) * sizeof(T), c->stream));
+  const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+  if (!c->guarded) {
+    CU(c, cudaMallocAsync((void**)p, bytes, c->stream));
+    return SPS_OK;
+  }
+  // debug: [guard | buffer | guard], both zones filled with GUARD_FILL and verified by
+  // sps_check_guards (an out-of-bounds write by any kernel lands in a zone)
+  char* base = nullptr;
+  CU(c, cudaMallocAsync((void**)&base, bytes + 2 * GUARD_BYTES, c->stream));
+  CU(c, cudaMemsetAsync(base, GUARD_FILL, GUARD_BYTES, c->stream));
+  CU(c, cudaMemsetAsync(base + GUARD_BYTES + bytes, GUARD_FILL, GUARD_BYTES, c->stream));
+  c->guards.push_back(sps_ctx::Guard{base, bytes, name});
+  *p = reinterpret_cast<T*>(base + GUARD_BYTES);
   return SPS_OK;
+}
+#define DALLOC(c, p, n) dalloc(c, p, n, #p)
+
+// Free a dalloc'd buffer (stream-ordered); with guards, the allocation starts GUARD_BYTES earlier.
+void dfree(sps_ctx* c, void* p, cudaStream_t s) {
+  if (!p) return;
+  if (c->guarded) {
+    for (size_t i = 0; i < c->guards.size(); ++i)
+      if (c->guards[i].base + GUARD_BYTES == (char*)p) {
+        cudaFreeAsync(c->guards[i].base, s);
+        c->guards.erase(c->guards.begin() + (std::ptrdiff_t)i);
+        return;
+      }
+  }
+  cudaFreeAsync(p, s);
 }
 
 int num_sms() {
@@ -633,10 +671,10 @@ sps_status launch_oz(sps_ctx* c, const double* theta, int64_t ldt, int64_t P, in
   if (need > c->oz_T_cap && c->capturing)  // (sized for P_local at create: no allocation inside a graph)
     return fail(c, SPS_E_STATE, "ozaki: particle images not allocated before graph capture");
   if (need > c->oz_T_cap) {
-    if (c->oz_T) cudaFreeAsync(c->oz_T, c->stream);
+    dfree(c, c->oz_T, c->stream);
     c->oz_T = nullptr;
     c->oz_T_cap = 0;
-    TRY(dalloc(c, &c->oz_T, need));
+    TRY(DALLOC(c, &c->oz_T, need));
     c->oz_T_cap = need;
   }
   PROF_BEGIN(c);
@@ -1093,10 +1131,8 @@ void free_ctx(sps_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   lap("sync");
   cudaStream_t fs = c->stream ? c->stream : 0;
-  for (double* z : c->Zbuf)
-    if (z) cudaFreeAsync(z, fs);
-  for (double* z : c->LUbuf)
-    if (z) cudaFreeAsync(z, fs);
+  for (double* z : c->Zbuf) dfree(c, z, fs);
+  for (double* z : c->LUbuf) dfree(c, z, fs);
   lap("zbuf");
   for (int q = 0; q < 2; ++q)
     if (c->gexec[q]) cudaGraphExecDestroy(c->gexec[q]);
@@ -1117,17 +1153,16 @@ void free_ctx(sps_ctx* c) {
                   c->grp_ms_gath, c->Lj, c->Lj_gath, c->scal, c->pw_parts, c->pw_slice, c->pw_gath, c->mx_parts,
                   c->mx_slice, c->mx_gath, c->fn_A, c->fn_out, c->ll_scratch, c->Sinv, c->LpriorP, c->SinvP, c->Rp, c->RpP, c->bpart, c->ctl, c->inc_dev,
                   c->sig_rec, c->sig_in, c->fu_tick, c->fu_tpart, c->oz_X, c->oz_T, c->oz_xamax};
-  for (void* p : ptrs)
-    if (p) cudaFreeAsync(p, fs);
+  for (void* p : ptrs) dfree(c, p, fs);
   lap("cudaFree");
   if (c->hctl) cudaFreeHost(c->hctl);
   if (c->hslot) cudaFreeHost(c->hslot);
   if (c->hllbad) cudaFreeHost(c->hllbad);
   if (c->llbad) cudaFree(c->llbad);
   lap("freeHost");
-  if (c->ticket) cudaFreeAsync(c->ticket, fs);
+  dfree(c, c->ticket, fs);
   if (c->trace) cudaFree(c->trace);  // managed
-  if (c->tl) cudaFreeAsync(c->tl, fs);
+  dfree(c, c->tl, fs);
   cudaStreamSynchronize(fs);
   for (cudaEvent_t e : c->evs)
     if (e) cudaEventDestroy(e);
@@ -1206,6 +1241,7 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
   if (validate(cfg_in) != SPS_OK || !X || !y || !prior_mean || !prior_cov) return SPS_E_CONFIG;
   sps_ctx* c = new sps_ctx();
   c->cfg = *cfg_in;
+  c->guarded = getenv("SPS_GUARD") && atoi(getenv("SPS_GUARD")) != 0;  // debug memory check
   c->cfg.monitors = nullptr;
   c->cfg.nccl_id = nullptr;
   *out = c;
@@ -1330,28 +1366,36 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
     if (r != ncclSuccess) return fail(c, SPS_E_NCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(r));
   }
   const int64_t Pl = c->Pl;
-  TRY(dalloc(c, &c->X, (size_t)c->n * c->k));
-  TRY(dalloc(c, &c->Xs, (size_t)c->n * c->ldx + 2));
-  TRY(dalloc(c, &c->y, (size_t)c->n));
-  TRY(dalloc(c, &c->mu, d));
-  TRY(dalloc(c, &c->Lprior, (size_t)d * d));
-  TRY(dalloc(c, &c->xbar, c->k));
-  TRY(dalloc(c, &c->mon, (size_t)c->nmon * d));
-  for (double** p : {&c->theta, &c->theta2, &c->theta_s}) TRY(dalloc(c, p, (size_t)Pl * d + 2 * PR_TILE));
-  for (double** p : {&c->L, &c->L2, &c->lp, &c->lp2, &c->lw, &c->lw_cur, &c->lp_s}) TRY(dalloc(c, p, (size_t)Pl));
-  TRY(dalloc(c, &c->part, (size_t)c->max_chunks * Pl));
-  TRY(dalloc(c, &c->bpart, (size_t)c->nblk * std::max(c->W, c->Wt)));
+  TRY(DALLOC(c, &c->X, (size_t)c->n * c->k));
+  TRY(DALLOC(c, &c->Xs, (size_t)c->n * c->ldx + 2));
+  TRY(DALLOC(c, &c->y, (size_t)c->n));
+  TRY(DALLOC(c, &c->mu, d));
+  TRY(DALLOC(c, &c->Lprior, (size_t)d * d));
+  TRY(DALLOC(c, &c->xbar, c->k));
+  TRY(DALLOC(c, &c->mon, (size_t)c->nmon * d));
+  TRY(DALLOC(c, &c->theta, (size_t)Pl * d + 2 * PR_TILE));
+  TRY(DALLOC(c, &c->theta2, (size_t)Pl * d + 2 * PR_TILE));
+  TRY(DALLOC(c, &c->theta_s, (size_t)Pl * d + 2 * PR_TILE));
+  TRY(DALLOC(c, &c->L, (size_t)Pl));
+  TRY(DALLOC(c, &c->L2, (size_t)Pl));
+  TRY(DALLOC(c, &c->lp, (size_t)Pl));
+  TRY(DALLOC(c, &c->lp2, (size_t)Pl));
+  TRY(DALLOC(c, &c->lw, (size_t)Pl));
+  TRY(DALLOC(c, &c->lw_cur, (size_t)Pl));
+  TRY(DALLOC(c, &c->lp_s, (size_t)Pl));
+  TRY(DALLOC(c, &c->part, (size_t)c->max_chunks * Pl));
+  TRY(DALLOC(c, &c->bpart, (size_t)c->nblk * std::max(c->W, c->Wt)));
   if (c->fu_fn) {
     const int64_t tiles = c->Pl / FU_TILE;
-    TRY(dalloc(c, &c->fu_tick, (size_t)(tiles + c->nblk)));
+    TRY(DALLOC(c, &c->fu_tick, (size_t)(tiles + c->nblk)));
     CU(c, cudaMemsetAsync(c->fu_tick, 0, sizeof(unsigned) * (size_t)(tiles + c->nblk), c->stream));
-    if (c->fu_TPR > 1) TRY(dalloc(c, &c->fu_tpart, (size_t)tiles * c->Wt));
+    if (c->fu_TPR > 1) TRY(DALLOC(c, &c->fu_tpart, (size_t)tiles * c->Wt));
     CU(c, cudaFuncSetAttribute(c->fu_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->fu_smem));
   }
-  TRY(dalloc(c, &c->Sinv, (size_t)d * d));
+  TRY(DALLOC(c, &c->Sinv, (size_t)d * d));
   CU(c, cudaHostAlloc((void**)&c->hslot, 2 * sizeof(Ctl), cudaHostAllocMapped));
   CU(c, cudaHostGetDevicePointer((void**)&c->dslot, c->hslot, 0));
-  TRY(dalloc(c, &c->ticket, 1));
+  TRY(DALLOC(c, &c->ticket, 1));
   CU(c, cudaMalloc((void**)&c->llbad, sizeof(int)));
   {
     static const int none = 0x7fffffff;
@@ -1366,16 +1410,16 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
   CU(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   CU(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   CU(c, cudaEventCreateWithFlags(&c->evs[1], cudaEventDisableTiming));
-  TRY(dalloc(c, &c->slice, (size_t)c->slice_len));
-  if (c->G > 1) TRY(dalloc(c, &c->gath, (size_t)c->slice_len * c->G));
+  TRY(DALLOC(c, &c->slice, (size_t)c->slice_len));
+  if (c->G > 1) TRY(DALLOC(c, &c->gath, (size_t)c->slice_len * c->G));
   else c->gath = c->slice;
   {
     // normals in rows of round_up(d, 4) (DMMA K padding), whole tiles: zeroed once, padding never written
     const size_t zn = (size_t)(Pl + PR_TILE) * round_up(d, 4);
-    TRY(dalloc(c, &c->Zbuf[0], zn));
-    TRY(dalloc(c, &c->Zbuf[1], zn));
-    TRY(dalloc(c, &c->LUbuf[0], (size_t)Pl));
-    TRY(dalloc(c, &c->LUbuf[1], (size_t)Pl));
+    TRY(DALLOC(c, &c->Zbuf[0], zn));
+    TRY(DALLOC(c, &c->Zbuf[1], zn));
+    TRY(DALLOC(c, &c->LUbuf[0], (size_t)Pl));
+    TRY(DALLOC(c, &c->LUbuf[1], (size_t)Pl));
     CU(c, cudaMemsetAsync(c->Zbuf[0], 0, zn * sizeof(double), c->stream));
     CU(c, cudaMemsetAsync(c->Zbuf[1], 0, zn * sizeof(double), c->stream));
     int lo = 0, hi = 0;
@@ -1387,54 +1431,54 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
       CU(c, cudaEventRecord(c->ev_zfree[q], c->stream));
     }
   }
-  TRY(dalloc(c, &c->shift, d));
+  TRY(DALLOC(c, &c->shift, d));
   {  // padded DMMA layouts (NP x KP, zeros outside d x d): Lprop, prior factor, prior precision
     const size_t pn = (size_t)round_up(d, 8) * round_up(d, 4);
-    TRY(dalloc(c, &c->Lprop, pn));
-    TRY(dalloc(c, &c->LpriorP, pn));
-    TRY(dalloc(c, &c->SinvP, pn));
-    TRY(dalloc(c, &c->RpP, pn));
-    TRY(dalloc(c, &c->Rp, (size_t)d * d));
+    TRY(DALLOC(c, &c->Lprop, pn));
+    TRY(DALLOC(c, &c->LpriorP, pn));
+    TRY(DALLOC(c, &c->SinvP, pn));
+    TRY(DALLOC(c, &c->RpP, pn));
+    TRY(DALLOC(c, &c->Rp, (size_t)d * d));
     CU(c, cudaMemsetAsync(c->Lprop, 0, pn * sizeof(double), c->stream));
     CU(c, cudaMemsetAsync(c->LpriorP, 0, pn * sizeof(double), c->stream));
     CU(c, cudaMemsetAsync(c->SinvP, 0, pn * sizeof(double), c->stream));
     CU(c, cudaMemsetAsync(c->RpP, 0, pn * sizeof(double), c->stream));
   }
-  TRY(dalloc(c, &c->V, (size_t)d * d));
-  TRY(dalloc(c, &c->rne, (size_t)c->nmon));
-  TRY(dalloc(c, &c->lwbuf, (size_t)c->Bmax * Pl));
+  TRY(DALLOC(c, &c->V, (size_t)d * d));
+  TRY(DALLOC(c, &c->rne, (size_t)c->nmon));
+  TRY(DALLOC(c, &c->lwbuf, (size_t)c->Bmax * Pl));
   const int ntiles = (int)((Pl + ESS_TILE - 1) / ESS_TILE);
-  TRY(dalloc(c, &c->essparts, (size_t)c->Bmax * ntiles * 3));
-  TRY(dalloc(c, &c->essslice, (size_t)c->Bmax * 3));
-  TRY(dalloc(c, &c->grp_ms, (size_t)c->Jl * 2));
+  TRY(DALLOC(c, &c->essparts, (size_t)c->Bmax * ntiles * 3));
+  TRY(DALLOC(c, &c->essslice, (size_t)c->Bmax * 3));
+  TRY(DALLOC(c, &c->grp_ms, (size_t)c->Jl * 2));
   if (const char* e = getenv("SPS_INC_CAP")) c->inc_cap = std::max(1, atoi(e));  // (test hook: tiny capacity)
-  TRY(dalloc(c, &c->inc_dev, (size_t)c->inc_cap));
+  TRY(DALLOC(c, &c->inc_dev, (size_t)c->inc_cap));
   if (cfg.tempering == SPS_DATA_TEMPERING) {
-    TRY(dalloc(c, &c->lse, (size_t)c->n + 1));
-    TRY(dalloc(c, &c->logpl, (size_t)c->n));
+    TRY(DALLOC(c, &c->lse, (size_t)c->n + 1));
+    TRY(DALLOC(c, &c->logpl, (size_t)c->n));
   }
-  TRY(dalloc(c, &c->Lj, (size_t)c->Jl));
+  TRY(DALLOC(c, &c->Lj, (size_t)c->Jl));
   if (c->G > 1) {
-    TRY(dalloc(c, &c->essgath, (size_t)c->Bmax * 3 * c->G));
-    TRY(dalloc(c, &c->grp_ms_gath, (size_t)c->J * 2));
-    TRY(dalloc(c, &c->Lj_gath, (size_t)c->J));
+    TRY(DALLOC(c, &c->essgath, (size_t)c->Bmax * 3 * c->G));
+    TRY(DALLOC(c, &c->grp_ms_gath, (size_t)c->J * 2));
+    TRY(DALLOC(c, &c->Lj_gath, (size_t)c->J));
   } else {
     c->essgath = c->essslice;
     c->grp_ms_gath = c->grp_ms;
     c->Lj_gath = c->Lj;
   }
-  TRY(dalloc(c, &c->scal, 8));
-  TRY(dalloc(c, &c->pw_parts, (size_t)PW_BLOCKS * 64 * 2));
-  TRY(dalloc(c, &c->pw_slice, 64 * 2));
-  if (c->G > 1) TRY(dalloc(c, &c->pw_gath, (size_t)64 * 2 * c->G));
+  TRY(DALLOC(c, &c->scal, 8));
+  TRY(DALLOC(c, &c->pw_parts, (size_t)PW_BLOCKS * 64 * 2));
+  TRY(DALLOC(c, &c->pw_slice, 64 * 2));
+  if (c->G > 1) TRY(DALLOC(c, &c->pw_gath, (size_t)64 * 2 * c->G));
   else c->pw_gath = c->pw_slice;
-  TRY(dalloc(c, &c->mx_parts, MX_BLOCKS));
-  TRY(dalloc(c, &c->mx_slice, 1));
-  if (c->G > 1) TRY(dalloc(c, &c->mx_gath, (size_t)c->G));
+  TRY(DALLOC(c, &c->mx_parts, MX_BLOCKS));
+  TRY(DALLOC(c, &c->mx_slice, 1));
+  if (c->G > 1) TRY(DALLOC(c, &c->mx_gath, (size_t)c->G));
   else c->mx_gath = c->mx_slice;
-  TRY(dalloc(c, &c->ctl, 1));
+  TRY(DALLOC(c, &c->ctl, 1));
   if (getenv("SPS_TIMELINE")) {
-    TRY(dalloc(c, &c->tl, (size_t)TL_W * TL_ROWS));
+    TRY(DALLOC(c, &c->tl, (size_t)TL_W * TL_ROWS));
     CU(c, cudaMemsetAsync(c->tl, 0, sizeof(unsigned long long) * TL_W * TL_ROWS, c->stream));
     const int* steps = &c->ctl->steps_done;
     CU(c, cudaMemcpyToSymbolAsync(g_tl, &c->tl, sizeof(c->tl), 0, cudaMemcpyHostToDevice, c->stream));
@@ -1461,8 +1505,8 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
     CU(c, cudaMemsetAsync(c->Xs + tot, 0, 2 * sizeof(double), c->stream));
     if (c->oz_KB > 0) {  // observation tile images of the sign-flipped X (ozaki.cuh)
       const int64_t ot = (c->n + OZ_NT - 1) / OZ_NT;
-      TRY(dalloc(c, &c->oz_X, (size_t)ot * oz_tile_bytes(OZ_NT, c->oz_KB)));
-      TRY(dalloc(c, &c->oz_xamax, 8));
+      TRY(DALLOC(c, &c->oz_X, (size_t)ot * oz_tile_bytes(OZ_NT, c->oz_KB)));
+      TRY(DALLOC(c, &c->oz_xamax, 8));
       CU(c, cudaMemsetAsync(c->oz_xamax, 0, 8 * sizeof(int), c->stream));
       k_oz_slice<<<(unsigned)((ot * OZ_NT + 127) / 128), 128, 0, c->stream>>>(c->Xs, c->n, c->ldx, c->k, c->oz_KB, OZ_NT,
                                                                                 1, 0, c->oz_X, nullptr, c->oz_xamax);
@@ -1472,7 +1516,7 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
       CU(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, ob));
       // particle images for this rank's P_local (the M steps' launches, captured into graphs)
       c->oz_T_cap = (size_t)((c->Pl + OZ_MT - 1) / OZ_MT) * oz_tile_bytes(OZ_MT, c->oz_KB);
-      TRY(dalloc(c, &c->oz_T, c->oz_T_cap));
+      TRY(DALLOC(c, &c->oz_T, c->oz_T_cap));
     }
     k_colmeans<<<(c->k + 127) / 128, 128, 0, c->stream>>>(c->X, c->n, c->k, c->xbar);
     CHECK_LAUNCH(c);
@@ -1556,7 +1600,43 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
   }
   CU(c, cudaEventCreate(&c->ev0));
   CU(c, cudaEventCreate(&c->ev1));
+  if (c->guarded && getenv("SPS_GUARD_POKE")) {  // test hook: an 8-byte overrun past the named buffer
+    const char* want = getenv("SPS_GUARD_POKE");
+    for (const auto& g : c->guards)
+      if (!std::strcmp(g.name, want)) CU(c, cudaMemsetAsync(g.base + GUARD_BYTES + g.bytes, 0, 8, c->stream));
+  }
   return sps_reset(c, cfg.seed, cfg.pass);
+}
+
+sps_status sps_check_guards(sps_ctx* c, int64_t* n_corrupt) {
+  if (!c) return SPS_E_CONFIG;
+  if (n_corrupt) *n_corrupt = 0;
+  if (!c->guarded) return fail(c, SPS_E_CONFIG, "sps_check_guards: context created without SPS_GUARD=1");
+  CU(c, cudaSetDevice(c->cfg.device));
+  if (c->aux) CU(c, cudaStreamSynchronize(c->aux));
+  CU(c, cudaStreamSynchronize(c->stream));
+  std::vector<unsigned char> zone(GUARD_BYTES);
+  int64_t bad = 0;
+  const char* first = nullptr;
+  int64_t first_off = 0;
+  for (const auto& g : c->guards)
+    for (int side = 0; side < 2; ++side) {
+      const char* z = side == 0 ? g.base : g.base + GUARD_BYTES + g.bytes;
+      CU(c, cudaMemcpy(zone.data(), z, GUARD_BYTES, cudaMemcpyDeviceToHost));
+      for (size_t i = 0; i < GUARD_BYTES; ++i)
+        if (zone[i] != GUARD_FILL) {
+          if (!first) {
+            first = g.name;
+            first_off = side == 0 ? (int64_t)i - (int64_t)GUARD_BYTES : (int64_t)(g.bytes + i);
+          }
+          ++bad;
+        }
+    }
+  if (n_corrupt) *n_corrupt = bad;
+  if (bad)
+    return fail(c, SPS_E_GUARD, "guard zones overwritten: %lld bytes; first: %s at byte offset %lld", (long long)bad,
+                first, (long long)first_off);
+  return SPS_OK;
 }
 
 sps_status sps_reset(sps_ctx* c, uint64_t seed, int32_t pass) {
@@ -1698,10 +1778,10 @@ sps_status sps_loglik(sps_ctx* c, const double* theta_dev, int64_t P, int32_t ld
   const int max_chunks = 64;
   const size_t need = (size_t)max_chunks * (size_t)P;
   if (need > c->ll_scratch_cap) {
-    if (c->ll_scratch) cudaFreeAsync(c->ll_scratch, c->stream);
+    dfree(c, c->ll_scratch, c->stream);
     c->ll_scratch = nullptr;
     c->ll_scratch_cap = 0;
-    TRY(dalloc(c, &c->ll_scratch, need));
+    TRY(DALLOC(c, &c->ll_scratch, need));
     c->ll_scratch_cap = need;
   }
   int nch = 1;
@@ -2176,10 +2256,10 @@ static sps_status reserve_sigma(sps_ctx* c, int64_t need) {
   if (need <= c->sig_rec_cap) return SPS_OK;
   const int64_t cap = std::max<int64_t>(need, 2 * c->sig_rec_cap), dd = (int64_t)c->d * c->d;
   double* nb = nullptr;
-  TRY(dalloc(c, &nb, (size_t)(cap * dd)));
+  TRY(DALLOC(c, &nb, (size_t)(cap * dd)));
   if (c->sig_rec) {
     CU(c, cudaMemcpyAsync(nb, c->sig_rec, sizeof(double) * c->sig_rec_cap * dd, cudaMemcpyDeviceToDevice, c->stream));
-    CU(c, cudaFreeAsync(c->sig_rec, c->stream));
+    dfree(c, c->sig_rec, c->stream);
   }
   c->sig_rec = nb;
   c->sig_rec_cap = cap;
@@ -2325,11 +2405,11 @@ sps_status sps_moments(sps_ctx* c, int32_t m, const double* A, double* mean, dou
   if (m == 0) return SPS_OK;
   CU(c, cudaSetDevice(c->cfg.device));
   if (m > c->fn_cap) {
-    if (c->fn_A) cudaFreeAsync(c->fn_A, c->stream);
-    if (c->fn_out) cudaFreeAsync(c->fn_out, c->stream);
+    dfree(c, c->fn_A, c->stream);
+    dfree(c, c->fn_out, c->stream);
     c->fn_A = c->fn_out = nullptr;
-    TRY(dalloc(c, &c->fn_A, (size_t)m * c->d));
-    TRY(dalloc(c, &c->fn_out, (size_t)m * 4));
+    TRY(DALLOC(c, &c->fn_A, (size_t)m * c->d));
+    TRY(DALLOC(c, &c->fn_out, (size_t)m * 4));
     c->fn_cap = m;
   }
   CU(c, cudaMemcpyAsync(c->fn_A, A, sizeof(double) * m * c->d, cudaMemcpyHostToDevice, c->stream));
@@ -2440,7 +2520,7 @@ sps_status sps_set_design(sps_ctx* c, int32_t L, const int32_t* t_cycle, const d
   if (!c || L < 0) return SPS_E_CONFIG;
   CU(c, cudaSetDevice(c->cfg.device));
   CU(c, cudaStreamSynchronize(c->stream));
-  if (c->sig_in) CU(c, cudaFreeAsync(c->sig_in, c->stream));
+  dfree(c, c->sig_in, c->stream);
   c->sig_in = nullptr;
   c->sig_in_n = 0;
   c->des_t.clear();
@@ -2459,7 +2539,7 @@ sps_status sps_set_design(sps_ctx* c, int32_t L, const int32_t* t_cycle, const d
     steps += R_cycle[l];
   }
   const int64_t dd = (int64_t)c->d * c->d;
-  TRY(dalloc(c, &c->sig_in, (size_t)(steps * dd)));
+  TRY(DALLOC(c, &c->sig_in, (size_t)(steps * dd)));
   CU(c, cudaMemcpyAsync(c->sig_in, sigma, sizeof(double) * steps * dd, cudaMemcpyHostToDevice, c->stream));
   CU(c, cudaStreamSynchronize(c->stream));
   c->sig_in_n = steps;
