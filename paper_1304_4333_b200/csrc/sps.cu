@@ -117,6 +117,9 @@ struct sps_ctx {
   sps_config cfg{};
   int n = 0, k = 0, C = 0, d = 0, J = 0, N = 0, G = 1, rank = 0, Jl = 0, g0 = 0;
   int64_t P = 0, Pl = 0, p0 = 0;
+  // exchange path (gathers, unfused finalize, host-driven M steps): G > 1, or one rank with a real
+  // NCCL communicator (cfg.nccl_id + SPS_XCHG_1RANK=1: the multi-GPU code path on one GPU)
+  bool xchg = false;
   int ldx = 0, KT = 0, PPT = 1, nmon = 0, dmax = 0, pp = 0, bpg = 0, nblk_mom = 0, ngy_mom = 0;
   int max_chunks = 1, Bmax = 8;
   cudaStream_t stream = nullptr;
@@ -391,7 +394,7 @@ int num_sms() {
 }
 
 sps_status gather(sps_ctx* c, const double* send, double* recv, size_t count) {
-  if (c->G == 1) {  // single rank: the gathered buffer aliases the local slice
+  if (!c->xchg) {  // single rank: the gathered buffer aliases the local slice
     if (send != recv) CU(c, cudaMemcpyAsync(recv, send, count * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
     return SPS_OK;
   }
@@ -1097,7 +1100,7 @@ sps_status moments_finalize(sps_ctx* c, bool decide, int nchunks, double temper,
                             const double* logu, int mode, bool allow_stop, int slot, bool fork_normals = false,
                             bool fused = false) {
   const bool graph = c->capturing;
-  if (c->G > 1) {
+  if (c->xchg) {
     TRY(accept_moments(c, decide, nchunks, temper, step, stop, logu, nullptr, 0, fork_normals ? step : ~0u, fused));
     return finalize(c, mode, allow_stop, stop, slot);
   }
@@ -1134,7 +1137,7 @@ void free_ctx(sps_ctx* c) {
     fprintf(stderr, "free_ctx %-10s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(t - T0).count());
     T0 = t;
   };
-  if (c->G == 1) {  // aliases of the local slices
+  if (!c->xchg) {  // aliases of the local slices
     c->gath = c->essgath = c->grp_ms_gath = c->Lj_gath = c->pw_gath = c->mx_gath = nullptr;
   }
   if (c->aux) cudaStreamSynchronize(c->aux);
@@ -1356,7 +1359,8 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
     CU(c, cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, hi));  // the critical path
     c->own_stream = true;
   }
-  if (c->G > 1 && cfg_in->nccl_id &&
+  c->xchg = c->G > 1 || (cfg_in->nccl_id && getenv("SPS_XCHG_1RANK") && atoi(getenv("SPS_XCHG_1RANK")) != 0);
+  if (c->xchg && cfg_in->nccl_id &&
       std::memcmp(cfg_in->nccl_id, kLoopMagic, sizeof kLoopMagic - 1) == 0) {  // loopback transport
     const std::string key((const char*)cfg_in->nccl_id, 128);
     std::lock_guard<std::mutex> lk(g_loop_mu);
@@ -1366,7 +1370,7 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
       lb->G = c->G;
     }
     c->loop = lb;
-  } else if (c->G > 1) {
+  } else if (c->xchg) {
     std::string why;
     if (!cfg_in->nccl_id) return fail(c, SPS_E_CONFIG, "nranks > 1 requires nccl_id");
     if (!g_nccl.load(&why)) return fail(c, SPS_E_NCCL, "%s", why.c_str());
@@ -1421,7 +1425,7 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
   CU(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   CU(c, cudaEventCreateWithFlags(&c->evs[1], cudaEventDisableTiming));
   TRY(DALLOC(c, &c->slice, (size_t)c->slice_len));
-  if (c->G > 1) TRY(DALLOC(c, &c->gath, (size_t)c->slice_len * c->G));
+  if (c->xchg) TRY(DALLOC(c, &c->gath, (size_t)c->slice_len * c->G));
   else c->gath = c->slice;
   {
     // normals in rows of round_up(d, 4) (DMMA K padding), whole tiles: zeroed once, padding never written
@@ -1468,7 +1472,7 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
     TRY(DALLOC(c, &c->logpl, (size_t)c->n));
   }
   TRY(DALLOC(c, &c->Lj, (size_t)c->Jl));
-  if (c->G > 1) {
+  if (c->xchg) {
     TRY(DALLOC(c, &c->essgath, (size_t)c->Bmax * 3 * c->G));
     TRY(DALLOC(c, &c->grp_ms_gath, (size_t)c->J * 2));
     TRY(DALLOC(c, &c->Lj_gath, (size_t)c->J));
@@ -1480,11 +1484,11 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
   TRY(DALLOC(c, &c->scal, 8));
   TRY(DALLOC(c, &c->pw_parts, (size_t)PW_BLOCKS * 64 * 2));
   TRY(DALLOC(c, &c->pw_slice, 64 * 2));
-  if (c->G > 1) TRY(DALLOC(c, &c->pw_gath, (size_t)64 * 2 * c->G));
+  if (c->xchg) TRY(DALLOC(c, &c->pw_gath, (size_t)64 * 2 * c->G));
   else c->pw_gath = c->pw_slice;
   TRY(DALLOC(c, &c->mx_parts, MX_BLOCKS));
   TRY(DALLOC(c, &c->mx_slice, 1));
-  if (c->G > 1) TRY(DALLOC(c, &c->mx_gath, (size_t)c->G));
+  if (c->xchg) TRY(DALLOC(c, &c->mx_gath, (size_t)c->G));
   else c->mx_gath = c->mx_slice;
   TRY(DALLOC(c, &c->ctl, 1));
   if (getenv("SPS_TIMELINE")) {
@@ -1565,7 +1569,7 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
       static const bool no_cl = getenv("SPS_NO_CLUSTER_REDUCE") != nullptr;
       const size_t fsm = (size_t)fin_smem_doubles(d, c->J, c->nmon, true) * sizeof(double);
       for (int cl : {16, 8}) {
-        if (no_cl || c->G != 1 || fsm > 200 * 1024) break;
+        if (no_cl || c->xchg || fsm > 200 * 1024) break;
         cudaLaunchConfig_t lc = {};
         lc.gridDim = dim3((unsigned)cl);
         lc.blockDim = dim3(256);
@@ -2300,7 +2304,7 @@ sps_status sps_mphase(sps_ctx* c, int32_t R_fixed, int32_t* R_out, double* min_r
   c->phase_step0 = step0;
   static const bool no_graph = getenv("SPS_NO_GRAPH") != nullptr;
   static const bool no_loop = getenv("SPS_NO_LOOP") != nullptr;
-  const bool graph = c->G == 1 && !c->profiling && !no_graph;
+  const bool graph = !c->xchg && !c->profiling && !no_graph;
   const bool loop = graph && !no_loop;
   if (c->pre_normals_step != (int64_t)step0) {
     // the first step's normals after all earlier work of the main stream (graph replays record no Zbuf events)
