@@ -73,7 +73,10 @@ typedef struct sps_config {
   const double* monitors;  /* host, n_monitors x d row-major; copied by sps_create          */
   int32_t pass;            /* stream pass tag (Alg. 3); 0 for a one-pass run                */
   int32_t rank, nranks;    /* group sharding; nranks = 1 for a single GPU                   */
-  const void* nccl_id;     /* host, 128-byte ncclUniqueId; required when nranks > 1         */
+  const void* nccl_id;     /* host, 128-byte ncclUniqueId; required when nranks > 1 (ignored
+                            * at nranks = 1 unless SPS_XCHG_1RANK=1: then the one rank runs the
+                            * multi-GPU exchange path over a one-rank communicator -- a test /
+                            * measurement hook for the NCCL transport on one GPU)               */
   int32_t device;          /* CUDA device ordinal                                           */
   void* stream;            /* cudaStream_t to enqueue on; NULL -> the library creates one   */
 } sps_config;
