@@ -67,6 +67,47 @@ def parse():
     return ap.parse_args()
 
 
+# ------------------------------------------------------------------ multi-rank host logic
+# (plain functions of (world, args, dist): tests/test_multirank_cpu.py runs them under gloo, world_size 2)
+def plan_workload(world, scaling_arg="auto", workload="cfg2", particles=1 << 20):
+    """Groups / particles per run and the workload description for `world` ranks.  Returns
+    dict(data, J, N, g, scaling, desc); J % world == 0 (rank r owns groups [r J / world, (r + 1) J / world))."""
+    import sps_synth
+
+    scaling = scaling_arg if scaling_arg != "auto" else ("weak" if world == 1 else "strong")
+    if workload == "cfg4":  # configs[3]: one context over all ranks, 1024 / world groups each
+        J, N, g, scaling = 1024, 1024, sps_synth.CONFIGS["cfg4"]["g"], "strong"
+        desc = ("configs[3]: large synthetic binary logit, n=100000, k=100 (1 + 30 continuous + 69 binary), "
+                f"J=1024 x N=1024 particles group-sharded over {world} GPU(s), g=1/4, full Algorithm 2 to posterior")
+        return dict(data="cfg4", J=J, N=N, g=g, scaling=scaling, desc=desc)
+    N, g = WORKLOAD["N"], WORKLOAD["g"]
+    if scaling == "strong":
+        J = max(world, particles // N) // world * world
+        desc = (f"configs[4] strong scaling: cfg2 data (n=1000, k=25, g=1/16), P={J * N} particles (J={J} x "
+                f"N={N}) fixed in total, {J // world} groups per GPU over {world} GPUs, full Algorithm 2 to posterior")
+    else:
+        J = WORKLOAD["J_per_gpu"] * world
+        desc = WORKLOAD_DESC if world == 1 else (WORKLOAD_DESC + f"; weak scaling: 64 groups per GPU x {world}")
+    return dict(data="cfg2", J=J, N=N, g=g, scaling=scaling, desc=desc)
+
+
+def broadcast_id(dist, rank, make_id):
+    """Rank 0 makes a 128-byte communicator id (ncclGetUniqueId), every rank receives it."""
+    ids = [make_id() if rank == 0 else None]
+    dist.broadcast_object_list(ids, src=0)
+    return ids[0]
+
+
+def max_over_ranks(dist, world, x, device):
+    """The job's time: max over ranks of a per-rank float (all_reduce MAX; identity at world = 1)."""
+    import torch
+
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -158,12 +199,8 @@ def run_reference(args, rank, world):
     v = pairs / secs
     # the same workload description (and scaling mode) as our arm at this N; the oracle runs its bounded
     # sample of it (same data, same g) on the host cores
-    scaling = args.scaling if args.scaling != "auto" else ("weak" if world == 1 else "strong")
-    if scaling == "strong":
-        wdesc = (f"configs[4] strong scaling: cfg2 data (n=1000, k=25, g=1/16), P={max(world, args.particles // 1024) * 1024} "
-                 f"particles (J={max(world, args.particles // 1024)} x N=1024) fixed in total, full Algorithm 2 to posterior")
-    else:
-        wdesc = WORKLOAD_DESC
+    plan = plan_workload(world, args.scaling, args.workload, args.particles)
+    scaling, wdesc = plan["scaling"], plan["desc"]
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "pairs/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -194,9 +231,7 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-        ids = [sps.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(ids, src=0)
-        nccl_id = ids[0]
+        nccl_id = broadcast_id(dist, rank, sps.nccl_unique_id)
     else:
         nccl_id = None
 
@@ -204,25 +239,9 @@ def main():
         if world > 1:
             dist.barrier()
 
-    scaling = args.scaling if args.scaling != "auto" else ("weak" if world == 1 else "strong")
-    if args.workload == "cfg4":  # configs[3]: one context over all ranks, 1024 / world groups each
-        X, y = sps_synth.config_data("cfg4")
-        g = sps_synth.CONFIGS["cfg4"]["g"]
-        J, N = 1024, 1024
-        scaling = "strong"
-        wdesc = ("configs[3]: large synthetic binary logit, n=100000, k=100 (1 + 30 continuous + 69 binary), "
-                 f"J=1024 x N=1024 particles group-sharded over {world} GPU(s), g=1/4, full Algorithm 2 to posterior")
-    else:
-        X, y = sps_synth.config_data("cfg2")
-        g = WORKLOAD["g"]
-        N = WORKLOAD["N"]
-        if scaling == "strong":
-            J = max(world, args.particles // N)
-            wdesc = (f"configs[4] strong scaling: cfg2 data (n=1000, k=25, g=1/16), P={J * N} particles (J={J} x "
-                     f"N={N}) fixed in total, {J // world} groups per GPU over {world} GPUs, full Algorithm 2 to posterior")
-        else:
-            J = WORKLOAD["J_per_gpu"] * world
-            wdesc = WORKLOAD_DESC if world == 1 else (WORKLOAD_DESC + f"; weak scaling: 64 groups per GPU x {world}")
+    plan = plan_workload(world, args.scaling, args.workload, args.particles)
+    X, y = sps_synth.config_data(plan["data"])
+    J, N, g, scaling, wdesc = plan["J"], plan["N"], plan["g"], plan["scaling"], plan["desc"]
     n, k = X.shape
     cov = sps.g_prior(X, 2, g, device=local)
     stream = torch.cuda.Stream(device=dev)
@@ -256,10 +275,7 @@ def main():
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
-    tot_ms = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(tot_ms, op=dist.ReduceOp.MAX)
-    tot_ms = float(tot_ms.item())
+    tot_ms = max_over_ranks(dist, world, sum(times), dev)
     value = pairs / (tot_ms / 1e3)
 
     # ---- roofline of the dominant kernel (K1) measured inside a real run, events on the ctx stream
@@ -311,9 +327,7 @@ def main():
         for s in range(args.steps):
             id2 = None
             if world > 1:  # every communicator needs its own ncclUniqueId (rank 0 makes it, all receive it)
-                ids2 = [sps.nccl_unique_id() if rank == 0 else None]
-                dist.broadcast_object_list(ids2, src=0)
-                id2 = ids2[0]
+                id2 = broadcast_id(dist, rank, sps.nccl_unique_id)
             t0 = time.perf_counter()
             c2 = sps.Sps(Xp, yp, np.zeros(k), cov, J=J, N=N, seed=1 + s, rank=rank, nranks=world,
                          nccl_id=id2, device=local)
@@ -323,10 +337,8 @@ def main():
             e2e_pairs += r2["pairs"]
             L2 = r2["L"]
             d2h = 4 * 6 * L2 + 8 * 6 + 32  # per-cycle trace + moments + logml
-        wt = torch.tensor([wall], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(wt, op=dist.ReduceOp.MAX)
-        e2e = {"value": e2e_pairs / float(wt.item()), "unit": "pairs/s", "h2d_bytes_per_step": int(h2d),
+        wt = max_over_ranks(dist, world, wall, dev)
+        e2e = {"value": e2e_pairs / wt, "unit": "pairs/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h)}
 
     # ---- strong scaling: the same workload on ONE GPU (rank 0; the other ranks wait at the barrier)

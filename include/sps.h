@@ -267,6 +267,13 @@ sps_status sps_nccl_unique_id(void* id128);
  * memory at a host barrier.  Exercises the sharded engine without NCCL; slow. */
 sps_status sps_loopback_unique_id(void* id128);
 
+/* Test export (host only, no device): one all-gather of the loopback group `id128` (G ranks, one
+ * host thread per rank, each calling with its own rank): `send` (bytes, host) of every rank lands in
+ * `recv` (G x bytes, host) in rank order, after all G ranks have arrived -- the exchange primitive the
+ * sharded engine uses over the loopback transport.  SPS_E_CONFIG on a bad id / rank / G mismatch. */
+sps_status sps_test_loopback_allgather(const void* id128, int32_t rank, int32_t G, const void* send, int64_t bytes,
+                                       void* recv);
+
 /* Zellner g-prior (PAPER.md:665-668 eq. g-prior_def, exchangeable, normalized
  * by eq. prior_norm): cov (d x d, host) = blocks
  * (2 if i == j else 1) * g T (X'X)^-1.  Computed on the device.  (R9) */

@@ -69,6 +69,7 @@ EXPORTED = [
     "sps_g_prior", "sps_test_philox", "sps_test_normals", "sps_test_portable", "sps_test_resample_int",
     "sps_test_resample_group", "sps_test_accept", "sps_reset", "sps_set_profiling", "sps_get_counters", "sps_sync", "sps_loopback_unique_id",
     "sps_record_sigma", "sps_get_sigma", "sps_set_design", "sps_predictive", "sps_check_guards",
+    "sps_test_loopback_allgather",
 ]
 
 
@@ -121,6 +122,7 @@ def _declare(L):
         "sps_get_particles": ([vp, dp, dp, dp], st),
         "sps_shard": ([vp, C.POINTER(C.c_int64), ip, ip], st),
         "sps_check_guards": ([vp, C.POINTER(C.c_int64)], st),
+        "sps_test_loopback_allgather": ([vp, C.c_int32, C.c_int32, vp, C.c_int64, vp], st),
         "sps_destroy": ([vp], None),
         "sps_last_error": ([vp], C.c_char_p),
         "sps_nccl_unique_id": ([vp], st),

@@ -251,6 +251,16 @@ def loopback_unique_id() -> bytes:
     return buf.raw
 
 
+def test_loopback_allgather(lid: bytes, rank: int, G: int, send: np.ndarray) -> np.ndarray:
+    """One all-gather of the loopback group lid (host only; call from G threads, one per rank)."""
+    send = np.ascontiguousarray(send, dtype=np.uint8)
+    recv = np.zeros(G * send.size, dtype=np.uint8)
+    idb = C.create_string_buffer(bytes(lid), 128)
+    _check(lib().sps_test_loopback_allgather(idb, rank, G, send.ctypes.data_as(C.c_void_p), send.size,
+                                             recv.ctypes.data_as(C.c_void_p)), what="sps_test_loopback_allgather")
+    return recv
+
+
 def g_prior(X, C_, g, device=0):
     X = np.ascontiguousarray(X, dtype=np.float64)
     n, k = X.shape

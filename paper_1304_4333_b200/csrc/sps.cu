@@ -101,6 +101,17 @@ struct Loopback {
 };
 std::mutex g_loop_mu;
 std::map<std::string, std::shared_ptr<Loopback>> g_loops;
+// The group registered under a loopback id (created by its first rank).
+std::shared_ptr<Loopback> loopback_get(const void* id128, int G) {
+  const std::string key((const char*)id128, 128);
+  std::lock_guard<std::mutex> lk(g_loop_mu);
+  auto& lb = g_loops[key];
+  if (!lb) {
+    lb = std::make_shared<Loopback>();
+    lb->G = G;
+  }
+  return lb;
+}
 }  // namespace
 
 // ================================================================== context
@@ -1225,6 +1236,16 @@ void sps_destroy(sps_ctx* ctx) {
   delete ctx;
 }
 
+sps_status sps_test_loopback_allgather(const void* id128, int32_t rank, int32_t G, const void* send, int64_t bytes,
+                                       void* recv) {
+  if (!id128 || G < 1 || rank < 0 || rank >= G || bytes < 0 || (bytes > 0 && (!send || !recv))) return SPS_E_CONFIG;
+  if (std::memcmp(id128, kLoopMagic, sizeof kLoopMagic - 1) != 0) return SPS_E_CONFIG;
+  std::shared_ptr<Loopback> lb = loopback_get(id128, G);
+  if (lb->G != G) return SPS_E_CONFIG;
+  lb->allgather(rank, send, (size_t)bytes, recv);
+  return SPS_OK;
+}
+
 sps_status sps_loopback_unique_id(void* id128) {
   if (!id128) return SPS_E_CONFIG;
   static std::mutex mu;
@@ -1362,14 +1383,7 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
   c->xchg = c->G > 1 || (cfg_in->nccl_id && getenv("SPS_XCHG_1RANK") && atoi(getenv("SPS_XCHG_1RANK")) != 0);
   if (c->xchg && cfg_in->nccl_id &&
       std::memcmp(cfg_in->nccl_id, kLoopMagic, sizeof kLoopMagic - 1) == 0) {  // loopback transport
-    const std::string key((const char*)cfg_in->nccl_id, 128);
-    std::lock_guard<std::mutex> lk(g_loop_mu);
-    auto& lb = g_loops[key];
-    if (!lb) {
-      lb = std::make_shared<Loopback>();
-      lb->G = c->G;
-    }
-    c->loop = lb;
+    c->loop = loopback_get(cfg_in->nccl_id, c->G);
   } else if (c->xchg) {
     std::string why;
     if (!cfg_in->nccl_id) return fail(c, SPS_E_CONFIG, "nranks > 1 requires nccl_id");

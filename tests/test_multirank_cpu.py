@@ -3,7 +3,11 @@ the NCCL unique id that bench.py broadcasts from rank 0 arrives intact on every
 rank, and the group-sharded exchange protocol of the engine (each rank owns
 J/G contiguous groups; slices are all-gathered and combined in rank order,
 DESIGN.md "Multi-GPU") reproduces the unsharded statistics bit for bit and
-gives identical decisions on every rank."""
+gives identical decisions on every rank.  bench.py's own multi-rank helpers
+(plan_workload, broadcast_id, max_over_ranks) run under gloo as they do under
+NCCL, and the library's loopback all-gather (the exchange primitive of the
+sharded engine's in-process transport, libsps.so host code) runs on host
+threads without a device."""
 import os
 import socket
 
@@ -74,7 +78,18 @@ def _worker(rank, world, port, q):
         same_on_ranks = all(x == res[0] for x in res)
         close_to_ref = np.allclose(bar, ref[0], rtol=1e-13) and np.allclose(V, ref[1], rtol=1e-12) and \
             abs(rne - ref[2]) < 1e-12 * ref[2]
-        q.put((rank, ok_id, same_on_ranks, close_to_ref))
+        # 3. bench.py's multi-rank helpers, exactly as the N > 1 bench calls them (gloo instead of NCCL)
+        import bench
+
+        bid = bench.broadcast_id(dist, rank, sps.nccl_unique_id)
+        allb = [None] * world
+        dist.all_gather_object(allb, bid)
+        ok_bench_id = len(bid) == 128 and all(x == bid for x in allb) and bid != ids[0]  # fresh id per call
+        tmax = bench.max_over_ranks(dist, world, 10.0 + rank * 2.5, "cpu")
+        plan = bench.plan_workload(world)
+        ok_bench = ok_bench_id and tmax == 10.0 + (world - 1) * 2.5 and plan["scaling"] == "strong" and \
+            plan["J"] * plan["N"] == 1 << 20 and plan["J"] % world == 0
+        q.put((rank, ok_id, same_on_ranks, close_to_ref and ok_bench))
     finally:
         dist.destroy_process_group()
 
@@ -95,3 +110,55 @@ def test_gloo_two_ranks_protocol(world):
         p.join(timeout=60)
     for rank, ok_id, same, close in out:
         assert ok_id and same and close, (rank, ok_id, same, close)
+
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_library_loopback_allgather_host_threads(G):
+    """libsps.so's loopback all-gather (sps_test_loopback_allgather; host only): G threads, 40 rounds of
+    varying sizes (0 included) -- every rank receives all ranks' bytes in rank order every round, and
+    fast ranks never overwrite a round the slow ones are still reading (double-buffered generations)."""
+    import threading
+
+    import paper_1304_4333_b200 as sps
+    from paper_1304_4333_b200 import api
+
+    sps.build()
+    lid = sps.loopback_unique_id()
+    rounds = 40
+    sizes = [(37 * r) % 1001 for r in range(rounds)]
+    payload = lambda rank, r: np.full(sizes[r], (rank * 41 + r * 7) % 251, dtype=np.uint8)  # noqa: E731
+    got = {}
+    errs = []
+
+    def worker(rank):
+        try:
+            for r in range(rounds):
+                got[(rank, r)] = api.test_loopback_allgather(lid, rank, G, payload(rank, r))
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=worker, args=(q,)) for q in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=60)
+    assert not errs, errs
+    for r in range(rounds):
+        want = np.concatenate([payload(q, r) for q in range(G)])
+        for rank in range(G):
+            assert np.array_equal(got[(rank, r)], want), (rank, r)
+
+
+def test_library_loopback_allgather_bad_args():
+    import paper_1304_4333_b200 as sps
+    from paper_1304_4333_b200 import api
+
+    sps.build()
+    lid = sps.loopback_unique_id()
+    with pytest.raises(sps.SpsError):
+        api.test_loopback_allgather(lid, 2, 2, np.zeros(4, np.uint8))  # rank >= G
+    with pytest.raises(sps.SpsError):
+        api.test_loopback_allgather(b"not-a-loopback-id".ljust(128, b"\0"), 0, 1, np.zeros(4, np.uint8))
+    assert np.array_equal(api.test_loopback_allgather(lid, 0, 1, np.arange(5, dtype=np.uint8)), np.arange(5))
+    with pytest.raises(sps.SpsError):  # the group was registered with G = 1
+        api.test_loopback_allgather(lid, 0, 2, np.zeros(4, np.uint8))
