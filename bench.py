@@ -119,15 +119,32 @@ class ClockSampler:
         self.proc = None
         self.path = None
 
+    def _lines(self):
+        try:
+            return open(self.path).read().splitlines()
+        except OSError:
+            return []
+
     def start(self):
+        """Start sampling every 50 ms; returns once the first sample is in (nvidia-smi takes a few hundred
+        ms to start), so that the timed region that follows is covered from its beginning."""
         fd, self.path = tempfile.mkstemp(suffix=".csv")
         os.close(fd)
+        self.n0 = 0
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200",
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "50",
                  "-i", str(self.gpu)], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
+            return
+        t0 = time.time()
+        while not self._lines() and time.time() - t0 < 5.0 and self.proc.poll() is None:
+            time.sleep(0.01)
+
+    def mark(self):
+        """The timed region starts now: samples taken before are dropped."""
+        self.n0 = len(self._lines())
 
     def stop(self):
         if self.proc is None:
@@ -139,7 +156,9 @@ class ClockSampler:
             self.proc.kill()
         sms, maxs, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
+        lines = self._lines()
+        lines = lines[self.n0:] if len(lines) > self.n0 else lines[-1:]  # (a region shorter than one period)
+        for line in lines:
             f = [x.strip() for x in line.split(",")]
             if len(f) < 9:
                 continue
@@ -254,9 +273,10 @@ def main():
         ctx.run()
 
     clocks = ClockSampler(local)
+    clocks.start()
     barrier()
     torch.cuda.synchronize()
-    clocks.start()
+    clocks.mark()
     times, pairs, launches = [], 0.0, 0
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
