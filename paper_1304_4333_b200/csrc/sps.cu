@@ -172,7 +172,8 @@ struct sps_ctx {
   unsigned long long* tl = nullptr;     // debug (SPS_TIMELINE): per-step kernel start / end clocks
   double tl_acc[24] = {};
   int tl_rows = 0;
-  double tl_bin[6][8] = {};  // by t_l bin (<=32, <=64, <=128, <=256, <=512, >512): steps, K1 span, step span, gap
+  double tl_bin[6][8] = {};
+  double tl_gap_par[2][2] = {};  // next-propose gap by step parity within the phase: sum, count  // by t_l bin (<=32, <=64, <=128, <=256, <=512, >512): steps, K1 span, step span, gap
   double trace_acc[80] = {};
   int trace_n = 0;
   double* Zbuf[2] = {nullptr, nullptr};  // standard normals, one M step ahead (side stream)
@@ -1756,7 +1757,9 @@ sps_status sps_get_counters(const sps_ctx* cc, sps_counters* out) {
                                "fin chol|RNE", "fin(chol only)", "fin(RNE w1 only)"};
     fprintf(stderr, "SPS_TIMELINE mean us over %d steps:", c->tl_rows);
     for (int q = 0; q < 24; ++q) fprintf(stderr, " %s=%.2f", nm[q], c->tl_acc[q] / c->tl_rows / 1e3);
-    fprintf(stderr, "\n");
+    fprintf(stderr, " gap next propose<-fin after even / odd steps=%.2f / %.2f\n",
+            c->tl_gap_par[0][0] / std::max(1.0, c->tl_gap_par[0][1]) / 1e3,
+            c->tl_gap_par[1][0] / std::max(1.0, c->tl_gap_par[1][1]) / 1e3);
     static const char* bn[] = {"t<=32", "t<=64", "t<=128", "t<=256", "t<=512", "t>512"};
     for (int b = 0; b < 6; ++b)
       if (c->tl_bin[b][0] > 0)
@@ -2051,7 +2054,12 @@ static sps_status timeline_accumulate(sps_ctx* c, int R) {
     c->tl_acc[9] += (double)t[10] - (double)t[9];   // finalize start - reduce end
     c->tl_acc[10] += (double)t[2] - (double)t[1];   // normals start - propose end
     c->tl_acc[11] += (double)t[3] - (double)t[5];   // normals end - K1 end
-    if (r + 1 < rows && h[(size_t)(r + 1) * TL_W]) c->tl_acc[12] += (double)h[(size_t)(r + 1) * TL_W] - (double)t[11];
+    if (r + 1 < rows && h[(size_t)(r + 1) * TL_W]) {
+      const double g = (double)h[(size_t)(r + 1) * TL_W] - (double)t[11];
+      c->tl_acc[12] += g;
+      c->tl_gap_par[r & 1][0] += g;  // even r: next step in the same graph body; odd: the next body
+      c->tl_gap_par[r & 1][1] += 1;
+    }
     c->tl_acc[13] += (double)t[11] - (double)t[0];  // step: propose start -> finalize end
     {
       const int tt = c->cfg.tempering == SPS_POWER_TEMPERING ? c->n : c->t;
@@ -2215,6 +2223,17 @@ static sps_status build_mstep_graphs(sps_ctx* c, bool allow_stop) {
 // Device-side M phase: a graph with one WHILE node whose body (captured from one M step) runs until
 // the finalize kernel clears the condition (min RNE >= K, or the step cap).  Captured per phase and
 // applied to the previous executable graph with cudaGraphExecUpdate when possible.
+// M steps per body of the device-side loop (SPS_LOOP_BODY: tuning; even, 2..16; default 4: cfg2 run
+// 148.2 / 147.0 / 147.3 / 147.7 ms at 2 / 4 / 6 / 8).
+static int loop_body() {
+  static const int b = [] {
+    const char* e = getenv("SPS_LOOP_BODY");
+    const int v = e ? atoi(e) : 4;
+    return std::min(16, std::max(2, v / 2 * 2));
+  }();
+  return b;
+}
+
 static sps_status build_mstep_loop(sps_ctx* c, bool allow_stop, int rmax) {
   cudaGraph_t g = nullptr;
   CU(c, cudaGraphCreate(&g, 0));
@@ -2234,10 +2253,11 @@ static sps_status build_mstep_loop(sps_ctx* c, bool allow_stop, int rmax) {
   c->loop_rmax = rmax;
   CU(c, cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
   c->capturing = c->capturing_loop = true;
-  // two M steps per body: half the loop-iteration boundaries (~4.8 us each vs ~1.5 between kernels);
-  // after a stop the second step's kernels return at once
-  sps_status st = launch_mstep(c, c->phase_step0, allow_stop, true);
-  if (st == SPS_OK) st = launch_mstep(c, c->phase_step0 + 1u, allow_stop, true);
+  // B (even) M steps per body: a loop-iteration boundary costs ~5.5 us more than the gap between two
+  // steps of one body (SPS_TIMELINE: 6.8 vs 1.35 us); after a stop the body's remaining steps'
+  // kernels return at once.  B even keeps each body position on one parity (Z / log u buffers).
+  sps_status st = SPS_OK;
+  for (int q = 0; q < loop_body() && st == SPS_OK; ++q) st = launch_mstep(c, c->phase_step0 + (uint32_t)q, allow_stop, true);
   c->capturing = c->capturing_loop = false;
   cudaGraph_t captured = nullptr;
   const cudaError_t ee = cudaStreamEndCapture(c->stream, &captured);
@@ -2343,9 +2363,9 @@ sps_status sps_mphase(sps_ctx* c, int32_t R_fixed, int32_t* R_out, double* min_r
     c->syncs += 1;
     const Ctl got = c->hslot[0];
     const int r = got.steps_done;
-    c->launches += c->gl_launches / 2 * r;  // (the body holds two steps)
-    c->k1_launches += c->gl_k1 / 2 * r;
-    c->k1_pairs += c->gl_pairs / 2 * r;
+    c->launches += c->gl_launches / loop_body() * r;  // (the body holds loop_body() steps)
+    c->k1_launches += c->gl_k1 / loop_body() * r;
+    c->k1_pairs += c->gl_pairs / loop_body() * r;
     c->pairs += (double)c->P * t1 * r;
     if (got.err == ERR_NUMERIC)
       return fail(c, SPS_E_NUMERIC, "numerical failure in the M phase (non-finite loglik or Cholesky failure "
