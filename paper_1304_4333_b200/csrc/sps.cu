@@ -639,7 +639,9 @@ sps_status get_plan(sps_ctx* c, int64_t P, int range, int max_chunks, sps_ctx::P
     const int sub_cap = std::min(std::max(16, sub_cap_env / 16 * 16), std::max(16, (chunk_cap / 2) / 16 * 16));
     const int S_min = ch.streams ? 1 : std::max(1, (range + chunk_cap - 1) / chunk_cap);
     static const int s_cap = getenv("SPS_K1_SMAX") ? std::max(1, atoi(getenv("SPS_K1_SMAX"))) : 1 << 20;  // tuning
-    static const double ovh = getenv("SPS_K1_OVH") ? atof(getenv("SPS_K1_OVH")) : 24.0;
+    // (round 2: 64 -- cfg2 run 145.6-146.0 -> 144.1-144.3 ms, in-run K1 frac 0.583 -> 0.590; 48-160 alike;
+    // 2^20, cfg3, cfg1 unchanged)
+    static const double ovh = getenv("SPS_K1_OVH") ? atof(getenv("SPS_K1_OVH")) : 64.0;
     const int S_hi = std::min(std::min(max_chunks, s_cap), std::max(S_min, std::min(S_min + 24, range / 8)));
     const int warp_regs = ((c->ll_regs * 32 + 255) / 256) * 256;
     const int by_regs = 65536 / ((LL_THREADS / 32) * warp_regs);
