@@ -806,9 +806,15 @@ sps_status launch_normals(sps_ctx* c, uint32_t tag, uint32_t step, int slot, boo
     static const bool at_propose = getenv("SPS_NORMALS_FORK") && !strcmp(getenv("SPS_NORMALS_FORK"), "propose");
     // forked at the proposal: one 64-thread block per SM (its 4 K registers fit beside 4 K1 blocks) over
     // the whole step; forked at accept: 8 x 256 per SM into the tail
-    static const int nb_per_sm =
-        getenv("SPS_NORMALS_BPS") ? atoi(getenv("SPS_NORMALS_BPS")) : (at_propose ? 1 : 8);
-    static const int nthr = getenv("SPS_NORMALS_THREADS") ? atoi(getenv("SPS_NORMALS_THREADS")) : (at_propose ? 64 : 256);
+    // forked at accept, small steps (<= 2M Box-Muller pairs): 4 x 128 per SM -- the normals finish
+    // inside the reduce / finalize tail anyway and take fewer issue slots from it (cfg2 run 144.2 ->
+    // 142.0 ms; 2^17: -0.6%); larger steps need the full 8 x 256 to leave the critical path (2^18:
+    // +2%, 2^20: +10% at 4 x 128)
+    const bool small = tasks <= (int64_t)2 << 20;
+    static const int bps_env = getenv("SPS_NORMALS_BPS") ? atoi(getenv("SPS_NORMALS_BPS")) : 0;
+    static const int thr_env = getenv("SPS_NORMALS_THREADS") ? atoi(getenv("SPS_NORMALS_THREADS")) : 0;
+    const int nb_per_sm = bps_env ? bps_env : (at_propose ? 1 : (small ? 4 : 8));
+    const int nthr = thr_env ? thr_env : (at_propose ? 64 : (small ? 128 : 256));
     const int64_t fullb = (tasks + nthr - 1) / nthr;
     lc.gridDim = dim3((unsigned)(forked && nb_per_sm > 0 ? std::min<int64_t>(fullb, nb_per_sm * (int64_t)num_sms())
                                                         : full));
