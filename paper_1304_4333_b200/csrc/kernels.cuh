@@ -256,16 +256,17 @@ __global__ void __launch_bounds__(256) k_functional_stats(const double* __restri
 // in observation order (the same serial sum as one thread per particle).
 // theta staged transposed in shared memory (d x SCAN_PB).
 constexpr int SCAN_PB = 32, SCAN_Q = 8;
+constexpr int SCAN_LD = SCAN_PB + 1;  // row stride of the transposed theta tile (odd: conflict-free transposing stores)
 
 __device__ __forceinline__ double scan_term_bin(const double* __restrict__ x, const double* __restrict__ sth, int k,
                                                 int pl) {
   double a0 = 0.0, a1 = 0.0;
   int i = 0;
   for (; i + 2 <= k; i += 2) {
-    a0 = fma(sth[i * SCAN_PB + pl], __ldg(x + i), a0);
-    a1 = fma(sth[(i + 1) * SCAN_PB + pl], __ldg(x + i + 1), a1);
+    a0 = fma(sth[i * SCAN_LD + pl], __ldg(x + i), a0);
+    a1 = fma(sth[(i + 1) * SCAN_LD + pl], __ldg(x + i + 1), a1);
   }
-  if (i < k) a0 = fma(sth[i * SCAN_PB + pl], __ldg(x + i), a0);
+  if (i < k) a0 = fma(sth[i * SCAN_LD + pl], __ldg(x + i), a0);
   const double s = a0 + a1;
   return -(fmax(s, 0.0) + log1p(exp(-fabs(s))));
 }
@@ -274,13 +275,30 @@ __global__ void __launch_bounds__(SCAN_PB * SCAN_Q) k_cphase_scan(
     const double* __restrict__ Xs, const int32_t* __restrict__ y, int ldx, int k, int C,
     const double* __restrict__ theta, int d, int64_t P, int s0, int B, double* __restrict__ lw_cur,
     double* __restrict__ lwbuf) {
-  extern __shared__ double sth[];  // d x SCAN_PB (transposed)
+  extern __shared__ double sth[];  // d x SCAN_LD (transposed)
   const int pl = threadIdx.x % SCAN_PB, q = threadIdx.x / SCAN_PB;
   const int64_t p0 = (int64_t)blockIdx.x * SCAN_PB;
   const int np = (int)min((int64_t)SCAN_PB, P - p0);
-  for (int e = threadIdx.x; e < d * SCAN_PB; e += blockDim.x) {
-    const int i = e / SCAN_PB, j = e % SCAN_PB;
-    sth[e] = j < np ? theta[(p0 + j) * d + i] : 0.0;
+  {  // the block's np contiguous theta rows, read coalesced (4 loads in flight per thread), stored
+     // transposed (a transposed, row-strided read was 20% of the kernel's stall samples)
+    const double* src = theta + p0 * d;
+    const int tot = np * d;
+    for (int e0 = threadIdx.x; e0 < d * SCAN_PB; e0 += 4 * blockDim.x) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + u * blockDim.x;
+        v[u] = e < tot ? src[e] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + u * blockDim.x;
+        if (e < d * SCAN_PB) {
+          const int j = e / d, i = e - j * d;  // row j (particle), column i
+          sth[i * SCAN_LD + j] = v[u];
+        }
+      }
+    }
   }
   __syncthreads();
   const int64_t p = p0 + pl;
@@ -307,7 +325,7 @@ __global__ void __launch_bounds__(SCAN_PB * SCAN_Q) k_cphase_scan(
         double m = 0.0;
         for (int c = 1; c < C; ++c) {
           double s = 0.0;
-          for (int i = 0; i < k; ++i) s = fma(sth[((c - 1) * k + i) * SCAN_PB + pl], __ldg(x + i), s);
+          for (int i = 0; i < k; ++i) s = fma(sth[((c - 1) * k + i) * SCAN_LD + pl], __ldg(x + i), s);
           eta[c] = s;
           m = fmax(m, s);
         }
@@ -349,14 +367,33 @@ __global__ void __launch_bounds__(256) k_ess_partials(const double* __restrict__
   const int b = blockIdx.y, ti = blockIdx.x, ntiles = gridDim.x;
   const double* v = lwbuf + (int64_t)b * P + (int64_t)ti * tile;
   const int cnt = (int)min((int64_t)tile, P - (int64_t)ti * tile);
-  double m = -INFINITY;
-  for (int i = threadIdx.x; i < cnt; i += blockDim.x) m = fmax(m, v[i]);
-  m = block_max(m, red);
-  double s1 = 0.0, s2 = 0.0;
-  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-    const double w = exp(v[i] - m);
-    s1 += w;
-    s2 += w * w;
+  double m = -INFINITY, s1 = 0.0, s2 = 0.0;
+  constexpr int EU = 8;  // a tile of <= 8 x blockDim values: all loads in flight, one pass over memory
+  if (cnt <= EU * (int)blockDim.x) {  // (the max waited on one load at a time: 46% of the stall samples)
+    double x[EU];
+#pragma unroll
+    for (int u = 0; u < EU; ++u) {
+      const int i = threadIdx.x + u * blockDim.x;
+      x[u] = i < cnt ? v[i] : -INFINITY;
+    }
+#pragma unroll
+    for (int u = 0; u < EU; ++u) m = fmax(m, x[u]);
+    m = block_max(m, red);
+#pragma unroll
+    for (int u = 0; u < EU; ++u)
+      if (threadIdx.x + u * blockDim.x < cnt) {  // the same terms in the same order as the loop below
+        const double w = exp(x[u] - m);
+        s1 += w;
+        s2 += w * w;
+      }
+  } else {
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) m = fmax(m, v[i]);
+    m = block_max(m, red);
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+      const double w = exp(v[i] - m);
+      s1 += w;
+      s2 += w * w;
+    }
   }
   s1 = block_sum(s1, red);
   s2 = block_sum(s2, red);

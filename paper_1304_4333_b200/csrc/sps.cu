@@ -1891,7 +1891,7 @@ sps_status sps_cphase(sps_ctx* c, int32_t t_target, double phi_target, int32_t* 
     int B = 8;  // first galloping chunk: twice the last cycle's advance (usually one chunk, one sync)
     while (B < 2 * c->last_adv && B < c->Bmax) B *= 2;
     const int ntiles = (int)((Pl + ESS_TILE - 1) / ESS_TILE);
-    const size_t scan_smem = sizeof(double) * c->d * SCAN_PB;
+    const size_t scan_smem = sizeof(double) * c->d * SCAN_LD;
     CU(c, cudaFuncSetAttribute(k_cphase_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem + 1024));
     for (;;) {
       int Be = std::min(std::min(B, c->Bmax), c->n - s);
