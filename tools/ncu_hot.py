@@ -15,8 +15,8 @@ want = ["Duration", "Issue Slots Busy", "Achieved Occupancy", "Warp Cycles Per I
         "Executed Instructions", "Registers Per Thread", "Block Limit Registers", "Memory Throughput",
         "DRAM Throughput", "L2 Hit Rate"]
 for r in csv.reader(io.StringIO(det)):
-    if len(r) > 14 and r[13] in want:
-        print(f"  {r[13]}: {r[15]} {r[14]}")
+    if len(r) > 14 and r[12] in want:  # [..., section, metric name, unit, value]
+        print(f"  {r[12]}: {r[14]} {r[13]}")
 src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(src)))
 h = [i for i, r in enumerate(rows) if "Warp Stall Sampling (All Samples)" in r]
