@@ -156,13 +156,16 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 // Debug timeline (SPS_TIMELINE): per M step (row = *g_tl_steps, the step
 // index within the phase) and kernel slot k, [2k] = start of block (0,0),
-// [2k+1] = latest block end (atomicMax).  Null when disabled.
+// [2k+1] = latest block end (atomicMax).  Null when disabled.  In constant memory: every kernel
+// tests it, and as a __device__ variable that test was a global load on the critical path of every
+// thread (ncu: the top stall of the proposal kernel, 9.7% of its samples; K1 after its barrier).
 constexpr int TL_W = 28, TL_ROWS = 4096;
-__device__ unsigned long long* g_tl = nullptr;
-__device__ const int* g_tl_steps = nullptr;
+__constant__ unsigned long long* g_tl = nullptr;
+__constant__ const int* g_tl_steps = nullptr;
 __device__ __forceinline__ void tl_start(int k) {
-  unsigned long long* tl = g_tl;
-  if (tl && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+    unsigned long long* tl = g_tl;
+    if (!tl) return;
     const int r = *g_tl_steps;
     if (r >= 0 && r < TL_ROWS) tl[r * TL_W + 2 * k] = gtimer();
   }
@@ -175,22 +178,25 @@ __device__ __forceinline__ void tl_mark_any(int slot) {  // calling thread: a ph
   }
 }
 __device__ __forceinline__ void tl_mark(int slot) {  // block (0,0) thread 0: a phase clock in slot 12..23
-  unsigned long long* tl = g_tl;
-  if (tl && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+    unsigned long long* tl = g_tl;
+    if (!tl) return;
     const int r = *g_tl_steps;
     if (r >= 0 && r < TL_ROWS) tl[r * TL_W + slot] = gtimer();
   }
 }
 __device__ __forceinline__ void tl_max(int slot) {  // thread 0 of every block: latest clock in slot 24..27
-  unsigned long long* tl = g_tl;
-  if (tl && threadIdx.x == 0) {
+  if (threadIdx.x == 0) {
+    unsigned long long* tl = g_tl;
+    if (!tl) return;
     const int r = *g_tl_steps;
     if (r >= 0 && r < TL_ROWS) atomicMax(&tl[r * TL_W + slot], gtimer());
   }
 }
 __device__ __forceinline__ void tl_end(int k) {
-  unsigned long long* tl = g_tl;
-  if (tl && threadIdx.x == 0) {
+  if (threadIdx.x == 0) {
+    unsigned long long* tl = g_tl;
+    if (!tl) return;
     const int r = *g_tl_steps;
     if (r >= 0 && r < TL_ROWS) atomicMax(&tl[r * TL_W + 2 * k + 1], gtimer());
   }
