@@ -244,15 +244,18 @@ __global__ void __launch_bounds__(4 * TILE, TILE == 32 ? 5 : 3) k_propose_rb(Dra
   };
   if (threadIdx.x == 0 && (int64_t)blockIdx.x < ntl) issue(blockIdx.x, 0);
   griddep_wait();  // the previous step's finalize: Lz, the stop flag, the step counter
-  if (early && a.stop && *a.stop) {  // speculative step after the stop: drain the loads, exit
-    if (threadIdx.x == 0 && (int64_t)blockIdx.x < ntl) mbar_wait(&bar[0], 0u);
-    return;
-  }
-  if (threadIdx.x == 0) {  // Lz, Rp (padded NP x KP) under their own barrier
-    const unsigned mb = (unsigned)(NP * KP * 8);
+  if (threadIdx.x == 0) {  // Lz, Rp (padded NP x KP) under their own barrier -- issued before the stop
+    const unsigned mb = (unsigned)(NP * KP * 8);  // flag is read, so that its load overlaps them
     mbar_arrive_expect_tx(&barL, 2 * mb);
     bulk_g2s(sL, a.Lz, mb, &barL);
     bulk_g2s(sS, a.Rp, mb, &barL);
+  }
+  if (early && a.stop && *a.stop) {  // speculative step after the stop: drain the loads, exit
+    if (threadIdx.x == 0) {
+      if ((int64_t)blockIdx.x < ntl) mbar_wait(&bar[0], 0u);
+      mbar_wait(&barL, 0u);
+    }
+    return;
   }
   if (a.set_step && blockIdx.x == 0 && threadIdx.x == 0) a.ctl->step_cur = a.step0 + (uint32_t)a.ctl->steps_done;
   if (a.set_step) tl_start(0);
