@@ -819,24 +819,23 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
   return y;
 }
 
-// Cholesky (lower) of the d x d SPD matrix held in shared memory as Ap (D x D,
-// identity-padded beyond d; D = round_up(d, 4) <= 32) by ONE warp, rows in
-// registers (lane i holds row i), columns fully unrolled: per column a 64-bit
-// shuffle of the pivot, rsqrt + 2 Newton steps, then the column through shared
-// memory for the trailing update (tools/chol_bench3.cu: ~250 cycles per column,
-// ~3x faster than run-time-loop shared-memory variants, whose row updates
-// serialize on shared-memory ordering).  One out-of-line copy per D serves
-// both factorization attempts (code size: this runs once per M step from a
-// cold instruction cache).  Writes the lower factor with row stride ldo >= D
-// (zeros above the diagonal and in the padding columns) for rows < d.
+// Cholesky (lower) of the d x d SPD matrix held in shared memory as Ap (row stride lda >= d;
+// entries beyond d unused) by ONE warp, rows in registers (lane i holds row i), columns fully
+// unrolled for D = d exactly (a round_up(d, 4) identity padding cost d = 25 three extra pivot steps):
+// per column a 64-bit shuffle of the pivot, rsqrt + 2 Newton steps, then the column through shared
+// memory for the trailing update (tools/chol_bench3.cu: ~250 cycles per column, ~3x faster than
+// run-time-loop shared-memory variants, whose row updates serialize on shared-memory ordering).  One
+// out-of-line copy per d serves both factorization attempts (code size: this runs once per M step
+// from a cold instruction cache).  Writes the lower factor with row stride ldo (zeros above the
+// diagonal) for rows and columns < d; the caller's padding of Lout stays as it is (zero).
 // Returns false if a pivot is not positive and finite.
 template <int D>
-__device__ __noinline__ bool warp_cholesky(const double* Ap, double* Lout, int ldo, int d) {
+__device__ __noinline__ bool warp_cholesky(const double* Ap, int lda, double* Lout, int ldo) {
   __shared__ double colbuf[32];
   const int lane = threadIdx.x & 31, row = lane < D ? lane : D - 1;
   double a[D];
 #pragma unroll
-  for (int l = 0; l < D; ++l) a[l] = Ap[row * D + l];
+  for (int l = 0; l < D; ++l) a[l] = Ap[row * lda + l];
   bool ok = true;
 #pragma unroll
   for (int j = 0; j < D; ++j) {
@@ -853,22 +852,21 @@ __device__ __noinline__ bool warp_cholesky(const double* Ap, double* Lout, int l
       __syncwarp();
     }
   }
-  if (lane < d)
+  if (lane < D)
 #pragma unroll
     for (int l = 0; l < D; ++l) Lout[lane * ldo + l] = l <= lane ? a[l] : 0.0;
   return ok;
 }
 
-__device__ bool warp_cholesky_d(const double* Ap, double* Lout, int ldo, int d) {
-  switch ((d + 3) >> 2) {
-    case 1: return warp_cholesky<4>(Ap, Lout, ldo, d);
-    case 2: return warp_cholesky<8>(Ap, Lout, ldo, d);
-    case 3: return warp_cholesky<12>(Ap, Lout, ldo, d);
-    case 4: return warp_cholesky<16>(Ap, Lout, ldo, d);
-    case 5: return warp_cholesky<20>(Ap, Lout, ldo, d);
-    case 6: return warp_cholesky<24>(Ap, Lout, ldo, d);
-    case 7: return warp_cholesky<28>(Ap, Lout, ldo, d);
-    default: return warp_cholesky<32>(Ap, Lout, ldo, d);
+__device__ bool warp_cholesky_d(const double* Ap, int lda, double* Lout, int ldo, int d) {
+  switch (d) {
+#define WCH(D_) \
+  case D_: return warp_cholesky<D_>(Ap, lda, Lout, ldo);
+    WCH(1) WCH(2) WCH(3) WCH(4) WCH(5) WCH(6) WCH(7) WCH(8) WCH(9) WCH(10) WCH(11) WCH(12) WCH(13) WCH(14)
+    WCH(15) WCH(16) WCH(17) WCH(18) WCH(19) WCH(20) WCH(21) WCH(22) WCH(23) WCH(24) WCH(25) WCH(26) WCH(27)
+    WCH(28) WCH(29) WCH(30) WCH(31)
+#undef WCH
+    default: return warp_cholesky<32>(Ap, lda, Lout, ldo);
   }
 }
 
@@ -1110,7 +1108,7 @@ __device__ void finalize_body(const FinArgs& f, double* sm) {
   if (f.mode == 1 && threadIdx.x == 0) tl_mark_any(18);
   const int ldp = round_up(d, 4);  // padded (DMMA) layout of the factor
   if (w == 0 && d <= 32) {         // chol((h/100) V), one ridge retry (R13)
-    bool ok = warp_cholesky_d(sA, f.Lprop, ldp, d);
+    bool ok = warp_cholesky_d(sA, ldc, f.Lprop, ldp, d);
     int ridge_used = 0;
     if (!ok) {
       double tr = 0.0;
@@ -1122,7 +1120,7 @@ __device__ void finalize_body(const FinArgs& f, double* sm) {
         for (int l = 0; l < d; ++l)
           sA[lane * ldc + l] = hd * (ridge_base(sV, sig, hd, lane * d + l) + (lane == l ? ridge : 0.0));
       __syncwarp();
-      ok = warp_cholesky_d(sA, f.Lprop, ldp, d);
+      ok = warp_cholesky_d(sA, ldc, f.Lprop, ldp, d);
       ridge_used = 1;
     }
     if (lane == 0) {
