@@ -217,6 +217,7 @@ struct sps_ctx {
   int plan_next = 0;
   Ctl* ctl = nullptr;
   Ctl* hctl = nullptr;  // pinned mirror
+  char* slab = nullptr;  // pooled pinned mapped slab holding hctl, hslot, hllbad
   // debug memory check (SPS_GUARD=1 at create): every device buffer between two guard zones
   struct Guard {
     char* base;
@@ -396,6 +397,32 @@ void dfree(sps_ctx* c, void* p, cudaStream_t s) {
       }
   }
   cudaFreeAsync(p, s);
+}
+
+// Pinned, mapped host slabs for a context's control mirrors ([hctl | hslot x 2 | hllbad x 2 | init
+// word]), pooled per process: cudaHostAlloc / cudaFreeHost cost milliseconds per context (cudaFreeHost
+// alone 4.5-6.4 ms in sps_destroy), which the end-to-end path (create, run, destroy per run) paid.
+constexpr size_t SLAB_CTL = (sizeof(Ctl) + 127) / 128 * 128;
+constexpr size_t SLAB_BYTES = 3 * SLAB_CTL + 128;
+std::mutex g_slab_mu;
+std::vector<char*> g_slabs;
+char* slab_get() {
+  {
+    std::lock_guard<std::mutex> lk(g_slab_mu);
+    if (!g_slabs.empty()) {
+      char* s = g_slabs.back();
+      g_slabs.pop_back();
+      return s;
+    }
+  }
+  char* s = nullptr;
+  if (cudaHostAlloc((void**)&s, SLAB_BYTES, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) return nullptr;
+  return s;
+}
+void slab_put(char* s) {
+  if (!s) return;
+  std::lock_guard<std::mutex> lk(g_slab_mu);
+  g_slabs.push_back(s);
 }
 
 int num_sms() {
@@ -1188,15 +1215,14 @@ void free_ctx(sps_ctx* c) {
                   c->sig_rec, c->sig_in, c->fu_tick, c->fu_tpart, c->oz_X, c->oz_T, c->oz_xamax};
   for (void* p : ptrs) dfree(c, p, fs);
   lap("cudaFree");
-  if (c->hctl) cudaFreeHost(c->hctl);
-  if (c->hslot) cudaFreeHost(c->hslot);
-  if (c->hllbad) cudaFreeHost(c->hllbad);
-  if (c->llbad) cudaFree(c->llbad);
+  dfree(c, c->llbad, fs);
   lap("freeHost");
   dfree(c, c->ticket, fs);
   if (c->trace) cudaFree(c->trace);  // managed
   dfree(c, c->tl, fs);
   cudaStreamSynchronize(fs);
+  slab_put(c->slab);  // (after the stream: no kernel of this context writes it any more)
+  c->slab = nullptr;
   for (cudaEvent_t e : c->evs)
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : c->prof_pool) cudaEventDestroy(e);
@@ -1430,16 +1456,19 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
     CU(c, cudaFuncSetAttribute(c->fu_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->fu_smem));
   }
   TRY(DALLOC(c, &c->Sinv, (size_t)d * d));
-  CU(c, cudaHostAlloc((void**)&c->hslot, 2 * sizeof(Ctl), cudaHostAllocMapped));
+  c->slab = slab_get();
+  if (!c->slab) return fail(c, SPS_E_CUDA, "cudaHostAlloc of the control slab failed");
+  std::memset(c->slab, 0, SLAB_BYTES);
+  c->hctl = reinterpret_cast<Ctl*>(c->slab);
+  c->hslot = reinterpret_cast<Ctl*>(c->slab + SLAB_CTL);
+  c->hllbad = reinterpret_cast<int*>(c->slab + 3 * SLAB_CTL);
+  int* hinit = c->hllbad + 2;  // staging word for the device-side llbad
   CU(c, cudaHostGetDevicePointer((void**)&c->dslot, c->hslot, 0));
-  TRY(DALLOC(c, &c->ticket, 1));
-  CU(c, cudaMalloc((void**)&c->llbad, sizeof(int)));
-  {
-    static const int none = 0x7fffffff;
-    CU(c, cudaMemcpy(c->llbad, &none, sizeof(int), cudaMemcpyHostToDevice));
-  }
-  CU(c, cudaHostAlloc((void**)&c->hllbad, 2 * sizeof(int), cudaHostAllocMapped));
   CU(c, cudaHostGetDevicePointer((void**)&c->dllbad, c->hllbad, 0));
+  TRY(DALLOC(c, &c->ticket, 1));
+  TRY(DALLOC(c, &c->llbad, 1));
+  *hinit = 0x7fffffff;
+  CU(c, cudaMemcpyAsync(c->llbad, hinit, sizeof(int), cudaMemcpyHostToDevice, c->stream));
   c->hllbad[0] = c->hllbad[1] = 0x7fffffff;
   if (getenv("SPS_TRACE")) CU(c, cudaMallocManaged((void**)&c->trace, 128 * sizeof(unsigned long long)));
   CU(c, cudaMemsetAsync(c->ticket, 0, sizeof(unsigned), c->stream));
@@ -1521,7 +1550,6 @@ sps_status sps_create(const sps_config* cfg_in, const double* X, const int32_t* 
     CU(c, cudaMemcpyToSymbolAsync(g_tl, &c->tl, sizeof(c->tl), 0, cudaMemcpyHostToDevice, c->stream));
     CU(c, cudaMemcpyToSymbolAsync(g_tl_steps, &steps, sizeof(steps), 0, cudaMemcpyHostToDevice, c->stream));
   }
-  CU(c, cudaMallocHost((void**)&c->hctl, sizeof(Ctl)));
   std::memset(c->hctl, 0, sizeof(Ctl));
   c->hctl->h = cfg.h_init;
   CU(c, cudaMemcpyAsync(c->ctl, c->hctl, sizeof(Ctl), cudaMemcpyHostToDevice, c->stream));
