@@ -311,7 +311,9 @@ def main():
     # FP64 pipe slots actually issued per pair: k FMA-equivalents (DMMA + remainder DFMA) + epilogue ops
     pipe_tflops = pairs_per_launch * 2 * (k * (WORKLOAD["C"] - 1) + EPILOGUE_DP_OPS_BINARY) / (k1_avg_ms * 1e-3) / 1e12
     traffic = None
-    tr_path = os.path.join(ROOT, "profiles", "r01_k1_ncu.json")
+    tr_path = os.path.join(ROOT, "profiles", "r02_k1_ncu.json")
+    if not os.path.exists(tr_path):
+        tr_path = os.path.join(ROOT, "profiles", "r01_k1_ncu.json")
     if os.path.exists(tr_path):
         traffic = json.load(open(tr_path)).get("dram_bytes_per_launch")
     k1_share = cnt["k1_ms"] / max(sum(times) / max(len(times), 1), 1e-9)
@@ -439,7 +441,7 @@ def main():
                          / FP64_PEAK_TFLOPS,
                          "frac_pipe_slots": pipe_tflops / FP64_PEAK_TFLOPS,
                          "peak_source": "measured FP64 DMMA rate, 37.07 TF/s (tools/fp64_peaks.cu, profiles/r01_fp64_peaks.json; "
-                                        "the DFMA epilogue shares the pipe); ncu: profiles/r01_k1_full_ncu_v12.txt, "
+                                        "the DFMA epilogue shares the pipe); ncu: profiles/r02_k1_ncu.json, profiles/r02_ncu_k1_hot.txt, "
                                         "profiles/r02_ncu_fused_vs_k1.txt",
                          "full_data_eval": {"ms": full_ms, "pairs_per_s": full_pairs_s,
                                             "frac": full_pairs_s * ops_per_pair / 1e12 / FP64_PEAK_TFLOPS}},
