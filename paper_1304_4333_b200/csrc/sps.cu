@@ -1267,6 +1267,15 @@ void sps_destroy(sps_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->cfg.device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  // guarded context (SPS_GUARD=1): verify the guard zones one last time; with SPS_GUARD_ABORT=1 an
+  // overwritten zone aborts the process (a whole test suite run under both checks every context)
+  if (ctx->guarded && !ctx->guards.empty() && ctx->stream) {
+    int64_t bad = 0;
+    if (sps_check_guards(ctx, &bad) == SPS_E_GUARD) {
+      fprintf(stderr, "SPS_GUARD: %s\n", ctx->err.c_str());
+      if (getenv("SPS_GUARD_ABORT") && atoi(getenv("SPS_GUARD_ABORT")) != 0) abort();
+    }
+  }
   free_ctx(ctx);
   delete ctx;
 }
