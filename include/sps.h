@@ -251,8 +251,9 @@ sps_status sps_shard(const sps_ctx* ctx, int64_t* P_local, int32_t* group0, int3
  * reads every zone back.  *n_corrupt (may be NULL) = overwritten guard bytes.  Returns SPS_OK,
  * SPS_E_GUARD (the last-error message names the first buffer and the byte offset relative to
  * its start: negative = before it, >= its size = past its end), or SPS_E_CONFIG if the context
- * was created without SPS_GUARD=1.  Test hook: SPS_GUARD_POKE=<buffer name, e.g. &c->theta>
- * writes 8 bytes past that buffer at create. */
+ * was created without SPS_GUARD=1.  sps_destroy repeats the check on a guarded context, reports a
+ * hit on stderr and, with SPS_GUARD_ABORT=1, aborts the process.  Test hook: SPS_GUARD_POKE=<buffer
+ * name, e.g. &c->theta> writes 8 bytes past that buffer at create. */
 sps_status sps_check_guards(sps_ctx* ctx, int64_t* n_corrupt);
 
 void sps_destroy(sps_ctx* ctx);
