@@ -415,8 +415,14 @@ char* slab_get() {
       return s;
     }
   }
+  // pool empty: one allocation carved into 16 slabs (the first context pays the host allocation for
+  // the next 15 -- e.g. the end-to-end contexts created beside a live one)
+  constexpr int NSLAB = 16;
   char* s = nullptr;
-  if (cudaHostAlloc((void**)&s, SLAB_BYTES, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) return nullptr;
+  if (cudaHostAlloc((void**)&s, NSLAB * SLAB_BYTES, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess)
+    return nullptr;
+  std::lock_guard<std::mutex> lk(g_slab_mu);
+  for (int q = NSLAB - 1; q >= 1; --q) g_slabs.push_back(s + (size_t)q * SLAB_BYTES);
   return s;
 }
 void slab_put(char* s) {
