@@ -1,3 +1,8 @@
+"""Host graph-build cost per fresh and reused context (cfg2): instantiation of the device-side M-phase
+loop graph on a new context vs executable-graph updates per M phase on a reused one.
+
+    python tools/graph_build_cost.py
+"""
 import os, sys, time
 import numpy as np
 sys.path.insert(0, '/root/repo')
